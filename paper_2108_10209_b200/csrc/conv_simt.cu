@@ -1,0 +1,420 @@
+// SIMT fp32 convolution kernels (forward, dgrad, wgrad) on NHWC activations.
+//
+// These restate the reference's fp32 conv (tensor.py:268-316: im2col + sgemm,
+// col2im scatter for the input gradient) as implicit GEMMs with no im2col
+// buffer.  They are the exact-fp32 path (fp32 products, fp32 accumulation in
+// a different order than OpenBLAS) used for the small-channel layers, for
+// the first layer (Cin = 1) and as the cross-check of the tcgen05 kernels.
+//
+//   forward : y[p][n] = epi( sum_{tap,c} x[p+d(tap)][c] * wk[n][tap][c] )
+//   dgrad   : same kernel with wk = dgrad-transposed weights
+//             wt[c][tap'][o] = w[o][8-tap'][c] and epi = ReLU mask of the
+//             layer input (model.py:101-113 feeds grad_in * (pre>0) back)
+//   wgrad   : dw[o][tap][c] = sum_p g[p][o] * x[p+d(tap)][c]  (deterministic
+//             split over pixels: partial sums per split, reduced in fixed order)
+#include "n2f_internal.cuh"
+
+namespace n2f {
+namespace {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// 3x3 implicit GEMM, M = pixels (BM = 128), N = output channels, K = 9 * C.
+// ---------------------------------------------------------------------------
+template <int BN, int TM, int TN>
+__global__ void __launch_bounds__(kThreads)
+    k_conv3x3(const float* __restrict__ x, const float* __restrict__ wk,
+              const float* __restrict__ bias, const float* __restrict__ mask,
+              float* __restrict__ y, int H, int W, int C, int N, int epi) {
+  constexpr int BM = 128, BK = 8, LDA = BM + 4, LDB = BN + 4;
+  static_assert((BM / TM) * (BN / TN) == kThreads, "thread tile");
+  __shared__ __align__(16) float As[2][BK][LDA];
+  __shared__ __align__(16) float Bs[2][BK][LDB];
+
+  const int tid = threadIdx.x;
+  const int P = H * W;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+
+  const int am = tid >> 1, ah = (tid & 1) * 4;
+  const int ap = m0 + am;
+  const bool avalid = ap < P;
+  const int ay = avalid ? ap / W : 0;
+  const int ax = avalid ? ap - ay * W : 0;
+  const int bn = tid >> 1, bh = (tid & 1) * 4;
+  const bool bload = bn < BN;
+  const int cpt = C / BK;
+  const int KB = 9 * cpt;
+
+  float4 ra = make_float4(0.f, 0.f, 0.f, 0.f), rb = ra;
+  auto load = [&](int kb) {
+    const int tap = kb / cpt;
+    const int c0 = (kb - tap * cpt) * BK;
+    const int ky = tap / 3, kx = tap - 3 * (tap / 3);
+    const int yy = ay + ky - 1, xx = ax + kx - 1;
+    if (avalid && yy >= 0 && yy < H && xx >= 0 && xx < W)
+      ra = __ldg(reinterpret_cast<const float4*>(x + (size_t)(yy * W + xx) * C + c0 + ah));
+    else
+      ra = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (bload)
+      rb = __ldg(reinterpret_cast<const float4*>(wk + (size_t)(n0 + bn) * 9 * C + tap * C + c0 + bh));
+  };
+  auto store = [&](int buf) {
+    As[buf][ah + 0][am] = ra.x;
+    As[buf][ah + 1][am] = ra.y;
+    As[buf][ah + 2][am] = ra.z;
+    As[buf][ah + 3][am] = ra.w;
+    if (bload) {
+      Bs[buf][bh + 0][bn] = rb.x;
+      Bs[buf][bh + 1][bn] = rb.y;
+      Bs[buf][bh + 2][bn] = rb.z;
+      Bs[buf][bh + 3][bn] = rb.w;
+    }
+  };
+
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+
+  load(0);
+  store(0);
+  __syncthreads();
+  for (int kb = 0; kb < KB; ++kb) {
+    const int cur = kb & 1;
+    if (kb + 1 < KB) load(kb + 1);
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; i += 4) {
+        float4 v = *reinterpret_cast<const float4*>(&As[cur][k][ty * TM + i]);
+        a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
+      }
+#pragma unroll
+      for (int j = 0; j < TN; j += 4) {
+        float4 v = *reinterpret_cast<const float4*>(&Bs[cur][k][tx * TN + j]);
+        b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (kb + 1 < KB) store(cur ^ 1);
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int p = m0 + ty * TM + i;
+    if (p >= P) continue;
+#pragma unroll
+    for (int j = 0; j < TN; j += 4) {
+      const int n = n0 + tx * TN + j;
+      float4 v = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+      if (epi == kEpiBiasRelu || epi == kEpiBias) {
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n));
+        v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
+        if (epi == kEpiBiasRelu) {
+          v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+        }
+      } else if (epi == kEpiMask) {
+        const float4 mk = __ldg(reinterpret_cast<const float4*>(mask + (size_t)p * N + n));
+        v.x = mk.x > 0.f ? v.x : 0.f;
+        v.y = mk.y > 0.f ? v.y : 0.f;
+        v.z = mk.z > 0.f ? v.z : 0.f;
+        v.w = mk.w > 0.f ? v.w : 0.f;
+      }
+      *reinterpret_cast<float4*>(y + (size_t)p * N + n) = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// First layer (Cin = 1): direct 3x3, one thread per (pixel, 4 output channels).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_conv_first(const float* __restrict__ x, const float* __restrict__ w,
+                 const float* __restrict__ b, float* __restrict__ y, int H, int W, int N, int relu) {
+  __shared__ float ws[kMaxC * 9];
+  __shared__ float bs[kMaxC];
+  for (int i = threadIdx.x; i < N * 9; i += blockDim.x) ws[i] = w[i];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) bs[i] = b[i];
+  __syncthreads();
+  const int nq = N / 4;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t P = (int64_t)H * W;
+  if (idx >= P * nq) return;
+  const int p = (int)(idx / nq);
+  const int q = (int)(idx - (int64_t)p * nq);
+  const int py = p / W, px = p - py * W;
+  float xv[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
+    xv[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + yy * W + xx) : 0.f;
+  }
+  float o[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int n = 4 * q + j;
+    float a = 0.f;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) a = fmaf(xv[t], ws[n * 9 + t], a);
+    o[j] = relu ? fmaxf(a + bs[n], 0.f) : a + bs[n];
+  }
+  *reinterpret_cast<float4*>(y + (size_t)p * N + 4 * q) = make_float4(o[0], o[1], o[2], o[3]);
+}
+
+// ---------------------------------------------------------------------------
+// wgrad: dw_part[s][o][k] = sum_{p in split s} g[p][o] * xg[p][k],  k = tap*C + c
+// BM over o, BN over k, BP pixels per pipeline stage.
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int TM, int TN>
+__global__ void __launch_bounds__(kThreads)
+    k_wgrad3x3(const float* __restrict__ g, const float* __restrict__ x, float* __restrict__ dw_part,
+               float* __restrict__ db_part, int H, int W, int C, int NO, int chunk) {
+  constexpr int BP = 8, LDG = BM + 4, LDX = BN + 4;
+  constexpr int NG4 = BP * BM / 4, NX4 = BP * BN / 4;
+  constexpr int PER = (NG4 + NX4 + kThreads - 1) / kThreads;
+  static_assert((BM / TM) * (BN / TN) == kThreads, "thread tile");
+  __shared__ __align__(16) float Gs[2][BP][LDG];
+  __shared__ __align__(16) float Xs[2][BP][LDX];
+
+  const int tid = threadIdx.x;
+  const int P = H * W, K = 9 * C;
+  const int o0 = blockIdx.x * BM, k0 = blockIdx.y * BN, s = blockIdx.z;
+  const int pbeg = s * chunk;
+  const int pend = min(P, pbeg + chunk);
+  const int nstage = (max(pend - pbeg, 0) + BP - 1) / BP;
+
+  float4 r[PER];
+  auto load = [&](int st) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int f = tid + u * kThreads;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (f < NG4) {
+        const int pp = f / (BM / 4), o4 = f - pp * (BM / 4);
+        const int p = pbeg + st * BP + pp;
+        if (p < pend) v = __ldg(reinterpret_cast<const float4*>(g + (size_t)p * NO + o0 + 4 * o4));
+      } else if (f < NG4 + NX4) {
+        const int e = f - NG4;
+        const int pp = e / (BN / 4), k4 = e - pp * (BN / 4);
+        const int p = pbeg + st * BP + pp;
+        const int k = k0 + 4 * k4;
+        if (p < pend && k < K) {
+          const int tap = k / C, c = k - tap * C;
+          const int py = p / W, px = p - py * W;
+          const int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
+          if (yy >= 0 && yy < H && xx >= 0 && xx < W)
+            v = __ldg(reinterpret_cast<const float4*>(x + (size_t)(yy * W + xx) * C + c));
+        }
+      }
+      r[u] = v;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int f = tid + u * kThreads;
+      if (f < NG4) {
+        const int pp = f / (BM / 4), o4 = f - pp * (BM / 4);
+        *reinterpret_cast<float4*>(&Gs[buf][pp][4 * o4]) = r[u];
+      } else if (f < NG4 + NX4) {
+        const int e = f - NG4;
+        const int pp = e / (BN / 4), k4 = e - pp * (BN / 4);
+        *reinterpret_cast<float4*>(&Xs[buf][pp][4 * k4]) = r[u];
+      }
+    }
+  };
+
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  float acc[TM][TN];
+  float bacc[TM];
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    bacc[i] = 0.f;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.f;
+  }
+  const bool do_bias = (blockIdx.y == 0) && (tx == 0) && (db_part != nullptr);
+
+  if (nstage > 0) {
+    load(0);
+    store(0);
+  }
+  __syncthreads();
+  for (int st = 0; st < nstage; ++st) {
+    const int cur = st & 1;
+    if (st + 1 < nstage) load(st + 1);
+#pragma unroll
+    for (int pp = 0; pp < BP; ++pp) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; i += 4) {
+        float4 v = *reinterpret_cast<const float4*>(&Gs[cur][pp][ty * TM + i]);
+        a[i] = v.x; a[i + 1] = v.y; a[i + 2] = v.z; a[i + 3] = v.w;
+      }
+#pragma unroll
+      for (int j = 0; j < TN; j += 4) {
+        float4 v = *reinterpret_cast<const float4*>(&Xs[cur][pp][tx * TN + j]);
+        b[j] = v.x; b[j + 1] = v.y; b[j + 2] = v.z; b[j + 3] = v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        if (do_bias) bacc[i] += a[i];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+    }
+    if (st + 1 < nstage) store(cur ^ 1);
+    __syncthreads();
+  }
+
+  float* dst = dw_part + (size_t)s * NO * K;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int o = o0 + ty * TM + i;
+#pragma unroll
+    for (int j = 0; j < TN; j += 4) {
+      const int k = k0 + tx * TN + j;
+      if (k < K)
+        *reinterpret_cast<float4*>(dst + (size_t)o * K + k) =
+            make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+    }
+    if (do_bias) db_part[(size_t)s * NO + o] = bacc[i];
+  }
+}
+
+// First-layer wgrad (Cin = 1): dw[o][tap], db[o]; 8 pixel lanes x 32 channels.
+__global__ void __launch_bounds__(kThreads)
+    k_wgrad_first(const float* __restrict__ g, const float* __restrict__ x,
+                  float* __restrict__ dw_part, float* __restrict__ db_part, int H, int W, int NO,
+                  int chunk) {
+  // blockDim = 256 = (256/NO) lanes x NO channels; NO == 32 in the network.
+  __shared__ float red[kThreads][10];
+  const int o = threadIdx.x % NO, lane = threadIdx.x / NO, nl = blockDim.x / NO;
+  const int s = blockIdx.x;
+  const int P = H * W;
+  const int pbeg = s * chunk, pend = min(P, pbeg + chunk);
+  float acc[10];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) acc[t] = 0.f;
+  for (int p = pbeg + lane; p < pend; p += nl) {
+    const float gv = __ldg(g + (size_t)p * NO + o);
+    const int py = p / W, px = p - py * W;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
+      const float xv = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + yy * W + xx) : 0.f;
+      acc[t] = fmaf(gv, xv, acc[t]);
+    }
+    acc[9] += gv;
+  }
+#pragma unroll
+  for (int t = 0; t < 10; ++t) red[threadIdx.x][t] = acc[t];
+  __syncthreads();
+  if (lane == 0) {
+    for (int l = 1; l < nl; ++l)
+#pragma unroll
+      for (int t = 0; t < 10; ++t) acc[t] += red[l * NO + o][t];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) dw_part[(size_t)s * NO * 9 + o * 9 + t] = acc[t];
+    db_part[(size_t)s * NO + o] = acc[9];
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+int conv3x3_simt(const float* x, const float* wk, const float* bias, const float* mask, float* y,
+                 int h, int w, int cin, int cout, int epi, cudaStream_t st) {
+  if (cin % 8 || cout % 32) return fail(N2F_ERR_ARG, "conv3x3_simt: cin %d cout %d", cin, cout);
+  const int P = h * w;
+  dim3 block(kThreads);
+  if (cout % 128 == 0) {
+    dim3 grid((P + 127) / 128, cout / 128);
+    k_conv3x3<128, 8, 8><<<grid, block, 0, st>>>(x, wk, bias, mask, y, h, w, cin, cout, epi);
+  } else if (cout % 64 == 0) {
+    dim3 grid((P + 127) / 128, cout / 64);
+    k_conv3x3<64, 8, 4><<<grid, block, 0, st>>>(x, wk, bias, mask, y, h, w, cin, cout, epi);
+  } else {
+    dim3 grid((P + 127) / 128, cout / 32);
+    k_conv3x3<32, 4, 4><<<grid, block, 0, st>>>(x, wk, bias, mask, y, h, w, cin, cout, epi);
+  }
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
+                    int cout, cudaStream_t st, int relu) {
+  if (cout % 4 || cout > kMaxC) return fail(N2F_ERR_ARG, "conv_first: cout %d", cout);
+  const int64_t total = (int64_t)h * w_ * (cout / 4);
+  k_conv_first<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, st>>>(x, w, b, y, h,
+                                                                                  w_, cout, relu);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+// wgrad CTA tile (over cout x 9*cin) for a layer
+static void wgrad_tile(int cout, int* bm, int* bn) {
+  if (cout % 128 == 0) { *bm = 128; *bn = 128; }
+  else if (cout % 64 == 0) { *bm = 64; *bn = 64; }
+  else { *bm = 32; *bn = 128; }
+}
+
+int wgrad_nsplit(int64_t pixels, int cin, int cout) {
+  // aim for ~4 waves of 256-thread CTAs over 148 SMs, >= 512 pixels per split
+  int bm, bn;
+  wgrad_tile(cout, &bm, &bn);
+  const int64_t tiles =
+      (cin == 1) ? 1 : (int64_t)((cout + bm - 1) / bm) * ((9 * cin + bn - 1) / bn);
+  int64_t want = (4 * 148 + tiles - 1) / tiles;
+  int64_t maxs = (pixels + 511) / 512;
+  int64_t n = want < maxs ? want : maxs;
+  if (n < 1) n = 1;
+  if (n > 1024) n = 1024;
+  return (int)n;
+}
+
+int wgrad3x3_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
+                  int cin, int cout, int nsplit, cudaStream_t st) {
+  const int P = h * w;
+  int chunk = (P + nsplit - 1) / nsplit;
+  chunk = (chunk + 7) / 8 * 8;
+  const int K = 9 * cin;
+  if (cin % 4 || cout % 32) return fail(N2F_ERR_ARG, "wgrad3x3_simt: cin %d cout %d", cin, cout);
+  int bm, bn;
+  wgrad_tile(cout, &bm, &bn);
+  dim3 grid(cout / bm, (K + bn - 1) / bn, nsplit);
+  if (bm == 128)
+    k_wgrad3x3<128, 128, 8, 8><<<grid, kThreads, 0, st>>>(g, x, dw_part, db_part, h, w, cin, cout,
+                                                          chunk);
+  else if (bm == 64)
+    k_wgrad3x3<64, 64, 4, 4><<<grid, kThreads, 0, st>>>(g, x, dw_part, db_part, h, w, cin, cout,
+                                                        chunk);
+  else
+    k_wgrad3x3<32, 128, 4, 4><<<grid, kThreads, 0, st>>>(g, x, dw_part, db_part, h, w, cin, cout,
+                                                         chunk);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int wgrad_first_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
+                     int cout, int nsplit, cudaStream_t st) {
+  if (kThreads % cout) return fail(N2F_ERR_ARG, "wgrad_first: cout %d", cout);
+  const int P = h * w;
+  const int chunk = (P + nsplit - 1) / nsplit;
+  k_wgrad_first<<<nsplit, kThreads, 0, st>>>(g, x, dw_part, db_part, h, w, cout, chunk);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+}  // namespace n2f

@@ -1,0 +1,637 @@
+// The per-image fit-and-denoise engine: context (workspaces sized once per
+// image shape), one training epoch as a fixed kernel sequence, the whole loop
+// as ONE CUDA graph with a device-driven while node, and the C-ABI entry
+// points of include/n2f.h that drive it.
+//
+// Hot path restated (reference trainer.py:125-213):
+//   normalise + 4 training pairs        -> prep.cu (bit-exact)
+//   build_network (He-uniform, seeded)   -> prep.cu k_init_layer (bit-exact)
+//   per epoch: 4 x [fwd L1..L8, fused head+loss+head-bwd, wgrad/dgrad L8..L1,
+//              Adam], full-res validation fwd + head, stop-state update
+//   finalize: window mean + denormalise  -> train.cu k_window_mean (bit-exact)
+#include <math.h>
+#include <string.h>
+
+#include <vector>
+
+#include "n2f_internal.cuh"
+#include "train.cuh"
+
+using namespace n2f;
+
+struct n2f_ctx {
+  int device = 0;
+  int H = 0, W = 0;
+  n2f_config cfg{};
+  cudaStream_t stream = nullptr;
+  int impl = kImplSimt;
+
+  // geometry
+  int ph[4]{}, pw[4]{};
+  int64_t plane = 0;  // elements of one training plane
+  int64_t Pt = 0;     // pixels per training pair (identical for the 4 pairs)
+  int64_t Pv = 0;     // validation pixels (H*W)
+
+  // device buffers
+  std::vector<void*> allocs;
+  size_t bytes = 0;
+  void* img = nullptr;    // staging input (H*W f64)
+  void* clean = nullptr;  // staging clean image (exact scheme)
+  double* mm = nullptr;   // {vmin, vmax, nonfinite}
+  double* mm_part = nullptr;
+  float* norm = nullptr;  // H*W f32
+  float* pin = nullptr;   // 4 planes
+  float* ptgt = nullptr;  // 4 planes
+  float* params = nullptr;
+  float* m = nullptr;
+  float* v = nullptr;
+  int64_t poff[2 * kLayers]{};  // tensor offsets in the arena (w0,b0,w1,b1,...)
+  int64_t pnum[2 * kLayers]{};
+  int64_t ptotal = 0;
+  float* wt[kLayers]{};  // dgrad-transposed weights (layers 1..7)
+  float* act[kLayers]{};  // outputs of layers 0..7 for the training pass
+  float* z = nullptr;     // logits of the last training step
+  float* gA = nullptr;
+  float* gB = nullptr;
+  float* vA = nullptr;
+  float* vB = nullptr;
+  float* ring = nullptr;
+  int nsplit[kLayers]{};
+  float* part_w[kLayers]{};
+  float* part_b[kLayers]{};
+  int nblk_head = 0, nblk_val = 0;
+  double* part_loss = nullptr;  // [4][nblk_head]
+  double* part_se = nullptr;    // [nblk_val]
+  DevState* dstate = nullptr;
+  int* step_counter = nullptr;
+  double* val_hist = nullptr;
+  double* loss_hist = nullptr;
+  unsigned long long* time_hist = nullptr;
+  float* bc1 = nullptr;
+  float* bc2 = nullptr;
+  int table_len = 0;
+  double* out_stage = nullptr;  // H*W f64 for the host API
+
+  // host pinned mirrors
+  double* h_mm = nullptr;
+  DevState* h_state = nullptr;
+
+  // graph
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphConditionalHandle handle = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  AdamArgs adam{};
+};
+
+namespace {
+
+template <typename T>
+int dalloc(n2f_ctx* c, T** p, size_t count) {
+  void* q = nullptr;
+  const size_t b = count * sizeof(T);
+  N2F_CUDA(cudaMalloc(&q, b < 16 ? 16 : b));
+  c->allocs.push_back(q);
+  c->bytes += b;
+  *p = reinterpret_cast<T*>(q);
+  return N2F_OK;
+}
+
+int nblocks_for(int64_t pixels, int per_block) {
+  int64_t n = (pixels + per_block - 1) / per_block;
+  if (n > 148 * 8) n = 148 * 8;
+  if (n < 1) n = 1;
+  return (int)n;
+}
+
+const float* W_(n2f_ctx* c, int li) { return c->params + c->poff[2 * li]; }
+const float* B_(n2f_ctx* c, int li) { return c->params + c->poff[2 * li + 1]; }
+
+int conv3x3(n2f_ctx* c, const float* x, const float* wk, const float* bias, const float* mask,
+            float* y, int h, int w, int cin, int cout, int epi) {
+  return conv3x3_simt(x, wk, bias, mask, y, h, w, cin, cout, epi, c->stream);
+}
+
+// One training step on pair k: forward, fused head/loss/head-backward,
+// backward through L8..L1 (wgrad partials + masked dgrad), Adam.
+int enqueue_step(n2f_ctx* c, int k) {
+  cudaStream_t st = c->stream;
+  const int h = c->ph[k], w = c->pw[k];
+  const int64_t P = (int64_t)h * w;
+  const float* x0 = c->pin + k * c->plane;
+  const float* tgt = c->ptgt + k * c->plane;
+  N2F_TRY(conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st));
+  for (int li = 1; li < 8; ++li)
+    N2F_TRY(conv3x3(c, c->act[li - 1], W_(c, li), B_(c, li), nullptr, c->act[li], h, w, kCin[li],
+                    kCout[li], kEpiBiasRelu));
+  N2F_TRY(launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, c->gA, c->part_w[8], c->part_b[8],
+                            c->part_loss + (int64_t)k * c->nblk_head, c->z, P, c->nblk_head,
+                            c->cfg.loss, c->step_counter, st));
+  float* g = c->gA;
+  float* gn = c->gB;
+  for (int li = 7; li >= 1; --li) {
+    N2F_TRY(wgrad3x3_simt(g, c->act[li - 1], c->part_w[li], c->part_b[li], h, w, kCin[li],
+                          kCout[li], c->nsplit[li], st));
+    N2F_TRY(conv3x3(c, g, c->wt[li], nullptr, c->act[li - 1], gn, h, w, kCout[li], kCin[li],
+                    kEpiMask));
+    float* t = g;
+    g = gn;
+    gn = t;
+  }
+  N2F_TRY(wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
+  N2F_TRY(launch_adam(c->adam, c->step_counter, 0, st));
+  return N2F_OK;
+}
+
+// Full-resolution validation forward + head (writes the ring slot + se partials).
+int enqueue_validate(n2f_ctx* c) {
+  cudaStream_t st = c->stream;
+  const int h = c->H, w = c->W;
+  N2F_TRY(conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, h, w, kCout[0], st));
+  float* a = c->vA;
+  float* b = c->vB;
+  for (int li = 1; li < 8; ++li) {
+    N2F_TRY(conv3x3(c, a, W_(c, li), B_(c, li), nullptr, b, h, w, kCin[li], kCout[li], kEpiBiasRelu));
+    float* t = a;
+    a = b;
+    b = t;
+  }
+  N2F_TRY(launch_head_val(a, W_(c, 8), B_(c, 8), c->norm, c->ring, c->Pv, c->nblk_val, c->dstate,
+                          c->cfg.avg_window, c->part_se, st));
+  return N2F_OK;
+}
+
+int enqueue_epoch(n2f_ctx* c, int use_handle) {
+  for (int k = 0; k < 4; ++k) N2F_TRY(enqueue_step(c, k));
+  N2F_TRY(enqueue_validate(c));
+  const double pt[4] = {(double)c->Pt, (double)c->Pt, (double)c->Pt, (double)c->Pt};
+  N2F_TRY(launch_stop(c->dstate, c->part_se, c->nblk_val, (double)c->Pv, c->part_loss,
+                      c->nblk_head, pt, c->val_hist, c->loss_hist, c->time_hist,
+                      c->cfg.patience_epochs, c->cfg.max_epochs, c->handle, use_handle, c->stream));
+  return N2F_OK;
+}
+
+int build_graph(n2f_ctx* c) {
+  N2F_CUDA(cudaGraphCreate(&c->graph, 0));
+  N2F_CUDA(cudaGraphConditionalHandleCreate(&c->handle, c->graph, 1, cudaGraphCondAssignDefault));
+  // cudaGraphNodeParams has a deleted default constructor (union member);
+  // build it in zeroed raw storage.
+  alignas(cudaGraphNodeParams) unsigned char raw[sizeof(cudaGraphNodeParams)];
+  memset(raw, 0, sizeof raw);
+  cudaGraphNodeParams& cp = *reinterpret_cast<cudaGraphNodeParams*>(raw);
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = c->handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  N2F_CUDA(cudaGraphAddNode(&node, c->graph, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  N2F_CUDA(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+  int s = enqueue_epoch(c, 1);
+  cudaGraph_t captured = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &captured);
+  if (s != N2F_OK) return s;
+  N2F_CUDA(e);
+  N2F_CUDA(cudaGraphInstantiate(&c->exec, c->graph, 0));
+  return N2F_OK;
+}
+
+int setup(n2f_ctx* c) {
+  N2F_CUDA(cudaSetDevice(c->device));
+  N2F_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  N2F_CUDA(cudaEventCreate(&c->ev0));
+  N2F_CUDA(cudaEventCreate(&c->ev1));
+  const int H = c->H, W = c->W;
+  const int He = H & ~1, We = W & ~1;
+  if (c->cfg.scheme == 1) {
+    for (int k = 0; k < 4; ++k) { c->ph[k] = He / 2; c->pw[k] = We / 2; }
+    c->plane = (int64_t)(He / 2) * (We / 2);
+  } else {
+    c->ph[0] = c->ph[1] = He; c->pw[0] = c->pw[1] = We / 2;
+    c->ph[2] = c->ph[3] = He / 2; c->pw[2] = c->pw[3] = We;
+    c->plane = (int64_t)He * (We / 2);
+  }
+  c->Pt = c->plane;
+  c->Pv = (int64_t)H * W;
+
+  N2F_TRY(dalloc(c, reinterpret_cast<double**>(&c->img), c->Pv));
+  if (c->cfg.scheme == 2) N2F_TRY(dalloc(c, reinterpret_cast<double**>(&c->clean), c->Pv));
+  N2F_TRY(dalloc(c, &c->mm, 4));
+  N2F_TRY(dalloc(c, &c->mm_part, minmax_scratch_doubles()));
+  N2F_TRY(dalloc(c, &c->norm, c->Pv));
+  N2F_TRY(dalloc(c, &c->pin, 4 * c->plane));
+  N2F_TRY(dalloc(c, &c->ptgt, 4 * c->plane));
+
+  int64_t off = 0;
+  for (int li = 0; li < kLayers; ++li) {
+    c->poff[2 * li] = off;
+    c->pnum[2 * li] = (int64_t)kCout[li] * kKsz[li] * kKsz[li] * kCin[li];
+    off += c->pnum[2 * li];
+    c->poff[2 * li + 1] = off;
+    c->pnum[2 * li + 1] = kCout[li];
+    off += kCout[li];
+  }
+  c->ptotal = off;
+  N2F_TRY(dalloc(c, &c->params, off));
+  N2F_TRY(dalloc(c, &c->m, off));
+  N2F_TRY(dalloc(c, &c->v, off));
+  for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt[li], c->pnum[2 * li]));
+  for (int li = 0; li < 8; ++li) N2F_TRY(dalloc(c, &c->act[li], c->Pt * kCout[li]));
+  N2F_TRY(dalloc(c, &c->z, c->Pt));
+  N2F_TRY(dalloc(c, &c->gA, c->Pt * kMaxC));
+  N2F_TRY(dalloc(c, &c->gB, c->Pt * kMaxC));
+  N2F_TRY(dalloc(c, &c->vA, c->Pv * kMaxC));
+  N2F_TRY(dalloc(c, &c->vB, c->Pv * kMaxC));
+  N2F_TRY(dalloc(c, &c->ring, (int64_t)c->cfg.avg_window * c->Pv));
+
+  c->nblk_head = nblocks_for(c->Pt, 64);
+  c->nblk_val = nblocks_for(c->Pv, 64);
+  for (int li = 0; li < 8; ++li) c->nsplit[li] = wgrad_nsplit(c->Pt, kCin[li], kCout[li]);
+  c->nsplit[8] = c->nblk_head;
+  for (int li = 0; li < kLayers; ++li) {
+    N2F_TRY(dalloc(c, &c->part_w[li], (int64_t)c->nsplit[li] * c->pnum[2 * li]));
+    N2F_TRY(dalloc(c, &c->part_b[li], (int64_t)c->nsplit[li] * c->pnum[2 * li + 1]));
+  }
+  N2F_TRY(dalloc(c, &c->part_loss, 4 * (int64_t)c->nblk_head));
+  N2F_TRY(dalloc(c, &c->part_se, c->nblk_val));
+  N2F_TRY(dalloc(c, &c->dstate, 1));
+  N2F_TRY(dalloc(c, &c->step_counter, 1));
+  N2F_TRY(dalloc(c, &c->val_hist, c->cfg.max_epochs));
+  N2F_TRY(dalloc(c, &c->loss_hist, 4 * (int64_t)c->cfg.max_epochs));
+  N2F_TRY(dalloc(c, &c->time_hist, c->cfg.max_epochs));
+  N2F_TRY(dalloc(c, &c->out_stage, c->Pv));
+
+  // Adam bias-correction table: fl32(1 - beta^t) with Python's pow semantics;
+  // beyond ~17.3k steps both saturate to 1.0f, so the table is capped.
+  int64_t steps = 4 * (int64_t)c->cfg.max_epochs;
+  c->table_len = (int)(steps < 32768 ? steps : 32768);
+  std::vector<float> t1(c->table_len), t2(c->table_len);
+  for (int t = 1; t <= c->table_len; ++t) {
+    t1[t - 1] = (float)(1.0 - pow(0.9, (double)t));
+    t2[t - 1] = (float)(1.0 - pow(0.999, (double)t));
+  }
+  if (steps > c->table_len && (t1.back() != 1.0f || t2.back() != 1.0f))
+    return fail(N2F_ERR_ARG, "bias-correction table did not saturate");
+  N2F_TRY(dalloc(c, &c->bc1, c->table_len));
+  N2F_TRY(dalloc(c, &c->bc2, c->table_len));
+  N2F_CUDA(cudaMemcpy(c->bc1, t1.data(), t1.size() * 4, cudaMemcpyHostToDevice));
+  N2F_CUDA(cudaMemcpy(c->bc2, t2.data(), t2.size() * 4, cudaMemcpyHostToDevice));
+
+  AdamArgs& a = c->adam;
+  a.ntensors = 2 * kLayers;
+  a.total = c->ptotal;
+  a.p = c->params;
+  a.m = c->m;
+  a.v = c->v;
+  a.bc1 = c->bc1;
+  a.bc2 = c->bc2;
+  a.table_len = c->table_len;
+  a.beta1 = 0.9f;
+  a.one_minus_beta1 = (float)(1.0 - 0.9);
+  a.beta2 = 0.999f;
+  a.one_minus_beta2 = (float)(1.0 - 0.999);
+  a.lr = (float)c->cfg.lr;
+  a.eps = 1e-8f;
+  for (int li = 0; li < kLayers; ++li) {
+    for (int q = 0; q < 2; ++q) {
+      AdamTensor& T = a.t[2 * li + q];
+      T.off = c->poff[2 * li + q];
+      T.n = c->pnum[2 * li + q];
+      T.part = q == 0 ? c->part_w[li] : c->part_b[li];
+      T.nsplit = c->nsplit[li];
+      T.wt = (q == 0 && li >= 1 && li <= 7) ? c->wt[li] : nullptr;
+      T.cin = kCin[li];
+      T.cout = kCout[li];
+    }
+  }
+
+  N2F_CUDA(cudaMallocHost(&c->h_mm, 4 * sizeof(double)));
+  N2F_CUDA(cudaMallocHost(&c->h_state, sizeof(DevState)));
+  if (c->cfg.use_graph) N2F_TRY(build_graph(c));
+  return N2F_OK;
+}
+
+// minmax + checks; returns N2F_OK and sets *degenerate
+int prepare_input(n2f_ctx* c, const void* image, int dtype, const void* clean, int* degenerate) {
+  cudaStream_t st = c->stream;
+  N2F_TRY(launch_minmax(image, dtype, c->Pv, c->mm_part, c->mm, st));
+  N2F_CUDA(cudaMemcpyAsync(c->h_mm, c->mm, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  N2F_CUDA(cudaStreamSynchronize(st));
+  if (c->h_mm[2] != 0.0) return fail(N2F_ERR_NONFINITE, "image contains non-finite values");
+  *degenerate = c->h_mm[0] == c->h_mm[1];
+  if (*degenerate) return N2F_OK;
+  N2F_TRY(launch_pairs(image, dtype, clean, c->mm, c->H, c->W, c->cfg.scheme, c->cfg.loss == 0,
+                       c->norm, c->pin, c->ptgt, c->plane, st));
+  return N2F_OK;
+}
+
+// Derived operand copies of the weights (dgrad-transposed layouts).  Adam
+// keeps them current after every step; this refreshes them after init/set.
+int refresh_derived(n2f_ctx* c) {
+  for (int li = 1; li < 8; ++li)
+    N2F_TRY(transpose_dgrad_weights(c->params + c->poff[2 * li], c->wt[li], kCin[li], kCout[li],
+                                    c->stream));
+  return N2F_OK;
+}
+
+int init_network(n2f_ctx* c) {
+  cudaStream_t st = c->stream;
+  for (int li = 0; li < kLayers; ++li)
+    N2F_TRY(launch_init_layer(c->cfg.seed, li, kCin[li], kCout[li], kKsz[li],
+                              c->params + c->poff[2 * li], st));
+  for (int li = 0; li < kLayers; ++li)
+    N2F_CUDA(cudaMemsetAsync(c->params + c->poff[2 * li + 1], 0, c->pnum[2 * li + 1] * 4, st));
+  N2F_TRY(refresh_derived(c));
+  N2F_CUDA(cudaMemsetAsync(c->m, 0, c->ptotal * 4, st));
+  N2F_CUDA(cudaMemsetAsync(c->v, 0, c->ptotal * 4, st));
+  N2F_CUDA(cudaMemsetAsync(c->step_counter, 0, sizeof(int), st));
+  N2F_TRY(launch_reset_state(c->dstate, st));
+  return N2F_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+namespace {
+
+__global__ void k_to_f64(const void* __restrict__ src, int dtype, int64_t n, double* __restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = dtype == N2F_F64 ? reinterpret_cast<const double*>(src)[i]
+                              : (double)reinterpret_cast<const float*>(src)[i];
+}
+
+size_t dtype_size(int dtype) { return dtype == N2F_F64 ? 8 : 4; }
+
+int check_cfg(const n2f_config* cfg) {
+  if (!cfg) return fail(N2F_ERR_ARG, "null config");
+  if (cfg->loss != 0 && cfg->loss != 1) return fail(N2F_ERR_ARG, "loss must be bce(0) or mse(1)");
+  if (cfg->scheme < 0 || cfg->scheme > 2) return fail(N2F_ERR_ARG, "scheme must be 0..2");
+  if (!(cfg->lr > 0)) return fail(N2F_ERR_ARG, "lr must be > 0");
+  if (cfg->patience_epochs < 1) return fail(N2F_ERR_ARG, "patience_epochs must be >= 1");
+  if (cfg->avg_window < 1) return fail(N2F_ERR_ARG, "avg_window must be >= 1");
+  if (cfg->max_epochs < 1) return fail(N2F_ERR_ARG, "max_epochs must be >= 1");
+  return N2F_OK;
+}
+
+int run_loop(n2f_ctx* c) {
+  if (c->cfg.use_graph) {
+    N2F_CUDA(cudaGraphLaunch(c->exec, c->stream));
+    return N2F_OK;
+  }
+  for (int e = 0; e < c->cfg.max_epochs; ++e) {
+    N2F_TRY(enqueue_epoch(c, 0));
+    N2F_CUDA(cudaMemcpyAsync(c->h_state, c->dstate, sizeof(DevState), cudaMemcpyDeviceToHost,
+                             c->stream));
+    N2F_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->h_state->stopped) break;
+  }
+  return N2F_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* n2f_last_error(void) {
+  return error_text().c_str();
+}
+
+const char* n2f_version(void) { return "n2f-b200 0.1 (sm_100a)"; }
+
+int n2f_create(int device, int height, int width, const n2f_config* cfg, n2f_ctx** out) {
+  if (!out) return fail(N2F_ERR_ARG, "null out");
+  *out = nullptr;
+  N2F_TRY(check_cfg(cfg));
+  if (height < 4 || width < 4)
+    return fail(N2F_ERR_ARG, "image must be at least 4x4, got (%d, %d)", height, width);
+  if (cfg->conv_impl == kImplTc) return fail(N2F_ERR_UNSUPPORTED, "tcgen05 conv path not built yet");
+  n2f_ctx* c = new n2f_ctx();
+  c->device = device;
+  c->H = height;
+  c->W = width;
+  c->cfg = *cfg;
+  int s = setup(c);
+  if (s != N2F_OK) {
+    n2f_destroy(c);
+    return s;
+  }
+  *out = c;
+  return N2F_OK;
+}
+
+int n2f_destroy(n2f_ctx* c) {
+  if (!c) return N2F_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->h_mm) cudaFreeHost(c->h_mm);
+  if (c->h_state) cudaFreeHost(c->h_state);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return N2F_OK;
+}
+
+void* n2f_ctx_stream(n2f_ctx* c) { return c ? (void*)c->stream : nullptr; }
+size_t n2f_ctx_device_bytes(n2f_ctx* c) { return c ? c->bytes : 0; }
+
+int n2f_fit_denoise_dev(n2f_ctx* c, const void* image, int dtype, const void* clean, double* out,
+                        n2f_result* res) {
+  if (!c || !image || !out || !res) return fail(N2F_ERR_ARG, "null argument");
+  if (dtype != N2F_F32 && dtype != N2F_F64) return fail(N2F_ERR_ARG, "dtype");
+  if (c->cfg.scheme == 2 && !clean)
+    return fail(N2F_ERR_ARG, "the exact scheme requires the clean ground-truth image");
+  N2F_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  N2F_CUDA(cudaEventRecord(c->ev0, st));
+  int degenerate = 0;
+  N2F_TRY(prepare_input(c, image, dtype, clean, &degenerate));
+  res->vmin = c->h_mm[0];
+  res->vmax = c->h_mm[1];
+  if (degenerate) {
+    k_to_f64<<<256, 256, 0, st>>>(image, dtype, c->Pv, out);
+    N2F_LAUNCH_CHECK();
+    N2F_CUDA(cudaEventRecord(c->ev1, st));
+    N2F_CUDA(cudaStreamSynchronize(st));
+    res->epochs_run = 0;
+    res->stop_reason = N2F_STOP_DEGENERATE;
+    res->best_score = INFINITY;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    res->gpu_ms = ms;
+    return N2F_OK;
+  }
+  N2F_TRY(init_network(c));
+  N2F_TRY(run_loop(c));
+  N2F_TRY(launch_window_mean(c->ring, c->Pv, c->cfg.avg_window, c->dstate, 0, 0, c->mm, 0, 0, out,
+                             st));
+  N2F_CUDA(cudaEventRecord(c->ev1, st));
+  N2F_CUDA(cudaMemcpyAsync(c->h_state, c->dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  N2F_CUDA(cudaStreamSynchronize(st));
+  const int ne = c->h_state->epoch;
+  res->epochs_run = ne;
+  res->stop_reason = c->h_state->stop_reason;
+  res->best_score = c->h_state->best;
+  if (res->val_history)
+    N2F_CUDA(cudaMemcpy(res->val_history, c->val_hist, ne * sizeof(double), cudaMemcpyDeviceToHost));
+  if (res->train_loss)
+    N2F_CUDA(cudaMemcpy(res->train_loss, c->loss_hist, 4 * ne * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+  if (res->epoch_seconds && ne > 0) {
+    std::vector<unsigned long long> t(ne);
+    N2F_CUDA(cudaMemcpy(t.data(), c->time_hist, ne * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost));
+    for (int e = 0; e < ne; ++e) res->epoch_seconds[e] = 1e-9 * (double)(t[e] - c->h_state->t0);
+  }
+  float ms = 0.f;
+  N2F_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  res->gpu_ms = ms;
+  return N2F_OK;
+}
+
+int n2f_fit_denoise_host(n2f_ctx* c, const void* image, int dtype, const void* clean, double* out,
+                         n2f_result* res) {
+  if (!c || !image || !out || !res) return fail(N2F_ERR_ARG, "null argument");
+  if (dtype != N2F_F32 && dtype != N2F_F64) return fail(N2F_ERR_ARG, "dtype");
+  N2F_CUDA(cudaSetDevice(c->device));
+  const size_t nb = c->Pv * dtype_size(dtype);
+  N2F_CUDA(cudaMemcpyAsync(c->img, image, nb, cudaMemcpyHostToDevice, c->stream));
+  const void* dclean = nullptr;
+  if (clean) {
+    if (!c->clean) return fail(N2F_ERR_ARG, "clean image given but scheme is not exact");
+    N2F_CUDA(cudaMemcpyAsync(c->clean, clean, nb, cudaMemcpyHostToDevice, c->stream));
+    dclean = c->clean;
+  }
+  N2F_TRY(n2f_fit_denoise_dev(c, c->img, dtype, dclean, c->out_stage, res));
+  N2F_CUDA(cudaMemcpyAsync(out, c->out_stage, c->Pv * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  return N2F_OK;
+}
+
+// ---- step-level debug/parity entry points ----------------------------------
+int n2f_ctx_prepare(n2f_ctx* c, const void* image, int dtype, const void* clean, int init_from_seed) {
+  if (!c || !image) return fail(N2F_ERR_ARG, "null argument");
+  N2F_CUDA(cudaSetDevice(c->device));
+  const size_t nb = c->Pv * dtype_size(dtype);
+  N2F_CUDA(cudaMemcpy(c->img, image, nb, cudaMemcpyHostToDevice));
+  const void* dclean = nullptr;
+  if (clean && c->clean) {
+    N2F_CUDA(cudaMemcpy(c->clean, clean, nb, cudaMemcpyHostToDevice));
+    dclean = c->clean;
+  }
+  int degenerate = 0;
+  N2F_TRY(prepare_input(c, c->img, dtype, dclean, &degenerate));
+  if (degenerate) return fail(N2F_ERR_ARG, "degenerate image");
+  if (init_from_seed) N2F_TRY(init_network(c));
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  return N2F_OK;
+}
+
+int n2f_ctx_param_count(n2f_ctx* c, int64_t* n) {
+  if (!c || !n) return fail(N2F_ERR_ARG, "null argument");
+  *n = c->ptotal;
+  return N2F_OK;
+}
+
+// which: 0 = params, 1 = adam m, 2 = adam v, 3 = gradients of the last step
+int n2f_ctx_get_arena(n2f_ctx* c, int which, float* host) {
+  if (!c || !host) return fail(N2F_ERR_ARG, "null argument");
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  if (which <= 2) {
+    const float* src = which == 0 ? c->params : which == 1 ? c->m : c->v;
+    N2F_CUDA(cudaMemcpy(host, src, c->ptotal * 4, cudaMemcpyDeviceToHost));
+    return N2F_OK;
+  }
+  float* tmp = nullptr;
+  N2F_CUDA(cudaMalloc(&tmp, c->ptotal * 4));
+  for (int q = 0; q < 2 * kLayers; ++q) {
+    const AdamTensor& T = c->adam.t[q];
+    int s = reduce_partials(T.part, tmp + T.off, T.nsplit, T.n, c->stream);
+    if (s != N2F_OK) {
+      cudaFree(tmp);
+      return s;
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(host, tmp, c->ptotal * 4, cudaMemcpyDeviceToHost, c->stream);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(tmp);
+  N2F_CUDA(e);
+  return N2F_OK;
+}
+
+// Overwrite params (engine layout) and reset Adam moments/step and stop state.
+int n2f_ctx_set_params(n2f_ctx* c, const float* host) {
+  if (!c || !host) return fail(N2F_ERR_ARG, "null argument");
+  N2F_CUDA(cudaMemcpy(c->params, host, c->ptotal * 4, cudaMemcpyHostToDevice));
+  N2F_TRY(refresh_derived(c));
+  N2F_CUDA(cudaMemsetAsync(c->m, 0, c->ptotal * 4, c->stream));
+  N2F_CUDA(cudaMemsetAsync(c->v, 0, c->ptotal * 4, c->stream));
+  N2F_CUDA(cudaMemsetAsync(c->step_counter, 0, sizeof(int), c->stream));
+  N2F_TRY(launch_reset_state(c->dstate, c->stream));
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  return N2F_OK;
+}
+
+int n2f_ctx_step(n2f_ctx* c, int pair, float* logits_host) {
+  if (!c || pair < 0 || pair > 3) return fail(N2F_ERR_ARG, "bad pair");
+  N2F_TRY(enqueue_step(c, pair));
+  if (logits_host)
+    N2F_CUDA(cudaMemcpyAsync(logits_host, c->z, c->Pt * 4, cudaMemcpyDeviceToHost, c->stream));
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  return N2F_OK;
+}
+
+int n2f_ctx_epoch(n2f_ctx* c, int* stopped) {
+  if (!c) return fail(N2F_ERR_ARG, "null ctx");
+  N2F_TRY(enqueue_epoch(c, 0));
+  N2F_CUDA(cudaMemcpyAsync(c->h_state, c->dstate, sizeof(DevState), cudaMemcpyDeviceToHost,
+                           c->stream));
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  if (stopped) *stopped = c->h_state->stopped;
+  return N2F_OK;
+}
+
+// Validation output of the current net (slot of the current epoch) + score.
+int n2f_ctx_validate(n2f_ctx* c, float* out_host, double* score) {
+  if (!c) return fail(N2F_ERR_ARG, "null ctx");
+  N2F_TRY(enqueue_validate(c));
+  N2F_CUDA(cudaMemcpyAsync(c->h_state, c->dstate, sizeof(DevState), cudaMemcpyDeviceToHost,
+                           c->stream));
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  const int slot = c->h_state->epoch % c->cfg.avg_window;
+  if (out_host)
+    N2F_CUDA(cudaMemcpy(out_host, c->ring + (int64_t)slot * c->Pv, c->Pv * 4,
+                        cudaMemcpyDeviceToHost));
+  if (score) {
+    std::vector<double> p(c->nblk_val);
+    N2F_CUDA(cudaMemcpy(p.data(), c->part_se, p.size() * 8, cudaMemcpyDeviceToHost));
+    double s = 0.0;
+    for (double q : p) s += q;
+    *score = s / (double)c->Pv;
+  }
+  return N2F_OK;
+}
+
+// Training planes (4 inputs then 4 targets) and the f32 normalised image.
+int n2f_ctx_get_pairs(n2f_ctx* c, float* pin, float* ptgt, float* norm, int* ph, int* pw) {
+  if (!c) return fail(N2F_ERR_ARG, "null ctx");
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  if (pin) N2F_CUDA(cudaMemcpy(pin, c->pin, 4 * c->plane * 4, cudaMemcpyDeviceToHost));
+  if (ptgt) N2F_CUDA(cudaMemcpy(ptgt, c->ptgt, 4 * c->plane * 4, cudaMemcpyDeviceToHost));
+  if (norm) N2F_CUDA(cudaMemcpy(norm, c->norm, c->Pv * 4, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 4; ++k) {
+    if (ph) ph[k] = c->ph[k];
+    if (pw) pw[k] = c->pw[k];
+  }
+  return N2F_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Internal declarations shared by the libn2f translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/n2f.h"
+
+namespace n2f {
+
+// ---- error plumbing ---------------------------------------------------------
+void set_error(const std::string& msg);
+const std::string& error_text();
+int fail(int code, const char* fmt, ...);
+
+#define N2F_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return ::n2f::fail(e_ == cudaErrorMemoryAllocation ? N2F_ERR_OOM : N2F_ERR_CUDA,   \
+                         "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                         __LINE__);                                                      \
+  } while (0)
+
+#define N2F_TRY(call)            \
+  do {                           \
+    int s_ = (call);             \
+    if (s_ != N2F_OK) return s_; \
+  } while (0)
+
+#define N2F_LAUNCH_CHECK() N2F_CUDA(cudaGetLastError())
+
+// ---- network geometry (reference model.py:20, 36-43) ------------------------
+constexpr int kLayers = 9;
+constexpr int kCin[kLayers] = {1, 32, 32, 64, 64, 128, 128, 256, 256};
+constexpr int kCout[kLayers] = {32, 32, 64, 64, 128, 128, 256, 256, 1};
+constexpr int kKsz[kLayers] = {3, 3, 3, 3, 3, 3, 3, 3, 1};
+constexpr int kMaxC = 256;
+
+// ---- conv implementations ---------------------------------------------------
+enum ConvImpl { kImplAuto = 0, kImplSimt = 1, kImplTc = 2 };
+
+// Epilogue modes of the 3x3 implicit GEMM.
+enum Epi { kEpiBiasRelu = 0, kEpiMask = 1, kEpiBias = 2, kEpiNone = 3 };
+
+// SIMT fp32 kernels (conv_simt.cu)
+int conv3x3_simt(const float* x, const float* wk, const float* bias, const float* mask, float* y,
+                 int h, int w, int cin, int cout, int epi, cudaStream_t st);
+int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
+                    int cout, cudaStream_t st, int relu = 1);
+int wgrad3x3_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
+                  int cin, int cout, int nsplit, cudaStream_t st);
+int wgrad_first_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
+                     int cout, int nsplit, cudaStream_t st);
+int wgrad_nsplit(int64_t pixels, int cin, int cout);
+
+// tcgen05 kernels (conv_tc.cu)
+int conv3x3_tc(const float* x, const float* wk_hi, const float* wk_lo, const float* bias,
+               const float* mask, float* y, int h, int w, int cin, int cout, int epi,
+               cudaStream_t st);
+bool tc_supported(int cin, int cout);
+
+// utility kernels (prep.cu / train.cu)
+int reduce_partials(const float* part, float* out, int nsplit, int64_t n, cudaStream_t st);
+int transpose_dgrad_weights(const float* w, float* wt, int cin, int cout, cudaStream_t st);
+
+double wall_seconds();
+
+}  // namespace n2f

@@ -1,0 +1,438 @@
+// Training-loop kernels: fused 1x1 head + loss (+ its backward), validation
+// tail, multi-tensor Adam with fused deterministic split-K reduction, the
+// device-side early-stopping state machine and the output window mean.
+#include "n2f_internal.cuh"
+#include "train.cuh"
+
+namespace n2f {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Two-branch logistic (tensor.py:153-161), IEEE division.
+__device__ __forceinline__ float sigmoid_ref(float z) {
+  if (z >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-z)));
+  const float e = expf(z);
+  return __fdiv_rn(e, __fadd_rn(1.f, e));
+}
+
+// dloss/dz and the per-element loss for the two training losses
+// (tensor.py:164-193, trainer.py:112-117).
+__device__ __forceinline__ float loss_grad(float z, float t, int loss, float inv_n_num,
+                                           float two_over_n, float* elem) {
+  const float s = sigmoid_ref(z);
+  if (loss == 0) {
+    *elem = __fadd_rn(__fsub_rn(fmaxf(z, 0.f), __fmul_rn(z, t)), log1pf(expf(-fabsf(z))));
+    return __fdiv_rn(__fsub_rn(s, t), inv_n_num);  // (sigmoid(z) - t) / N
+  }
+  const float d = __fsub_rn(s, t);
+  *elem = __fmul_rn(d, d);
+  const float gs = __fmul_rn(two_over_n, d);                   // (2/N) * diff
+  return __fmul_rn(__fmul_rn(gs, s), __fsub_rn(1.f, s));       // grad_s * s * (1 - s)
+}
+
+// ---------------------------------------------------------------------------
+// Fused head for a training step: z = b9 + a8 . w9 (1x1 conv 256->1), loss and
+// dloss/dz, then the head's backward: gp8 = dz * w9 masked by (a8 > 0), and
+// deterministic per-block partials of dw9 / db9 / loss.  Warp per pixel.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_head_train(const float* __restrict__ a8, const float* __restrict__ w9,
+                 const float* __restrict__ b9, const float* __restrict__ tgt,
+                 float* __restrict__ gp8, float* __restrict__ part_w, float* __restrict__ part_b,
+                 double* __restrict__ part_loss, float* __restrict__ zout, int64_t P, int chunk,
+                 int loss, int* __restrict__ step_counter) {
+  __shared__ float red_w[kWarps][kMaxC];
+  __shared__ float red_b[kWarps];
+  __shared__ double red_l[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t pbeg = (int64_t)blockIdx.x * chunk;
+  const int64_t pend = min(P, pbeg + chunk);
+  float w[8], gw[8];
+  {
+    const float4 w0 = __ldg(reinterpret_cast<const float4*>(w9 + 8 * lane));
+    const float4 w1 = __ldg(reinterpret_cast<const float4*>(w9 + 8 * lane + 4));
+    w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
+    w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) gw[c] = 0.f;
+  const float bias = __ldg(b9);
+  const float nf = (float)P;
+  const float two_over_n = (float)(2.0 / (double)P);
+  float gb = 0.f;
+  double lsum = 0.0;
+  for (int64_t p = pbeg + warp; p < pend; p += kWarps) {
+    const float* row = a8 + p * kMaxC + 8 * lane;
+    const float4 x0 = __ldg(reinterpret_cast<const float4*>(row));
+    const float4 x1 = __ldg(reinterpret_cast<const float4*>(row + 4));
+    const float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+    float dot = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) dot = fmaf(a[c], w[c], dot);
+    const float z = warp_sum(dot) + bias;
+    float elem;
+    const float dz = loss_grad(z, __ldg(tgt + p), loss, nf, two_over_n, &elem);
+    float g[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      g[c] = a[c] > 0.f ? __fmul_rn(w[c], dz) : 0.f;
+      gw[c] = fmaf(dz, a[c], gw[c]);
+    }
+    float* grow = gp8 + p * kMaxC + 8 * lane;
+    *reinterpret_cast<float4*>(grow) = make_float4(g[0], g[1], g[2], g[3]);
+    *reinterpret_cast<float4*>(grow + 4) = make_float4(g[4], g[5], g[6], g[7]);
+    if (lane == 0) {
+      gb += dz;
+      lsum += (double)elem;
+      zout[p] = z;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) red_w[warp][8 * lane + c] = gw[c];
+  if (lane == 0) {
+    red_b[warp] = gb;
+    red_l[warp] = lsum;
+  }
+  __syncthreads();
+  {
+    const int c = threadIdx.x;  // kThreads == kMaxC
+    float s = red_w[0][c];
+    for (int k = 1; k < kWarps; ++k) s += red_w[k][c];
+    part_w[(int64_t)blockIdx.x * kMaxC + c] = s;
+  }
+  if (threadIdx.x == 0) {
+    float sb = red_b[0];
+    double sl = red_l[0];
+    for (int k = 1; k < kWarps; ++k) {
+      sb += red_b[k];
+      sl += red_l[k];
+    }
+    part_b[blockIdx.x] = sb;
+    part_loss[blockIdx.x] = sl;
+    if (blockIdx.x == 0 && step_counter) *step_counter += 1;  // Adam step t for this step
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Validation head: z -> sigmoid -> clip to (0,1) (model.py:136-140), write
+// into the ring slot of this epoch, f64 squared error vs the f32 normalised
+// input (trainer.py:97-101).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_head_val(const float* __restrict__ a8, const float* __restrict__ w9,
+               const float* __restrict__ b9, const float* __restrict__ norm,
+               float* __restrict__ ring, int64_t P, int chunk, const DevState* __restrict__ st,
+               int window, double* __restrict__ part_se) {
+  __shared__ double red[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t pbeg = (int64_t)blockIdx.x * chunk;
+  const int64_t pend = min(P, pbeg + chunk);
+  float* out = ring + (int64_t)(st->epoch % window) * P;
+  float w[8];
+  {
+    const float4 w0 = __ldg(reinterpret_cast<const float4*>(w9 + 8 * lane));
+    const float4 w1 = __ldg(reinterpret_cast<const float4*>(w9 + 8 * lane + 4));
+    w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
+    w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
+  }
+  const float bias = __ldg(b9);
+  const float tiny = __int_as_float(1);           // nextafter(0, 1)
+  const float top = __int_as_float(0x3f7fffff);   // nextafter(1, 0)
+  double se = 0.0;
+  for (int64_t p = pbeg + warp; p < pend; p += kWarps) {
+    const float* row = a8 + p * kMaxC + 8 * lane;
+    const float4 x0 = __ldg(reinterpret_cast<const float4*>(row));
+    const float4 x1 = __ldg(reinterpret_cast<const float4*>(row + 4));
+    float dot = x0.x * w[0];
+    dot = fmaf(x0.y, w[1], dot); dot = fmaf(x0.z, w[2], dot); dot = fmaf(x0.w, w[3], dot);
+    dot = fmaf(x1.x, w[4], dot); dot = fmaf(x1.y, w[5], dot); dot = fmaf(x1.z, w[6], dot);
+    dot = fmaf(x1.w, w[7], dot);
+    const float z = warp_sum(dot) + bias;
+    if (lane == 0) {
+      const float o = fminf(fmaxf(sigmoid_ref(z), tiny), top);
+      out[p] = o;
+      const double d = (double)o - (double)__ldg(norm + p);
+      se += d * d;
+    }
+  }
+  if (lane == 0) red[warp] = se;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = red[0];
+    for (int k = 1; k < kWarps; ++k) s += red[k];
+    part_se[blockIdx.x] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Multi-tensor Adam (tensor.py:125-141) with the split-K gradient reduction
+// fused in (fixed summation order), and the dgrad-transposed weight copy.
+// NumPy-2 semantics: every Python-float scalar is rounded to fp32 first and
+// each operation is rounded separately (no FMA contraction).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_adam(AdamArgs args, const int* __restrict__ step_counter, int fixed_t) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= args.total) return;
+  int k = 0;
+  while (k + 1 < args.ntensors && i >= args.t[k + 1].off) ++k;
+  const AdamTensor& T = args.t[k];
+  const int64_t j = i - T.off;
+  float g = T.part[j];
+  for (int s = 1; s < T.nsplit; ++s) g += T.part[(int64_t)s * T.n + j];
+  const int t = step_counter ? *step_counter : fixed_t;
+  const int ti = (t < args.table_len ? t : args.table_len) - 1;
+  const float bc1 = args.bc1[ti], bc2 = args.bc2[ti];
+  float m = args.m[i], v = args.v[i], p = args.p[i];
+  m = __fmul_rn(m, args.beta1);
+  m = __fadd_rn(m, __fmul_rn(args.one_minus_beta1, g));
+  v = __fmul_rn(v, args.beta2);
+  v = __fadd_rn(v, __fmul_rn(args.one_minus_beta2, __fmul_rn(g, g)));
+  const float mh = __fdiv_rn(m, bc1);
+  const float vh = __fdiv_rn(v, bc2);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(args.lr, mh), __fadd_rn(__fsqrt_rn(vh), args.eps)));
+  args.m[i] = m;
+  args.v[i] = v;
+  args.p[i] = p;
+  if (T.wt) {  // wt[c][8-tap][o] = w[o][tap][c]
+    const int c = (int)(j % T.cin);
+    const int tap = (int)((j / T.cin) % 9);
+    const int o = (int)(j / ((int64_t)T.cin * 9));
+    T.wt[((int64_t)c * 9 + (8 - tap)) * T.cout + o] = p;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// End-of-epoch bookkeeping (trainer.py:78-94): reduce the validation and loss
+// partials in fixed order, record history, strict-improvement patience rule,
+// and drive the graph's while-condition.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_stop(DevState* __restrict__ st, const double* __restrict__ part_se, int n_se, double pv,
+           const double* __restrict__ part_loss, int n_loss, Pt4 pt,
+           double* __restrict__ val_hist, double* __restrict__ loss_hist,
+           unsigned long long* __restrict__ time_hist, int patience, int max_epochs,
+           cudaGraphConditionalHandle handle, int use_handle) {
+  __shared__ double red[kThreads];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n_se; i += kThreads) s += part_se[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double score = red[0] / pv;
+  __syncthreads();
+  double losses[4];
+  for (int q = 0; q < 4; ++q) {
+    double l = 0.0;
+    for (int i = threadIdx.x; i < n_loss; i += kThreads) l += part_loss[q * n_loss + i];
+    red[threadIdx.x] = l;
+    __syncthreads();
+    for (int w = kThreads / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    losses[q] = red[0] / pt.v[q];
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+  const int e = st->epoch;  // 0-based index of this epoch
+  val_hist[e] = score;
+  for (int q = 0; q < 4; ++q) loss_hist[4 * e + q] = losses[q];
+  time_hist[e] = now;
+  st->epoch = e + 1;
+  if (score < st->best) {
+    st->best = score;
+    st->since = 0;
+    st->best_epoch = e + 1;
+  } else {
+    st->since += 1;
+  }
+  int go = 1;
+  if (st->since >= patience) {
+    st->stopped = 1;
+    st->stop_reason = N2F_STOP_PATIENCE;
+    go = 0;
+  } else if (e + 1 >= max_epochs) {
+    st->stopped = 1;
+    st->stop_reason = N2F_STOP_MAX_EPOCHS;
+    go = 0;
+  }
+  if (use_handle) cudaGraphSetConditional(handle, go);
+}
+
+// Mean of the buffered outputs in epoch order (sequential fp32 adds, then
+// / fl32(n)), mapped back with f64 (x * (vmax - vmin) + vmin)
+// (trainer.py:104-109, imaging.py:208-211).
+__global__ void __launch_bounds__(kThreads)
+    k_window_mean(const float* __restrict__ ring, int64_t plane, int window,
+                  const DevState* __restrict__ st, int n_arg, int first_arg,
+                  const double* __restrict__ mm, double vmin_arg, double vmax_arg,
+                  double* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= plane) return;
+  int n = n_arg, first = first_arg;
+  if (st) {
+    n = st->epoch < window ? st->epoch : window;
+    first = (st->epoch - n) % window;
+  }
+  const double vmin = mm ? mm[0] : vmin_arg;
+  const double vmax = mm ? mm[1] : vmax_arg;
+  float acc = ring[(int64_t)first * plane + p];
+  for (int k = 1; k < n; ++k) acc = __fadd_rn(acc, ring[(int64_t)((first + k) % window) * plane + p]);
+  const float mean = __fdiv_rn(acc, (float)n);
+  out[p] = __dadd_rn(__dmul_rn((double)mean, __dsub_rn(vmax, vmin)), vmin);
+}
+
+// Standalone loss on logits (parity entry point).
+__global__ void __launch_bounds__(kThreads)
+    k_loss(const float* __restrict__ z, const float* __restrict__ t, float* __restrict__ grad,
+           int64_t n, int loss, double* __restrict__ part) {
+  __shared__ double red[kThreads];
+  const float nf = (float)n;
+  const float two_over_n = (float)(2.0 / (double)n);
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float elem;
+    grad[i] = loss_grad(z[i], t[i], loss, nf, two_over_n, &elem);
+    s += elem;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_val_tail(const float* __restrict__ z, const float* __restrict__ norm, float* __restrict__ out,
+               int64_t n, double* __restrict__ part) {
+  __shared__ double red[kThreads];
+  const float tiny = __int_as_float(1), top = __int_as_float(0x3f7fffff);
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float o = fminf(fmaxf(sigmoid_ref(z[i]), tiny), top);
+    out[i] = o;
+    const double d = (double)o - (double)norm[i];
+    s += d * d;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void k_sum_parts(const double* __restrict__ part, int n, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    *out = s;
+  }
+}
+
+__global__ void k_reset_state(DevState* st) {
+  if (threadIdx.x == 0) {
+    st->epoch = 0;
+    st->step = 0;
+    st->since = 0;
+    st->stopped = 0;
+    st->stop_reason = N2F_STOP_MAX_EPOCHS;
+    st->best_epoch = 0;
+    st->best = INFINITY;
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    st->t0 = now;
+  }
+}
+
+}  // namespace
+
+// ---- launchers ---------------------------------------------------------------
+int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
+                      float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
+                      int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st) {
+  const int chunk = (int)((P + nblk - 1) / nblk);
+  k_head_train<<<nblk, kThreads, 0, st>>>(a8, w9, b9, tgt, gp8, part_w, part_b, part_loss, zout, P,
+                                          chunk, loss, step_counter);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_head_val(const float* a8, const float* w9, const float* b9, const float* norm,
+                    float* ring, int64_t P, int nblk, const DevState* dst, int window,
+                    double* part_se, cudaStream_t st) {
+  const int chunk = (int)((P + nblk - 1) / nblk);
+  k_head_val<<<nblk, kThreads, 0, st>>>(a8, w9, b9, norm, ring, P, chunk, dst, window, part_se);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_adam(const AdamArgs& args, const int* step_counter, int fixed_t, cudaStream_t st) {
+  k_adam<<<(unsigned)((args.total + kThreads - 1) / kThreads), kThreads, 0, st>>>(args, step_counter,
+                                                                                   fixed_t);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_stop(DevState* dst, const double* part_se, int n_se, double pv, const double* part_loss,
+                int n_loss, const double pt[4], double* val_hist, double* loss_hist,
+                unsigned long long* time_hist, int patience, int max_epochs,
+                cudaGraphConditionalHandle handle, int use_handle, cudaStream_t st) {
+  Pt4 ptv{{pt[0], pt[1], pt[2], pt[3]}};
+  k_stop<<<1, kThreads, 0, st>>>(dst, part_se, n_se, pv, part_loss, n_loss, ptv, val_hist, loss_hist,
+                                 time_hist, patience, max_epochs, handle, use_handle);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_window_mean(const float* ring, int64_t plane, int window, const DevState* dst, int n,
+                       int first, const double* mm, double vmin, double vmax, double* out,
+                       cudaStream_t st) {
+  k_window_mean<<<(unsigned)((plane + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+      ring, plane, window, dst, n, first, mm, vmin, vmax, out);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_loss(const float* z, const float* t, float* grad, int64_t n, int loss, double* part,
+                int nblk, double* sum_out, cudaStream_t st) {
+  k_loss<<<nblk, kThreads, 0, st>>>(z, t, grad, n, loss, part);
+  k_sum_parts<<<1, 32, 0, st>>>(part, nblk, sum_out);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_val_tail(const float* z, const float* norm, float* out, int64_t n, double* part, int nblk,
+                    double* sum_out, cudaStream_t st) {
+  k_val_tail<<<nblk, kThreads, 0, st>>>(z, norm, out, n, part);
+  k_sum_parts<<<1, 32, 0, st>>>(part, nblk, sum_out);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_reset_state(DevState* dst, cudaStream_t st) {
+  k_reset_state<<<1, 32, 0, st>>>(dst);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+}  // namespace n2f

@@ -1,0 +1,77 @@
+// Device-side state and launchers of the training-loop kernels (train.cu).
+#pragma once
+#include "n2f_internal.cuh"
+
+namespace n2f {
+
+// Early-stopping state (trainer.py:54-66), resident on the device.
+struct DevState {
+  int epoch;        // completed epochs
+  int step;         // unused (Adam t lives in its own counter)
+  int since;        // epochs since the last strict improvement
+  int stopped;
+  int stop_reason;
+  int best_epoch;
+  double best;
+  unsigned long long t0;  // %globaltimer at the start of the fit
+};
+
+struct Pt4 {
+  double v[4];
+};
+
+struct AdamTensor {
+  int64_t off;        // offset in the parameter arena
+  int64_t n;          // elements
+  const float* part;  // [nsplit][n] gradient partials
+  int nsplit;
+  float* wt;          // optional dgrad-transposed copy (3x3 weights), else null
+  int cin, cout;
+};
+
+constexpr int kMaxTensors = 18;
+
+struct AdamArgs {
+  AdamTensor t[kMaxTensors];
+  int ntensors;
+  int64_t total;
+  float* p;
+  float* m;
+  float* v;
+  const float* bc1;  // fl32(1 - beta1^t), t = 1..table_len
+  const float* bc2;
+  int table_len;
+  float beta1, one_minus_beta1, beta2, one_minus_beta2, lr, eps;
+};
+
+int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
+                      float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
+                      int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st);
+int launch_head_val(const float* a8, const float* w9, const float* b9, const float* norm,
+                    float* ring, int64_t P, int nblk, const DevState* dst, int window,
+                    double* part_se, cudaStream_t st);
+int launch_adam(const AdamArgs& args, const int* step_counter, int fixed_t, cudaStream_t st);
+int launch_stop(DevState* dst, const double* part_se, int n_se, double pv, const double* part_loss,
+                int n_loss, const double pt[4], double* val_hist, double* loss_hist,
+                unsigned long long* time_hist, int patience, int max_epochs,
+                cudaGraphConditionalHandle handle, int use_handle, cudaStream_t st);
+int launch_window_mean(const float* ring, int64_t plane, int window, const DevState* dst, int n,
+                       int first, const double* mm, double vmin, double vmax, double* out,
+                       cudaStream_t st);
+int launch_loss(const float* z, const float* t, float* grad, int64_t n, int loss, double* part,
+                int nblk, double* sum_out, cudaStream_t st);
+int launch_val_tail(const float* z, const float* norm, float* out, int64_t n, double* part, int nblk,
+                    double* sum_out, cudaStream_t st);
+int launch_reset_state(DevState* dst, cudaStream_t st);
+
+// prep.cu
+int launch_minmax(const void* img, int dtype, int64_t n, double* part, double* out3,
+                  cudaStream_t st);
+size_t minmax_scratch_doubles();
+int launch_pairs(const void* img, int dtype, const void* clean, const double* mm, int H, int W,
+                 int scheme, int clip, float* norm, float* pin, float* ptgt, int64_t plane,
+                 cudaStream_t st);
+int launch_init_layer(uint64_t seed, int layer, int cin, int cout, int k, float* w,
+                      cudaStream_t st);
+
+}  // namespace n2f

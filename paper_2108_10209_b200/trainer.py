@@ -1,0 +1,323 @@
+"""Host-side mirror of the reference trainer API, running on the B200 engine.
+
+Same names, argument meaning, return types and error behaviour as the
+reference module ``noise2fast.trainer`` (pkg/src/noise2fast/trainer.py):
+
+* ``TrainConfig``            (trainer.py:29-51)  -- same fields, same checks
+* ``DenoiseResult``          (trainer.py:69-75)
+* ``train_single_channel``   (trainer.py:125-213) -- the hot path, one call
+  into ``libn2f.so``: the whole fit (normalise, pairs, init, every epoch,
+  validation, early stopping, window mean) runs on the GPU as one CUDA
+  graph; the host only validates arguments and formats the result
+* ``denoise_image``          (trainer.py:216-250) -- per (slice, channel)
+  fan-out with ``derive_seed(config.seed, ch, sl)`` seeds
+
+``install()`` rebinds ``noise2fast.trainer.train_single_channel`` (the module
+global that ``denoise_image`` and the CLI jobs look up, trainer.py:241) so an
+installed reference package runs on this engine.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import json
+import os
+import threading
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import N2FConfig, N2FResult, STOP_REASONS, call, load
+
+_LOSSES = ("bce", "mse")
+_SCHEMES = ("checkerboard", "quad", "exact")
+_M64 = 0xFFFFFFFFFFFFFFFF
+
+
+@dataclass
+class TrainConfig:
+    loss: str = "bce"
+    scheme: str = "checkerboard"
+    lr: float = 0.001
+    patience_epochs: int = 100
+    avg_window: int = 100
+    max_epochs: int = 20000
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.loss not in _LOSSES:
+            raise ValueError(f"loss must be one of {_LOSSES}, got {self.loss!r}")
+        if self.scheme not in _SCHEMES:
+            raise ValueError(f"scheme must be one of {_SCHEMES}, got {self.scheme!r}")
+        if self.lr <= 0:
+            raise ValueError("lr must be > 0")
+        if self.patience_epochs < 1:
+            raise ValueError("patience_epochs must be >= 1")
+        if self.avg_window < 1:
+            raise ValueError("avg_window must be >= 1")
+        if self.max_epochs < 1:
+            raise ValueError("max_epochs must be >= 1")
+
+
+@dataclass
+class DenoiseResult:
+    denoised: np.ndarray  # 2-D, original value scale, float64
+    epochs_run: int
+    val_history: list
+    wall_time: float
+    stop_reason: str  # "patience" | "max_epochs" | "degenerate"
+
+
+# ---------------------------------------------------------------------------
+# seeds (rng.py:20-39) -- integer SplitMix64, needed for denoise_image fan-out
+# ---------------------------------------------------------------------------
+
+
+def _mix64(z: int) -> int:
+    z = (z + 0x9E3779B97F4A7C15) & _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def derive_seed(seed: int, *ids: int) -> int:
+    acc = seed & _M64
+    for i in ids:
+        acc = _mix64(acc ^ (i & _M64))
+    return acc
+
+
+# ---------------------------------------------------------------------------
+# engine contexts (one per process/device/shape/config, reused across images)
+# ---------------------------------------------------------------------------
+
+
+def _device_index() -> int:
+    env = os.environ.get("N2F_DEVICE")
+    return int(env) if env is not None else 0
+
+
+class Engine:
+    """Owns one libn2f context: workspaces + the captured CUDA graph."""
+
+    def __init__(self, height: int, width: int, config, device: int | None = None,
+                 conv_impl: int = 0, use_graph: bool = True):
+        lib = load()
+        self.height, self.width = int(height), int(width)
+        self.device = _device_index() if device is None else int(device)
+        cfg = N2FConfig()
+        cfg.loss = _LOSSES.index(config.loss)
+        cfg.scheme = _SCHEMES.index(config.scheme)
+        cfg.lr = float(config.lr)
+        cfg.patience_epochs = int(config.patience_epochs)
+        cfg.avg_window = int(config.avg_window)
+        cfg.max_epochs = int(config.max_epochs)
+        cfg.conv_impl = int(conv_impl)
+        cfg.seed = int(config.seed) & _M64
+        cfg.use_graph = 1 if use_graph else 0
+        self.cfg = cfg
+        self.max_epochs = int(config.max_epochs)
+        h = _lib.C.c_void_p()
+        call("n2f_create", self.device, self.height, self.width, _lib.C.byref(cfg), _lib.C.byref(h))
+        self.handle = h
+        self._lib = lib
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.n2f_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return self._lib.n2f_ctx_stream(self.handle) or 0
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self._lib.n2f_ctx_device_bytes(self.handle))
+
+    def _result_struct(self):
+        n = self.max_epochs
+        hist = np.zeros(n, np.float64)
+        losses = np.zeros(4 * n, np.float64)
+        secs = np.zeros(n, np.float64)
+        r = N2FResult()
+        r.val_history = hist.ctypes.data_as(_lib.C.POINTER(_lib.C.c_double))
+        r.train_loss = losses.ctypes.data_as(_lib.C.POINTER(_lib.C.c_double))
+        r.epoch_seconds = secs.ctypes.data_as(_lib.C.POINTER(_lib.C.c_double))
+        return r, hist, losses, secs
+
+    def fit_host(self, image: np.ndarray, clean: np.ndarray | None = None):
+        """Whole fit from host arrays (float32 or float64, C-contiguous)."""
+        dtype = _lib.N2F_F64 if image.dtype == np.float64 else _lib.N2F_F32
+        out = np.empty((self.height, self.width), np.float64)
+        r, hist, losses, secs = self._result_struct()
+        call("n2f_fit_denoise_host", self.handle, image.ctypes.data,
+             dtype, clean.ctypes.data if clean is not None else None, out.ctypes.data,
+             _lib.C.byref(r))
+        n = r.epochs_run
+        return out, r, hist[:n].copy(), losses[: 4 * n].reshape(n, 4).copy(), secs[:n].copy()
+
+    def fit_device(self, image_ptr: int, dtype: int, out_ptr: int, clean_ptr: int | None = None):
+        """Whole fit on device-resident buffers (used by the bench's `value`)."""
+        r = N2FResult()
+        call("n2f_fit_denoise_dev", self.handle, image_ptr, dtype, clean_ptr, out_ptr,
+             _lib.C.byref(r))
+        return r
+
+
+_cache_lock = threading.Lock()
+_cache: dict = {}
+
+
+def _engine_for(shape, config) -> Engine:
+    key = (shape, config.loss, config.scheme, float(config.lr), int(config.patience_epochs),
+           int(config.avg_window), int(config.max_epochs), int(config.seed) & _M64, _device_index())
+    with _cache_lock:
+        eng = _cache.get(key)
+        if eng is None:
+            # keep one live context: large images own tens of GB of workspace
+            for k in list(_cache):
+                _cache.pop(k).close()
+            eng = Engine(shape[0], shape[1], config)
+            _cache[key] = eng
+        return eng
+
+
+def release_engines() -> None:
+    with _cache_lock:
+        for k in list(_cache):
+            _cache.pop(k).close()
+
+
+# ---------------------------------------------------------------------------
+# reference-facing API
+# ---------------------------------------------------------------------------
+
+
+def _write_telemetry(sink, record: dict) -> None:
+    if sink is not None:
+        sink.write(json.dumps(record) + "\n")
+
+
+def train_single_channel(noisy, config, clean=None, telemetry=None, telemetry_tags=None) -> DenoiseResult:
+    """Denoise one 2-D image by training a fresh network on it (on the GPU).
+
+    Drop-in for ``noise2fast.trainer.train_single_channel`` (trainer.py:125-213):
+    ``config`` may be this module's TrainConfig or the reference's.
+    """
+    t0 = time.perf_counter()
+    arr = np.asarray(noisy)
+    if arr.dtype not in (np.float32, np.float64):
+        arr = np.asarray(arr, dtype=np.float64)
+    if arr.ndim != 2:
+        raise ValueError(f"expected a 2-D image, got shape {arr.shape}")
+    if arr.shape[0] < 4 or arr.shape[1] < 4:
+        raise ValueError(f"image must be at least 4x4, got {arr.shape}")
+    clean_arr = None
+    if config.scheme == "exact":
+        if not np.isfinite(arr).all():
+            raise ValueError("image contains non-finite values")
+        if clean is None:
+            raise ValueError("the exact scheme requires the clean ground-truth image")
+        clean_arr = np.asarray(clean, dtype=np.float64)
+        if clean_arr.shape != arr.shape:
+            raise ValueError(f"clean shape {clean_arr.shape} != noisy shape {arr.shape}")
+        arr = np.asarray(arr, dtype=np.float64)
+    arr = np.ascontiguousarray(arr)
+    if clean_arr is not None:
+        clean_arr = np.ascontiguousarray(clean_arr)
+
+    eng = _engine_for(arr.shape, config)
+    wall0 = time.time()
+    try:
+        out, r, hist, losses, secs = eng.fit_host(arr, clean_arr)
+    except _lib.N2FError as e:
+        if e.code == _lib.N2F_ERR_NONFINITE:
+            raise ValueError("image contains non-finite values") from None
+        if e.code == _lib.N2F_ERR_ARG:
+            raise ValueError(e.msg) from None
+        raise
+    reason = STOP_REASONS[r.stop_reason]
+    if reason == "degenerate":
+        return DenoiseResult(out, 0, [], time.perf_counter() - t0, "degenerate")
+    tags = telemetry_tags or {}
+    if telemetry is not None:
+        for e in range(r.epochs_run):
+            _write_telemetry(telemetry, {
+                **tags,
+                "epoch": e + 1,
+                "train_loss_per_pair": [float(v) for v in losses[e]],
+                "val_mse": float(hist[e]),
+                "timestamp": wall0 + float(secs[e]),
+            })
+    return DenoiseResult(
+        denoised=out,
+        epochs_run=int(r.epochs_run),
+        val_history=[float(v) for v in hist],
+        wall_time=time.perf_counter() - t0,
+        stop_reason=reason,
+    )
+
+
+@dataclass
+class ImageData:
+    """Minimal stand-in for the reference ImageData (imaging.py): samples are
+    (n_slices, height, width, channels)."""
+
+    samples: np.ndarray
+    bit_depth: str = "float32"
+    data_range: float | None = 1.0
+
+    @property
+    def n_slices(self) -> int:
+        return self.samples.shape[0]
+
+    @property
+    def channels(self) -> int:
+        return self.samples.shape[3]
+
+
+def denoise_image(image, config, clean=None, telemetry=None):
+    """Denoise every channel of every slice with independent runs (trainer.py:216-250)."""
+    if not 1 <= image.channels <= 4:
+        raise ValueError(f"expected 1-4 channels, got {image.channels}")
+    if config.scheme == "exact":
+        if clean is None:
+            raise ValueError("the exact scheme requires the clean ground-truth image")
+        if clean.samples.shape != image.samples.shape:
+            raise ValueError("clean image layout differs from noisy image")
+    out = np.empty_like(image.samples, dtype=np.float32)
+    runs = []
+    for sl in range(image.n_slices):
+        for ch in range(image.channels):
+            sub = dataclasses.replace(config, seed=derive_seed(config.seed, ch, sl))
+            result = train_single_channel(
+                image.samples[sl, :, :, ch],
+                sub,
+                clean=None if clean is None else clean.samples[sl, :, :, ch],
+                telemetry=telemetry,
+                telemetry_tags={"slice": sl, "channel": ch},
+            )
+            out[sl, :, :, ch] = result.denoised
+            runs.append(result)
+    return type(image)(out, image.bit_depth, image.data_range), runs
+
+
+def install() -> None:
+    """Route the installed reference package's hot path through this engine.
+
+    Rebinds the module global ``noise2fast.trainer.train_single_channel``
+    (looked up at call time by ``denoise_image``, trainer.py:241, and hence by
+    the CLI jobs, cli.py:147/175).  Spawned CLI workers: see INTEGRATION.md.
+    """
+    import noise2fast.trainer as ref_trainer
+
+    ref_trainer.train_single_channel = train_single_channel
