@@ -63,6 +63,7 @@ typedef struct n2f_result {
   double* train_loss;         /* [4*max_epochs]   per-pair training loss       */
   double* epoch_seconds;      /* [max_epochs]     device time since start (s)  */
   double gpu_ms;              /* device time of the whole fit (CUDA events)    */
+  int64_t kernel_launches;    /* libn2f kernels executed by the fit            */
 } n2f_result;
 
 typedef struct n2f_ctx n2f_ctx;
@@ -155,6 +156,7 @@ int n2f_ctx_prepare(n2f_ctx* ctx, const void* image, int dtype, const void* clea
 int n2f_ctx_param_count(n2f_ctx* ctx, int64_t* n);
 int n2f_ctx_get_arena(n2f_ctx* ctx, int which, float* host);
 int n2f_ctx_set_params(n2f_ctx* ctx, const float* host);
+int n2f_ctx_set_arena(n2f_ctx* ctx, int which, const float* host, int adam_step);
 int n2f_ctx_step(n2f_ctx* ctx, int pair, float* logits_host);
 int n2f_ctx_epoch(n2f_ctx* ctx, int* stopped);
 int n2f_ctx_validate(n2f_ctx* ctx, float* out_host, double* score);

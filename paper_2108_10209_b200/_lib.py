@@ -45,6 +45,7 @@ class N2FResult(C.Structure):
         ("train_loss", C.POINTER(C.c_double)),
         ("epoch_seconds", C.POINTER(C.c_double)),
         ("gpu_ms", C.c_double),
+        ("kernel_launches", C.c_int64),
     ]
 
 
@@ -85,6 +86,7 @@ SIGNATURES = {
     "n2f_ctx_param_count": [_P, _P],
     "n2f_ctx_get_arena": [_P, _I, _P],
     "n2f_ctx_set_params": [_P, _P],
+    "n2f_ctx_set_arena": [_P, _I, _P, _I],
     "n2f_ctx_step": [_P, _I, _P],
     "n2f_ctx_epoch": [_P, _P],
     "n2f_ctx_validate": [_P, _P, _P],

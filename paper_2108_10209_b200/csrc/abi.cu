@@ -139,7 +139,7 @@ int n2f_conv_fwd(const float* x, const float* w, const float* b, float* y, int h
   } else {
     return fail(N2F_ERR_UNSUPPORTED, "conv_fwd: unsupported shape cin=%d cout=%d k=%d", cin, cout, k);
   }
-  N2F_CUDA(cudaStreamSynchronize(S(stream)));
+  if (!stream) N2F_CUDA(cudaStreamSynchronize(S(stream)));  // async on an explicit stream
   return N2F_OK;
 }
 

@@ -82,6 +82,7 @@ struct n2f_ctx {
   cudaGraphConditionalHandle handle = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   AdamArgs adam{};
+  int64_t epoch_launches = 0;  // kernels in one captured epoch body
 };
 
 namespace {
@@ -188,7 +189,10 @@ int build_graph(n2f_ctx* c) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   N2F_CUDA(cudaStreamBeginCaptureToGraph(c->stream, body, nullptr, nullptr, 0,
                                          cudaStreamCaptureModeRelaxed));
+  const int64_t before = g_launches;
   int s = enqueue_epoch(c, 1);
+  c->epoch_launches = g_launches - before;
+  g_launches = before;  // captured, not executed
   cudaGraph_t captured = nullptr;
   cudaError_t e = cudaStreamEndCapture(c->stream, &captured);
   if (s != N2F_OK) return s;
@@ -451,6 +455,7 @@ int n2f_fit_denoise_dev(n2f_ctx* c, const void* image, int dtype, const void* cl
   N2F_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   N2F_CUDA(cudaEventRecord(c->ev0, st));
+  const int64_t launches0 = g_launches;
   int degenerate = 0;
   N2F_TRY(prepare_input(c, image, dtype, clean, &degenerate));
   res->vmin = c->h_mm[0];
@@ -463,6 +468,7 @@ int n2f_fit_denoise_dev(n2f_ctx* c, const void* image, int dtype, const void* cl
     res->epochs_run = 0;
     res->stop_reason = N2F_STOP_DEGENERATE;
     res->best_score = INFINITY;
+    res->kernel_launches = g_launches - launches0;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     res->gpu_ms = ms;
@@ -477,6 +483,8 @@ int n2f_fit_denoise_dev(n2f_ctx* c, const void* image, int dtype, const void* cl
   N2F_CUDA(cudaStreamSynchronize(st));
   const int ne = c->h_state->epoch;
   res->epochs_run = ne;
+  res->kernel_launches =
+      g_launches - launches0 + (c->cfg.use_graph ? (int64_t)ne * c->epoch_launches : 0);
   res->stop_reason = c->h_state->stop_reason;
   res->best_score = c->h_state->best;
   if (res->val_history)
@@ -576,6 +584,20 @@ int n2f_ctx_set_params(n2f_ctx* c, const float* host) {
   N2F_CUDA(cudaMemsetAsync(c->v, 0, c->ptotal * 4, c->stream));
   N2F_CUDA(cudaMemsetAsync(c->step_counter, 0, sizeof(int), c->stream));
   N2F_TRY(launch_reset_state(c->dstate, c->stream));
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  return N2F_OK;
+}
+
+// Overwrite one arena (0 params, 1 Adam m, 2 Adam v) and the Adam step count
+// (t of the NEXT step is step+1), leaving everything else untouched.
+int n2f_ctx_set_arena(n2f_ctx* c, int which, const float* host, int step) {
+  if (!c || which < 0 || which > 2) return fail(N2F_ERR_ARG, "bad argument");
+  if (host) {
+    float* dst = which == 0 ? c->params : which == 1 ? c->m : c->v;
+    N2F_CUDA(cudaMemcpy(dst, host, c->ptotal * 4, cudaMemcpyHostToDevice));
+    if (which == 0) N2F_TRY(refresh_derived(c));
+  }
+  if (step >= 0) N2F_CUDA(cudaMemcpy(c->step_counter, &step, sizeof(int), cudaMemcpyHostToDevice));
   N2F_CUDA(cudaStreamSynchronize(c->stream));
   return N2F_OK;
 }

@@ -31,7 +31,14 @@ int fail(int code, const char* fmt, ...);
     if (s_ != N2F_OK) return s_; \
   } while (0)
 
-#define N2F_LAUNCH_CHECK() N2F_CUDA(cudaGetLastError())
+// Every launcher calls this once per kernel it launched (it also counts the
+// launches, so the engine can report how many of its kernels a fit ran).
+extern thread_local int64_t g_launches;
+#define N2F_LAUNCH_CHECK()  \
+  do {                      \
+    ++::n2f::g_launches;    \
+    N2F_CUDA(cudaGetLastError()); \
+  } while (0)
 
 // ---- network geometry (reference model.py:20, 36-43) ------------------------
 constexpr int kLayers = 9;

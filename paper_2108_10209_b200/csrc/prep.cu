@@ -11,6 +11,7 @@ namespace n2f {
 // error plumbing
 // ---------------------------------------------------------------------------
 static thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
 
 void set_error(const std::string& msg) { g_err = msg; }
 const std::string& error_text() { return g_err; }
@@ -214,6 +215,7 @@ int launch_minmax(const void* img, int dtype, int64_t n, double* part, double* o
                   cudaStream_t st) {
   k_minmax_part<<<kScanBlocks, kThreads, 0, st>>>(img, dtype, n, part);
   k_minmax_final<<<1, 32, 0, st>>>(part, kScanBlocks, out3);
+  ++g_launches;
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
@@ -225,10 +227,12 @@ int launch_pairs(const void* img, int dtype, const void* clean, const double* mm
   const int64_t n = (int64_t)H * W;
   k_normalize<<<nblocks(n) < 2048 ? nblocks(n) : 2048, kThreads, 0, st>>>(img, dtype, n, mm, norm);
   const int64_t nq = (int64_t)(H / 2) * (W / 2);
-  if (nq > 0)
+  N2F_LAUNCH_CHECK();
+  if (nq > 0) {
     k_pairs<<<nblocks(nq), kThreads, 0, st>>>(norm, clean, dtype, mm, H, W, scheme, clip, pin, ptgt,
                                               plane);
-  N2F_LAUNCH_CHECK();
+    N2F_LAUNCH_CHECK();
+  }
   return N2F_OK;
 }
 

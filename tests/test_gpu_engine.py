@@ -42,10 +42,10 @@ def _prepare(eng, img, init_from_seed=1):
 
 
 def _image(h, w, seed=3, sigma=25 / 255):
-    from oracle import n2f_oracle as o
+    from paper_2108_10209_b200 import synthetic as s
 
-    clean = o.blob_rect_image(h, w, seed)
-    return o.gaussian_noisy(clean, sigma, seed + 1).astype(np.float64), clean
+    clean = s.blob_rect_image(h, w, seed)
+    return s.gaussian_noisy(clean, sigma, seed + 1).astype(np.float64), clean
 
 
 @pytest.mark.parametrize("hw", [(32, 32), (64, 48), (128, 128)])
@@ -77,7 +77,8 @@ def test_one_step_and_one_epoch(oracle, hw, loss):
         oracle.net_step(net, grads, 1e-3)
         z = np.empty(a.size, np.float32)
         _lib.call("n2f_ctx_step", eng.handle, k, z.ctypes.data)
-        assert norm_rel(z, z_ref.reshape(-1)) < 1e-4, k
+        # free-running trajectory: logits of later steps see the accumulated drift
+        assert norm_rel(z, z_ref.reshape(-1)) < (1e-4 if k == 0 else 3e-3), k
         if k == 0:
             g = arena_to_layers(_arena(eng, 3), shapes)
             for li, ((gw, gb), (rw, rb)) in enumerate(zip(g, grads)):
@@ -97,6 +98,56 @@ def test_one_step_and_one_epoch(oracle, hw, loss):
     ref = oracle.predict(net, n32)
     assert norm_rel(out.reshape(img.shape), ref) < 1e-3
     assert abs(score.value - oracle.val_score(ref, n32)) < 1e-3 * score.value
+
+
+def _oracle_arenas(net):
+    """(params, m, v) of the oracle net in the engine's arena layout."""
+    from n2f_testutil import oihw_to_engine
+
+    ps, ms, vs = [], [], []
+    for i, (w, b) in enumerate(zip(net.weights, net.biases)):
+        ps += [oihw_to_engine(w).ravel(), b]
+        ms += [oihw_to_engine(net.m[2 * i]).ravel(), net.m[2 * i + 1]]
+        vs += [oihw_to_engine(net.v[2 * i]).ravel(), net.v[2 * i + 1]]
+    return [np.ascontiguousarray(np.concatenate(x), dtype=np.float32) for x in (ps, ms, vs)]
+
+
+@pytest.mark.parametrize("hw", [(64, 48), (128, 128), (256, 256)])
+@pytest.mark.parametrize("loss", ["bce", "mse"])
+def test_fixed_weight_steps(oracle, hw, loss):
+    """Each of the 4 steps of an epoch from IDENTICAL state (weights, Adam
+    moments, t) on both sides: logits, gradients and the Adam update agree
+    within 1e-3 (per-layer norm-relative), isolating per-step error from the
+    chaotic drift of a free-running trajectory."""
+    from paper_2108_10209_b200 import _lib
+
+    img, _ = _image(*hw)
+    eng = _engine(*hw, seed=7, loss=loss)
+    _prepare(eng, img)
+    net = oracle.init_net(7)
+    n32 = oracle.normalize(img)[0].astype(np.float32)
+    shapes = oracle.layer_shapes()
+    for k, (a, b) in enumerate(oracle.training_pairs(n32)):
+        p, m, v = _oracle_arenas(net)
+        for which, arr in enumerate((p, m, v)):
+            _lib.call("n2f_ctx_set_arena", eng.handle, which, arr.ctypes.data, net.t)
+        z_ref, cache = oracle.net_forward(net, a, keep=True)
+        _, gz = (oracle.bce_logits if loss == "bce" else oracle.mse_sigmoid)(z_ref, b)
+        grads = oracle.net_backward(net, cache, gz)
+        oracle.net_step(net, grads, 1e-3)
+        z = np.empty(a.size, np.float32)
+        _lib.call("n2f_ctx_step", eng.handle, k, z.ctypes.data)
+        assert norm_rel(z, z_ref.reshape(-1)) < 1e-4, ("logits", k)
+        g = arena_to_layers(_arena(eng, 3), shapes)
+        got = arena_to_layers(_arena(eng, 0), shapes)
+        for li in range(len(shapes)):
+            (gw, gb), (rw, rb) = g[li], grads[li]
+            assert norm_rel(gw, rw) < 1e-3, ("grad w", k, li, norm_rel(gw, rw))
+            assert norm_rel(gb, rb) < 1e-3, ("grad b", k, li, norm_rel(gb, rb))
+            w, bb = got[li]
+            err = norm_rel(np.concatenate([w.ravel(), bb]),
+                           np.concatenate([net.weights[li].ravel(), net.biases[li]]))
+            assert err < 1e-3, ("params", k, li, err)
 
 
 def test_fit_api_errors_and_degenerate():
