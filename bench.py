@@ -215,32 +215,6 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 
-def measure_dominant_kernel(torch, stream, conv_impl, iters=20):
-    """The dominant kernel of the step: the 256->256 3x3 conv (L8) on a
-    training pair plane (512 x 256 px).  Times it on a dedicated stream with
-    CUDA events; returns (ms per launch, algorithmic FLOP per launch)."""
-    from paper_2108_10209_b200 import _lib
-
-    h, w, c = SIZE, SIZE // 2, 256
-    x = torch.rand(h * w * c, device="cuda")
-    wt = torch.randn(c * 9 * c, device="cuda") * 0.02
-    b = torch.zeros(c, device="cuda")
-    y = torch.empty(h * w * c, device="cuda")
-    for _ in range(3):
-        _lib.call("n2f_conv_fwd", x.data_ptr(), wt.data_ptr(), b.data_ptr(), y.data_ptr(), h, w, c,
-                  c, 3, 1, conv_impl, stream.cuda_stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(iters):
-        _lib.call("n2f_conv_fwd", x.data_ptr(), wt.data_ptr(), b.data_ptr(), y.data_ptr(), h, w, c,
-                  c, 3, 1, conv_impl, stream.cuda_stream)
-    e1.record(stream)
-    e1.synchronize()
-    ms = e0.elapsed_time(e1) / iters
-    flop = 2.0 * h * w * c * 9 * c
-    return ms, flop
-
-
 def run_ours(args):
     import torch
 
@@ -316,10 +290,18 @@ def run_ours(args):
     h2d = SIZE * SIZE * 4
     d2h = SIZE * SIZE * 8 + res.epochs_run * (8 + 32 + 8) + 64
 
-    # ---- dominant kernel roofline ------------------------------------------
+    # ---- dominant kernel roofline: one profiled epoch on the same engine and
+    # stream right after the timed region (CUDA events around every launch)
     peak_tf, peak_gbs, peak_kind = load_peaks()
-    kms, kflop = measure_dominant_kernel(torch, stream, args.conv_impl)
+    pms, pfl, pln = eng.profile_epoch()
+    ci, li = np.unravel_index(int(np.argmax(pms)), pms.shape)
+    kms = float(pms[ci, li] / max(1, pln[ci, li]))
+    kflop = float(pfl[ci, li] / max(1, pln[ci, li]))
     achieved = kflop / (kms * 1e-3) / 1e12
+    kname = f"{Engine.PROF_CLASSES[ci]} layer {li + 1} ({pln[ci, li]} launches/epoch)"
+    shares = {name: round(float(pms[i].sum() / pms.sum()), 4) for i, name in enumerate(Engine.PROF_CLASSES)}
+    epoch_ms_profiled = float(pms.sum())
+    conv_tf = float(pfl[[1, 3, 4, 8]].sum() / (pms[[1, 3, 4, 8]].sum() * 1e-3) / 1e12)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")) as f:
@@ -356,8 +338,11 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic,
-                         "kernel": "conv3x3 fwd 256->256 on a 512x256 pair plane (L8)",
-                         "kernel_ms": kms, "peak_kind": f"{peak_kind} bf16 dense burst",
+                         "kernel": kname, "kernel_ms": kms, "kernel_algorithmic_flop": kflop,
+                         "peak_kind": f"{peak_kind} bf16 dense burst; kernels issue 3 tf32 MMAs "
+                                      "(3xTF32 split precision) per algorithmic MAC",
+                         "conv_kernels_tflops": conv_tf, "epoch_ms_profiled": epoch_ms_profiled,
+                         "time_share": shares,
                          "path_tflops": path_tflops, "path_frac": path_tflops / peak_tf},
             "cpu_baseline": cpu,
             "clocks": clk,

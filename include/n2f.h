@@ -157,8 +157,18 @@ int n2f_ctx_param_count(n2f_ctx* ctx, int64_t* n);
 int n2f_ctx_get_arena(n2f_ctx* ctx, int which, float* host);
 int n2f_ctx_set_params(n2f_ctx* ctx, const float* host);
 int n2f_ctx_set_arena(n2f_ctx* ctx, int which, const float* host, int adam_step);
+/* tcgen05 self-test: D[128 x n] = A[128 x 32] . B[n x 32]^T through one
+ * kind::tf32 MMA chain with K-major (0) or MN-major (1) SWIZZLE_128B operands. */
+int n2f_tc_selftest(const float* a, const float* b, float* d, int n, int a_mn, int b_mn,
+                    void* stream);
 int n2f_ctx_step(n2f_ctx* ctx, int pair, float* logits_host);
 int n2f_ctx_epoch(n2f_ctx* ctx, int* stopped);
+/* Profile one epoch: per (class, layer) device ms / algorithmic FLOPs / launches
+ * in arrays of N2F_PROF_CLASSES * 9 (classes: 0 first-layer fwd, 1 conv fwd,
+ * 2 head+loss, 3 wgrad, 4 dgrad, 5 first-layer wgrad, 6 Adam, 7 validation
+ * first layer, 8 validation conv, 9 validation head, 10 stop rule). */
+#define N2F_PROF_CLASSES 11
+int n2f_ctx_profile_epoch(n2f_ctx* ctx, double* ms, double* flop, int* launches);
 int n2f_ctx_validate(n2f_ctx* ctx, float* out_host, double* score);
 int n2f_ctx_get_pairs(n2f_ctx* ctx, float* pair_in, float* pair_tgt, float* norm, int ph[4],
                       int pw[4]);

@@ -133,6 +133,19 @@ int n2f_conv_fwd(const float* x, const float* w, const float* b, float* y, int h
     N2F_LAUNCH_CHECK();
   } else if (k == 3 && cin == 1 && cout % 4 == 0) {
     N2F_TRY(conv_first_simt(x, w, b, y, h, wd, cout, S(stream), relu));
+  } else if (k == 3 && impl == kImplTc && tc_supported(cin, cout)) {
+    static Scratch s;  // kept alive across async calls on an explicit stream
+    for (void* q : s.ptrs) cudaFree(q);
+    s.ptrs.clear();
+    float *xlo, *wlo;
+    N2F_TRY(s.get(&xlo, (size_t)P * cin));
+    N2F_TRY(s.get(&wlo, (size_t)cout * 9 * cin));
+    N2F_TRY(split_lo(x, xlo, P * cin, S(stream)));
+    N2F_TRY(split_lo(w, wlo, (int64_t)cout * 9 * cin, S(stream)));
+    ConvTcPlan pl;
+    N2F_TRY(conv_tc_plan(&pl, x, xlo, w, wlo, h, wd, cin, cout));
+    N2F_TRY(conv_tc_launch(pl, b, nullptr, y, nullptr, nullptr, relu ? kEpiBiasRelu : kEpiBias,
+                           S(stream)));
   } else if (k == 3 && cin % 8 == 0 && cout % 32 == 0) {
     N2F_TRY(conv3x3_simt(x, w, b, nullptr, y, h, wd, cin, cout, relu ? kEpiBiasRelu : kEpiBias,
                          S(stream)));
@@ -174,14 +187,39 @@ int n2f_conv_bwd(const float* g, const float* x, const float* w, const float* ma
       N2F_TRY(wgrad3x3_simt(g, x, pw, pb, h, wd, cin, cout, ns, S(stream)));
     if (dw) N2F_TRY(reduce_partials(pw, dw, ns, (int64_t)cout * 9 * cin, S(stream)));
     if (db) N2F_TRY(reduce_partials(pb, db, ns, cout, S(stream)));
+    if (dw && impl == kImplTc && tc_supported(cin, cout)) {  // dW on the tensor cores
+      const int nst = wgrad_tc_nsplit(cin, h, wd);
+      float *xlo, *glo, *ptc;
+      N2F_TRY(s.get(&xlo, (size_t)P * cin));
+      N2F_TRY(s.get(&glo, (size_t)P * cout));
+      N2F_TRY(s.get(&ptc, (size_t)nst * cout * 9 * cin));
+      N2F_TRY(split_lo(x, xlo, P * cin, S(stream)));
+      N2F_TRY(split_lo(g, glo, P * cout, S(stream)));
+      WgradTcPlan pl;
+      N2F_TRY(wgrad_tc_plan(&pl, x, xlo, g, glo, h, wd, cin, cout, nst));
+      N2F_TRY(wgrad_tc_launch(pl, ptc, S(stream)));
+      N2F_TRY(reduce_partials(ptc, dw, nst, (int64_t)cout * 9 * cin, S(stream)));
+    }
   }
   if (dx) {
     if (cout % 8 || cin % 32) return fail(N2F_ERR_UNSUPPORTED, "dgrad: cin %d cout %d", cin, cout);
     float* wt;
     N2F_TRY(s.get(&wt, (size_t)cout * 9 * cin));
     N2F_TRY(transpose_dgrad_weights(w, wt, cin, cout, S(stream)));
-    N2F_TRY(conv3x3_simt(g, wt, nullptr, mask, dx, h, wd, cout, cin, mask ? kEpiMask : kEpiNone,
-                         S(stream)));
+    if (impl == kImplTc && tc_supported(cout, cin)) {
+      float *glo, *wtlo;
+      N2F_TRY(s.get(&glo, (size_t)P * cout));
+      N2F_TRY(s.get(&wtlo, (size_t)cout * 9 * cin));
+      N2F_TRY(split_lo(g, glo, P * cout, S(stream)));
+      N2F_TRY(split_lo(wt, wtlo, (int64_t)cout * 9 * cin, S(stream)));
+      ConvTcPlan pl;
+      N2F_TRY(conv_tc_plan(&pl, g, glo, wt, wtlo, h, wd, cout, cin));
+      N2F_TRY(conv_tc_launch(pl, nullptr, mask, dx, nullptr, nullptr, mask ? kEpiMask : kEpiNone,
+                             S(stream)));
+    } else {
+      N2F_TRY(conv3x3_simt(g, wt, nullptr, mask, dx, h, wd, cout, cin, mask ? kEpiMask : kEpiNone,
+                           S(stream)));
+    }
   }
   N2F_CUDA(cudaStreamSynchronize(S(stream)));
   return N2F_OK;

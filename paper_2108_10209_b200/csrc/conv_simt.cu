@@ -13,6 +13,7 @@
 //   wgrad   : dw[o][tap][c] = sum_p g[p][o] * x[p+d(tap)][c]  (deterministic
 //             split over pixels: partial sums per split, reduced in fixed order)
 #include "n2f_internal.cuh"
+#include "tc_common.cuh"
 
 namespace n2f {
 namespace {
@@ -139,7 +140,8 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
     k_conv_first(const float* __restrict__ x, const float* __restrict__ w,
-                 const float* __restrict__ b, float* __restrict__ y, int H, int W, int N, int relu) {
+                 const float* __restrict__ b, float* __restrict__ y, float* __restrict__ ylo, int H,
+                 int W, int N, int relu) {
   __shared__ float ws[kMaxC * 9];
   __shared__ float bs[kMaxC];
   for (int i = threadIdx.x; i < N * 9; i += blockDim.x) ws[i] = w[i];
@@ -168,6 +170,12 @@ __global__ void __launch_bounds__(kThreads)
     o[j] = relu ? fmaxf(a + bs[n], 0.f) : a + bs[n];
   }
   *reinterpret_cast<float4*>(y + (size_t)p * N + 4 * q) = make_float4(o[0], o[1], o[2], o[3]);
+  if (ylo) {  // tf32 residuals for a tcgen05 consumer
+    float l[4], hh;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tc::split_tf32(o[j], hh, l[j]);
+    *reinterpret_cast<float4*>(ylo + (size_t)p * N + 4 * q) = make_float4(l[0], l[1], l[2], l[3]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -354,11 +362,11 @@ int conv3x3_simt(const float* x, const float* wk, const float* bias, const float
 }
 
 int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
-                    int cout, cudaStream_t st, int relu) {
+                    int cout, cudaStream_t st, int relu, float* ylo) {
   if (cout % 4 || cout > kMaxC) return fail(N2F_ERR_ARG, "conv_first: cout %d", cout);
   const int64_t total = (int64_t)h * w_ * (cout / 4);
-  k_conv_first<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, st>>>(x, w, b, y, h,
-                                                                                  w_, cout, relu);
+  k_conv_first<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+      x, w, b, y, ylo, h, w_, cout, relu);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

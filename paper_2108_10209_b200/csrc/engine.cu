@@ -83,6 +83,35 @@ struct n2f_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   AdamArgs adam{};
   int64_t epoch_launches = 0;  // kernels in one captured epoch body
+
+  // tcgen05 path: tf32 residual companions of every tensor-core operand,
+  // TMA plans per (shape class, layer), Adam descriptors per shape class
+  bool tc = false;
+  float* params_lo = nullptr;
+  float* wt_lo[kLayers]{};
+  float* act_lo[kLayers]{};
+  float* gA_lo = nullptr;
+  float* gB_lo = nullptr;
+  float* vA_lo = nullptr;
+  float* vB_lo = nullptr;
+  ConvTcPlan fwd_plan[2][kLayers]{};
+  ConvTcPlan dgrad_plan[2][kLayers]{};
+  ConvTcPlan val_plan[kLayers]{};
+  WgradTcPlan wgrad_plan[2][kLayers]{};
+  AdamArgs adam_sc[2]{};
+  // profiling
+  struct Mark {
+    int cls, li;
+    double flop;
+    cudaEvent_t a, b;
+  };
+  bool prof = false;
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  int bias_tiles[2]{};
+  int wsplit[2][kLayers]{};
+  int last_sc = 0;  // shape class of the last enqueued step (parity readback)
 };
 
 namespace {
@@ -113,9 +142,107 @@ int conv3x3(n2f_ctx* c, const float* x, const float* wk, const float* bias, cons
   return conv3x3_simt(x, wk, bias, mask, y, h, w, cin, cout, epi, c->stream);
 }
 
+// training-plane shape class of pair k (checkerboard: up pairs 0,1 vs left 2,3)
+int shape_class(const n2f_ctx* c, int k) {
+  return (c->ph[k] == c->ph[0] && c->pw[k] == c->pw[0]) ? 0 : 1;
+}
+
+// ---- per-kernel-class profiling (CUDA events around each launch, host loop)
+enum ProfClass {
+  kPFirst = 0, kPFwd, kPHead, kPWgrad, kPDgrad, kPWgradFirst, kPAdam, kPValFirst, kPValConv,
+  kPHeadVal, kPStop, kPClasses
+};
+
+cudaEvent_t prof_event(n2f_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+
+// Run `call` (returns a status); when profiling, bracket it with events and
+// charge the algorithmic FLOPs to (class, layer).
+#define PROF(cls, li, flop, call)                                   \
+  do {                                                              \
+    cudaEvent_t a_ = nullptr;                                       \
+    if (c->prof) {                                                  \
+      a_ = prof_event(c);                                           \
+      cudaEventRecord(a_, c->stream);                               \
+    }                                                               \
+    N2F_TRY(call);                                                  \
+    if (c->prof) {                                                  \
+      cudaEvent_t b_ = prof_event(c);                               \
+      cudaEventRecord(b_, c->stream);                               \
+      c->marks.push_back({(int)(cls), (int)(li), (double)(flop), a_, b_}); \
+    }                                                               \
+  } while (0)
+
+double conv_flop(int64_t P, int li) { return 2.0 * P * kCout[li] * kKsz[li] * kKsz[li] * kCin[li]; }
+
+// tcgen05 variant of a training step: L2..L8 forward and dgrad on the tensor
+// cores (3xTF32), bias gradients as fused column sums of each layer's
+// pre-activation gradient, wgrad still on the SIMT kernels.
+int enqueue_step_tc(n2f_ctx* c, int k) {
+  cudaStream_t st = c->stream;
+  const int sc = shape_class(c, k);
+  c->last_sc = sc;
+  const int h = c->ph[k], w = c->pw[k];
+  const int64_t P = (int64_t)h * w;
+  const float* x0 = c->pin + k * c->plane;
+  const float* tgt = c->ptgt + k * c->plane;
+  PROF(kPFirst, 0, conv_flop(P, 0),
+       conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1, c->act_lo[0]));
+  for (int li = 1; li < 8; ++li)
+    PROF(kPFwd, li, conv_flop(P, li),
+         conv_tc_launch(c->fwd_plan[sc][li], B_(c, li), nullptr, c->act[li],
+                        li < 7 ? c->act_lo[li] : nullptr, nullptr, kEpiBiasRelu, st));
+  PROF(kPHead, 8, 6.0 * P * kMaxC,
+       launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, c->gA, c->part_w[8], c->part_b[8],
+                         c->part_loss + (int64_t)k * c->nblk_head, c->z, P, c->nblk_head,
+                         c->cfg.loss, c->step_counter, st, c->gA_lo, c->part_b[7]));
+  float* g = c->gA;
+  float* gn = c->gB;
+  float* gnl = c->gB_lo;
+  for (int li = 7; li >= 1; --li) {
+    PROF(kPWgrad, li, conv_flop(P, li), wgrad_tc_launch(c->wgrad_plan[sc][li], c->part_w[li], st));
+    PROF(kPDgrad, li, conv_flop(P, li),
+         conv_tc_launch(c->dgrad_plan[sc][li], nullptr, c->act[li - 1], gn, li > 1 ? gnl : nullptr,
+                        li > 1 ? c->part_b[li - 1] : nullptr, kEpiMask, st));
+    float* t = g;
+    g = gn;
+    gn = t;
+    gnl = (gnl == c->gB_lo) ? c->gA_lo : c->gB_lo;
+  }
+  PROF(kPWgradFirst, 0, conv_flop(P, 0),
+       wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
+  PROF(kPAdam, 0, 0.0, launch_adam(c->adam_sc[sc], c->step_counter, 0, st));
+  return N2F_OK;
+}
+
+int enqueue_validate_tc(n2f_ctx* c) {
+  cudaStream_t st = c->stream;
+  PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
+       conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1, c->vA_lo));
+  for (int li = 1; li < 8; ++li) {
+    float* out = (li & 1) ? c->vB : c->vA;
+    float* outl = (li & 1) ? c->vB_lo : c->vA_lo;
+    PROF(kPValConv, li, conv_flop(c->Pv, li),
+         conv_tc_launch(c->val_plan[li], B_(c, li), nullptr, out, li < 7 ? outl : nullptr, nullptr,
+                        kEpiBiasRelu, st));
+  }
+  // layer 7 (odd) wrote vB
+  PROF(kPHeadVal, 8, 2.0 * c->Pv * kMaxC,
+       launch_head_val(c->vB, W_(c, 8), B_(c, 8), c->norm, c->ring, c->Pv, c->nblk_val, c->dstate,
+                       c->cfg.avg_window, c->part_se, st));
+  return N2F_OK;
+}
+
 // One training step on pair k: forward, fused head/loss/head-backward,
 // backward through L8..L1 (wgrad partials + masked dgrad), Adam.
 int enqueue_step(n2f_ctx* c, int k) {
+  if (c->tc) return enqueue_step_tc(c, k);
   cudaStream_t st = c->stream;
   const int h = c->ph[k], w = c->pw[k];
   const int64_t P = (int64_t)h * w;
@@ -146,6 +273,7 @@ int enqueue_step(n2f_ctx* c, int k) {
 
 // Full-resolution validation forward + head (writes the ring slot + se partials).
 int enqueue_validate(n2f_ctx* c) {
+  if (c->tc) return enqueue_validate_tc(c);
   cudaStream_t st = c->stream;
   const int h = c->H, w = c->W;
   N2F_TRY(conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, h, w, kCout[0], st));
@@ -166,9 +294,10 @@ int enqueue_epoch(n2f_ctx* c, int use_handle) {
   for (int k = 0; k < 4; ++k) N2F_TRY(enqueue_step(c, k));
   N2F_TRY(enqueue_validate(c));
   const double pt[4] = {(double)c->Pt, (double)c->Pt, (double)c->Pt, (double)c->Pt};
-  N2F_TRY(launch_stop(c->dstate, c->part_se, c->nblk_val, (double)c->Pv, c->part_loss,
-                      c->nblk_head, pt, c->val_hist, c->loss_hist, c->time_hist,
-                      c->cfg.patience_epochs, c->cfg.max_epochs, c->handle, use_handle, c->stream));
+  PROF(kPStop, 0, 0.0,
+       launch_stop(c->dstate, c->part_se, c->nblk_val, (double)c->Pv, c->part_loss, c->nblk_head,
+                   pt, c->val_hist, c->loss_hist, c->time_hist, c->cfg.patience_epochs,
+                   c->cfg.max_epochs, c->handle, use_handle, c->stream));
   return N2F_OK;
 }
 
@@ -253,9 +382,56 @@ int setup(n2f_ctx* c) {
   c->nblk_val = nblocks_for(c->Pv, 64);
   for (int li = 0; li < 8; ++li) c->nsplit[li] = wgrad_nsplit(c->Pt, kCin[li], kCout[li]);
   c->nsplit[8] = c->nblk_head;
+  // TC mode: the bias gradient of layer li (1..6) is a per-tile column sum
+  // written by the dgrad of layer li+1, L8's by the fused head
+  int tiles[2] = {conv_tc_tiles(c->ph[0], c->pw[0]), conv_tc_tiles(c->ph[2], c->pw[2])};
+  const int max_tiles = tiles[0] > tiles[1] ? tiles[0] : tiles[1];
+  int wsplit[2][kLayers] = {};  // tcgen05 wgrad split-K per shape class
+  for (int sc = 0; sc < 2; ++sc)
+    for (int li = 1; li < 8; ++li) wsplit[sc][li] = wgrad_tc_nsplit(kCin[li], c->ph[2 * sc], c->pw[2 * sc]);
   for (int li = 0; li < kLayers; ++li) {
-    N2F_TRY(dalloc(c, &c->part_w[li], (int64_t)c->nsplit[li] * c->pnum[2 * li]));
-    N2F_TRY(dalloc(c, &c->part_b[li], (int64_t)c->nsplit[li] * c->pnum[2 * li + 1]));
+    int64_t nb = c->nsplit[li], nw = c->nsplit[li];
+    if (c->tc && li >= 1 && li <= 6 && max_tiles > nb) nb = max_tiles;
+    if (c->tc && li == 7 && c->nblk_head > nb) nb = c->nblk_head;
+    if (c->tc && li >= 1 && li <= 7) {
+      nw = wsplit[0][li] > wsplit[1][li] ? wsplit[0][li] : wsplit[1][li];
+      if (c->nsplit[li] > nw) nw = c->nsplit[li];
+    }
+    N2F_TRY(dalloc(c, &c->part_w[li], nw * c->pnum[2 * li]));
+    N2F_TRY(dalloc(c, &c->part_b[li], nb * c->pnum[2 * li + 1]));
+  }
+  if (c->tc) {
+    N2F_TRY(dalloc(c, &c->params_lo, c->ptotal));
+    for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt_lo[li], c->pnum[2 * li]));
+    for (int li = 0; li < 7; ++li) N2F_TRY(dalloc(c, &c->act_lo[li], c->Pt * kCout[li]));
+    N2F_TRY(dalloc(c, &c->gA_lo, c->Pt * kMaxC));
+    N2F_TRY(dalloc(c, &c->gB_lo, c->Pt * kMaxC));
+    N2F_TRY(dalloc(c, &c->vA_lo, c->Pv * kMaxC));
+    N2F_TRY(dalloc(c, &c->vB_lo, c->Pv * kMaxC));
+    for (int sc = 0; sc < 2; ++sc) {
+      const int h = c->ph[2 * sc], w = c->pw[2 * sc];
+      for (int li = 1; li < 8; ++li) {
+        N2F_TRY(conv_tc_plan(&c->fwd_plan[sc][li], c->act[li - 1], c->act_lo[li - 1],
+                             c->params + c->poff[2 * li], c->params_lo + c->poff[2 * li], h, w,
+                             kCin[li], kCout[li]));
+        const bool odd = li & 1;  // L8 (li 7) reads gA (head output), then alternate
+        N2F_TRY(conv_tc_plan(&c->dgrad_plan[sc][li], odd ? c->gA : c->gB, odd ? c->gA_lo : c->gB_lo,
+                             c->wt[li], c->wt_lo[li], h, w, kCout[li], kCin[li]));
+        N2F_TRY(wgrad_tc_plan(&c->wgrad_plan[sc][li], c->act[li - 1], c->act_lo[li - 1],
+                              odd ? c->gA : c->gB, odd ? c->gA_lo : c->gB_lo, h, w, kCin[li],
+                              kCout[li], wsplit[sc][li]));
+      }
+    }
+    for (int sc = 0; sc < 2; ++sc)
+      for (int li = 1; li < 8; ++li) c->wsplit[sc][li] = wsplit[sc][li];
+    for (int li = 1; li < 8; ++li) {
+      const bool odd = li & 1;  // L1 writes vA; layer li reads vA when li is odd
+      N2F_TRY(conv_tc_plan(&c->val_plan[li], odd ? c->vA : c->vB, odd ? c->vA_lo : c->vB_lo,
+                           c->params + c->poff[2 * li], c->params_lo + c->poff[2 * li], c->H, c->W,
+                           kCin[li], kCout[li]));
+    }
+    c->bias_tiles[0] = tiles[0];
+    c->bias_tiles[1] = tiles[1];
   }
   N2F_TRY(dalloc(c, &c->part_loss, 4 * (int64_t)c->nblk_head));
   N2F_TRY(dalloc(c, &c->part_se, c->nblk_val));
@@ -309,6 +485,19 @@ int setup(n2f_ctx* c) {
       T.cout = kCout[li];
     }
   }
+  if (c->tc) {
+    a.plo = c->params_lo;
+    for (int li = 1; li < 8; ++li) {
+      a.t[2 * li].want_lo = 1;
+      a.t[2 * li].wtlo = c->wt_lo[li];
+    }
+    for (int sc = 0; sc < 2; ++sc) {
+      c->adam_sc[sc] = a;
+      for (int li = 1; li <= 6; ++li) c->adam_sc[sc].t[2 * li + 1].nsplit = c->bias_tiles[sc];
+      c->adam_sc[sc].t[2 * 7 + 1].nsplit = c->nblk_head;
+      for (int li = 1; li <= 7; ++li) c->adam_sc[sc].t[2 * li].nsplit = c->wsplit[sc][li];
+    }
+  }
 
   N2F_CUDA(cudaMallocHost(&c->h_mm, 4 * sizeof(double)));
   N2F_CUDA(cudaMallocHost(&c->h_state, sizeof(DevState)));
@@ -336,6 +525,11 @@ int refresh_derived(n2f_ctx* c) {
   for (int li = 1; li < 8; ++li)
     N2F_TRY(transpose_dgrad_weights(c->params + c->poff[2 * li], c->wt[li], kCin[li], kCout[li],
                                     c->stream));
+  if (c->tc) {
+    N2F_TRY(split_lo(c->params, c->params_lo, c->ptotal, c->stream));
+    for (int li = 1; li < 8; ++li)
+      N2F_TRY(split_lo(c->wt[li], c->wt_lo[li], c->pnum[2 * li], c->stream));
+  }
   return N2F_OK;
 }
 
@@ -412,8 +606,10 @@ int n2f_create(int device, int height, int width, const n2f_config* cfg, n2f_ctx
   N2F_TRY(check_cfg(cfg));
   if (height < 4 || width < 4)
     return fail(N2F_ERR_ARG, "image must be at least 4x4, got (%d, %d)", height, width);
-  if (cfg->conv_impl == kImplTc) return fail(N2F_ERR_UNSUPPORTED, "tcgen05 conv path not built yet");
+  if (cfg->conv_impl < kImplAuto || cfg->conv_impl > kImplTc)
+    return fail(N2F_ERR_ARG, "conv_impl must be 0 (auto), 1 (SIMT) or 2 (tcgen05)");
   n2f_ctx* c = new n2f_ctx();
+  c->tc = cfg->conv_impl != kImplSimt;  // auto = tcgen05
   c->device = device;
   c->H = height;
   c->W = width;
@@ -434,6 +630,7 @@ int n2f_destroy(n2f_ctx* c) {
   if (c->exec) cudaGraphExecDestroy(c->exec);
   if (c->graph) cudaGraphDestroy(c->graph);
   for (void* p : c->allocs) cudaFree(p);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->h_mm) cudaFreeHost(c->h_mm);
   if (c->h_state) cudaFreeHost(c->h_state);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -560,8 +757,9 @@ int n2f_ctx_get_arena(n2f_ctx* c, int which, float* host) {
   }
   float* tmp = nullptr;
   N2F_CUDA(cudaMalloc(&tmp, c->ptotal * 4));
+  const AdamArgs& args = c->tc ? c->adam_sc[c->last_sc] : c->adam;
   for (int q = 0; q < 2 * kLayers; ++q) {
-    const AdamTensor& T = c->adam.t[q];
+    const AdamTensor& T = args.t[q];
     int s = reduce_partials(T.part, tmp + T.off, T.nsplit, T.n, c->stream);
     if (s != N2F_OK) {
       cudaFree(tmp);
@@ -608,6 +806,34 @@ int n2f_ctx_step(n2f_ctx* c, int pair, float* logits_host) {
   if (logits_host)
     N2F_CUDA(cudaMemcpyAsync(logits_host, c->z, c->Pt * 4, cudaMemcpyDeviceToHost, c->stream));
   N2F_CUDA(cudaStreamSynchronize(c->stream));
+  return N2F_OK;
+}
+
+// One epoch with CUDA events around every launch (host loop, same stream):
+// per (kernel class, layer) total device ms, algorithmic FLOPs and launch
+// counts, arrays of N2F_PROF_CLASSES x 9.  Continues the current training.
+int n2f_ctx_profile_epoch(n2f_ctx* c, double* ms, double* flop, int* launches) {
+  if (!c || !ms || !flop || !launches) return fail(N2F_ERR_ARG, "null argument");
+  c->marks.clear();
+  c->ev_used = 0;
+  c->prof = true;
+  int s = enqueue_epoch(c, 0);
+  c->prof = false;
+  if (s != N2F_OK) return s;
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < kPClasses * kLayers; ++i) {
+    ms[i] = 0.0;
+    flop[i] = 0.0;
+    launches[i] = 0;
+  }
+  for (const auto& m : c->marks) {
+    float t = 0.f;
+    N2F_CUDA(cudaEventElapsedTime(&t, m.a, m.b));
+    const int i = m.cls * kLayers + m.li;
+    ms[i] += t;
+    flop[i] += m.flop;
+    launches[i] += 1;
+  }
   return N2F_OK;
 }
 

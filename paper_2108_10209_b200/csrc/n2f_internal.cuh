@@ -1,6 +1,7 @@
 // Internal declarations shared by the libn2f translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -57,18 +58,35 @@ enum Epi { kEpiBiasRelu = 0, kEpiMask = 1, kEpiBias = 2, kEpiNone = 3 };
 int conv3x3_simt(const float* x, const float* wk, const float* bias, const float* mask, float* y,
                  int h, int w, int cin, int cout, int epi, cudaStream_t st);
 int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
-                    int cout, cudaStream_t st, int relu = 1);
+                    int cout, cudaStream_t st, int relu = 1, float* ylo = nullptr);
 int wgrad3x3_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
                   int cin, int cout, int nsplit, cudaStream_t st);
 int wgrad_first_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
                      int cout, int nsplit, cudaStream_t st);
 int wgrad_nsplit(int64_t pixels, int cin, int cout);
 
-// tcgen05 kernels (conv_tc.cu)
-int conv3x3_tc(const float* x, const float* wk_hi, const float* wk_lo, const float* bias,
-               const float* mask, float* y, int h, int w, int cin, int cout, int epi,
-               cudaStream_t st);
+// tcgen05 kernels (conv_tc.cu).  A plan holds the TMA descriptors of one
+// (input buffer, weight buffer, shape) combination; it is built once and
+// launched many times (graph-capturable: maps are kernel parameters).
+struct ConvTcPlan {
+  CUtensorMap mx, mxl, mw, mwl;
+  int H, W, C, N, grid;
+};
 bool tc_supported(int cin, int cout);
+int conv_tc_plan(ConvTcPlan* pl, const float* x, const float* xlo, const float* w, const float* wlo,
+                 int H, int W, int C, int N);
+int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const float* mask, float* y, float* ylo,
+                   float* colsum, int epi, cudaStream_t st);
+int conv_tc_tiles(int H, int W);
+struct WgradTcPlan {
+  CUtensorMap mx, mxl, mg, mgl;
+  int H, W, C, N, mblocks, nsplit;
+};
+int wgrad_tc_nsplit(int cin, int H, int W);
+int wgrad_tc_plan(WgradTcPlan* pl, const float* x, const float* xlo, const float* g, const float* glo,
+                  int H, int W, int C, int N, int nsplit);
+int wgrad_tc_launch(const WgradTcPlan& pl, float* part, cudaStream_t st);
+int split_lo(const float* x, float* lo, int64_t n, cudaStream_t st);
 
 // utility kernels (prep.cu / train.cu)
 int reduce_partials(const float* part, float* out, int nsplit, int64_t n, cudaStream_t st);

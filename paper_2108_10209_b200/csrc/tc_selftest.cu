@@ -1,0 +1,108 @@
+// tcgen05 self-test (n2f_tc_selftest): D[128 x N] = A[128 x 32] . B[N x 32]^T
+// with operands staged by threads in the canonical UMMA layouts, four
+// kind::tf32 MMAs (K = 8 each), read back with tcgen05.ld.  It pins the
+// descriptor encodings (K-major SWIZZLE_128B, MN-major SWIZZLE_128B_BASE32B)
+// and shows how the tensor core converts fp32 inputs (it truncates to tf32).
+#include "n2f_internal.cuh"
+#include "tc_common.cuh"
+
+namespace n2f {
+namespace {
+
+using namespace tc;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// operand modes: 0 = K-major SW128, 1 = MN-major SW128, 2 = MN-major SW128_BASE32B
+__device__ __forceinline__ uint32_t operand_offset(int mode, int row, int k) {
+  if (mode == 0) return sw128_offset(row, 4 * k);
+  if (mode == 1) return (row / 32) * 4096 + sw128_offset(k, 4 * (row % 32));
+  return (row / 32) * 4096 + sw128b32_offset(k, 4 * (row % 32));
+}
+__device__ __forceinline__ uint64_t operand_desc(int mode, uint32_t base, int s) {
+  if (mode == 0) return sw128_desc(base + s * 32, 16, 1024);
+  if (mode == 1) return sw128_desc(base + s * 1024, 4096, 1024);
+  return sw128_desc(base + s * 1024, 4096, 512, kLayoutSw128Base32);
+}
+
+template <int AM, int BM>
+__global__ void __launch_bounds__(128) k_tc_selftest(const float* __restrict__ A,
+                                                     const float* __restrict__ B,
+                                                     float* __restrict__ D, int N) {
+  constexpr bool A_MN = AM != 0, B_MN = BM != 0;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* base = align1024(smem_raw);
+  uint8_t* sA = base;
+  uint8_t* sB = base + 16384;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 128 * 32; i += 128)
+    *reinterpret_cast<float*>(sA + operand_offset(AM, i / 32, i % 32)) = A[i];
+  for (int i = tid; i < N * 32; i += 128)
+    *reinterpret_cast<float*>(sB + operand_offset(BM, i / 32, i % 32)) = B[i];
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<256>(&tslot);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t taddr = tslot;
+  if (tid == 0) {
+    const uint32_t idesc = idesc_tf32(128, N, A_MN, B_MN);
+    for (int s = 0; s < 4; ++s)
+      mma_tf32(taddr, operand_desc(AM, smem_u32(sA), s), operand_desc(BM, smem_u32(sB), s), idesc,
+               s > 0);
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld32(taddr + ((uint32_t)(warp * 32) << 16) + c0, r);
+    tmem_ld_wait();
+    for (int j = 0; j < 32; ++j) D[(warp * 32 + lane) * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(taddr);
+}
+
+}  // namespace
+}  // namespace n2f
+
+using namespace n2f;
+
+extern "C" int n2f_tc_selftest(const float* A, const float* B, float* D, int N, int a_mn, int b_mn,
+                               void* stream) {
+  if (N < 32 || N > 256 || N % 32) return fail(N2F_ERR_ARG, "selftest N=%d", N);
+  if (a_mn < 0 || a_mn > 2 || b_mn < 0 || b_mn > 2) return fail(N2F_ERR_ARG, "selftest modes");
+  const int smem = 1024 + 16384 + N * 128;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto launch = [&](auto kern) -> int {
+    N2F_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<1, 128, smem, st>>>(A, B, D, N);
+    N2F_LAUNCH_CHECK();
+    return N2F_OK;
+  };
+  int s = N2F_OK;
+  switch (a_mn * 3 + b_mn) {
+    case 0: s = launch(k_tc_selftest<0, 0>); break;
+    case 1: s = launch(k_tc_selftest<0, 1>); break;
+    case 2: s = launch(k_tc_selftest<0, 2>); break;
+    case 3: s = launch(k_tc_selftest<1, 0>); break;
+    case 4: s = launch(k_tc_selftest<1, 1>); break;
+    case 5: s = launch(k_tc_selftest<1, 2>); break;
+    case 6: s = launch(k_tc_selftest<2, 0>); break;
+    case 7: s = launch(k_tc_selftest<2, 1>); break;
+    default: s = launch(k_tc_selftest<2, 2>); break;
+  }
+  if (s != N2F_OK) return s;
+  N2F_CUDA(cudaStreamSynchronize(st));
+  return N2F_OK;
+}

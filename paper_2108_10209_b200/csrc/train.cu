@@ -2,6 +2,7 @@
 // tail, multi-tensor Adam with fused deterministic split-K reduction, the
 // device-side early-stopping state machine and the output window mean.
 #include "n2f_internal.cuh"
+#include "tc_common.cuh"
 #include "train.cuh"
 
 namespace n2f {
@@ -48,8 +49,13 @@ __global__ void __launch_bounds__(kThreads)
                  const float* __restrict__ b9, const float* __restrict__ tgt,
                  float* __restrict__ gp8, float* __restrict__ part_w, float* __restrict__ part_b,
                  double* __restrict__ part_loss, float* __restrict__ zout, int64_t P, int chunk,
-                 int loss, int* __restrict__ step_counter) {
+                 int loss, int* __restrict__ step_counter, float* __restrict__ gp8lo,
+                 float* __restrict__ colsum) {
   __shared__ float red_w[kWarps][kMaxC];
+  __shared__ float red_c[kWarps][kMaxC];
+  float gcs[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) gcs[c] = 0.f;
   __shared__ float red_b[kWarps];
   __shared__ double red_l[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -89,6 +95,16 @@ __global__ void __launch_bounds__(kThreads)
     float* grow = gp8 + p * kMaxC + 8 * lane;
     *reinterpret_cast<float4*>(grow) = make_float4(g[0], g[1], g[2], g[3]);
     *reinterpret_cast<float4*>(grow + 4) = make_float4(g[4], g[5], g[6], g[7]);
+    if (gp8lo) {  // tf32 residuals for the tcgen05 dgrad of L8
+      float l[8], hh;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) tc::split_tf32(g[c], hh, l[c]);
+      float* lrow = gp8lo + p * kMaxC + 8 * lane;
+      *reinterpret_cast<float4*>(lrow) = make_float4(l[0], l[1], l[2], l[3]);
+      *reinterpret_cast<float4*>(lrow + 4) = make_float4(l[4], l[5], l[6], l[7]);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) gcs[c] += g[c];
     if (lane == 0) {
       gb += dz;
       lsum += (double)elem;
@@ -96,7 +112,10 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
 #pragma unroll
-  for (int c = 0; c < 8; ++c) red_w[warp][8 * lane + c] = gw[c];
+  for (int c = 0; c < 8; ++c) {
+    red_w[warp][8 * lane + c] = gw[c];
+    red_c[warp][8 * lane + c] = gcs[c];
+  }
   if (lane == 0) {
     red_b[warp] = gb;
     red_l[warp] = lsum;
@@ -104,9 +123,13 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   {
     const int c = threadIdx.x;  // kThreads == kMaxC
-    float s = red_w[0][c];
-    for (int k = 1; k < kWarps; ++k) s += red_w[k][c];
+    float s = red_w[0][c], t = red_c[0][c];
+    for (int k = 1; k < kWarps; ++k) {
+      s += red_w[k][c];
+      t += red_c[k][c];
+    }
     part_w[(int64_t)blockIdx.x * kMaxC + c] = s;
+    if (colsum) colsum[(int64_t)blockIdx.x * kMaxC + c] = t;  // bias grad of L8
   }
   if (threadIdx.x == 0) {
     float sb = red_b[0];
@@ -202,11 +225,16 @@ __global__ void __launch_bounds__(kThreads)
   args.m[i] = m;
   args.v[i] = v;
   args.p[i] = p;
+  float hi, lo = 0.f;
+  if (T.want_lo || T.wtlo) tc::split_tf32(p, hi, lo);
+  if (T.want_lo) args.plo[i] = lo;  // tf32 residual of the forward operand
   if (T.wt) {  // wt[c][8-tap][o] = w[o][tap][c]
     const int c = (int)(j % T.cin);
     const int tap = (int)((j / T.cin) % 9);
     const int o = (int)(j / ((int64_t)T.cin * 9));
-    T.wt[((int64_t)c * 9 + (8 - tap)) * T.cout + o] = p;
+    const int64_t q = ((int64_t)c * 9 + (8 - tap)) * T.cout + o;
+    T.wt[q] = p;
+    if (T.wtlo) T.wtlo[q] = lo;
   }
 }
 
@@ -369,10 +397,11 @@ __global__ void k_reset_state(DevState* st) {
 // ---- launchers ---------------------------------------------------------------
 int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
                       float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
-                      int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st) {
+                      int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st,
+                      float* gp8lo, float* colsum) {
   const int chunk = (int)((P + nblk - 1) / nblk);
   k_head_train<<<nblk, kThreads, 0, st>>>(a8, w9, b9, tgt, gp8, part_w, part_b, part_loss, zout, P,
-                                          chunk, loss, step_counter);
+                                          chunk, loss, step_counter, gp8lo, colsum);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

@@ -26,6 +26,8 @@ struct AdamTensor {
   const float* part;  // [nsplit][n] gradient partials
   int nsplit;
   float* wt;          // optional dgrad-transposed copy (3x3 weights), else null
+  float* wtlo;        // optional tf32 residual of wt
+  int want_lo;        // write the tf32 residual of p into AdamArgs::plo
   int cin, cout;
 };
 
@@ -36,6 +38,7 @@ struct AdamArgs {
   int ntensors;
   int64_t total;
   float* p;
+  float* plo;  // tf32 residual arena (same layout as p), for tensors with want_lo
   float* m;
   float* v;
   const float* bc1;  // fl32(1 - beta1^t), t = 1..table_len
@@ -46,7 +49,8 @@ struct AdamArgs {
 
 int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
                       float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
-                      int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st);
+                      int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st,
+                      float* gp8lo = nullptr, float* colsum = nullptr);
 int launch_head_val(const float* a8, const float* w9, const float* b9, const float* norm,
                     float* ring, int64_t P, int nblk, const DevState* dst, int window,
                     double* part_se, cudaStream_t st);

@@ -165,6 +165,19 @@ class Engine:
         n = r.epochs_run
         return out, r, hist[:n].copy(), losses[: 4 * n].reshape(n, 4).copy(), secs[:n].copy()
 
+    PROF_CLASSES = ("first_fwd", "conv_fwd", "head_loss", "wgrad", "dgrad", "first_wgrad", "adam",
+                    "val_first", "val_conv", "val_head", "stop")
+
+    def profile_epoch(self):
+        """One more training epoch with CUDA events around every launch:
+        (ms, flop, launches) arrays indexed [class, layer] (PROF_CLASSES x 9)."""
+        n = len(self.PROF_CLASSES) * 9
+        ms, fl = np.zeros(n), np.zeros(n)
+        ln = np.zeros(n, np.int32)
+        call("n2f_ctx_profile_epoch", self.handle, ms.ctypes.data, fl.ctypes.data, ln.ctypes.data)
+        shape = (len(self.PROF_CLASSES), 9)
+        return ms.reshape(shape), fl.reshape(shape), ln.reshape(shape)
+
     def fit_device(self, image_ptr: int, dtype: int, out_ptr: int, clean_ptr: int | None = None):
         """Whole fit on device-resident buffers (used by the bench's `value`)."""
         r = N2FResult()

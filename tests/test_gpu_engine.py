@@ -19,10 +19,13 @@ from n2f_testutil import arena_to_layers, net_to_arena, norm_rel, psnr
 pytestmark = pytest.mark.gpu
 
 
-def _engine(h, w, **cfg):
+def _engine(h, w, impl=0, **cfg):
     from paper_2108_10209_b200 import Engine, TrainConfig
 
-    return Engine(h, w, TrainConfig(**cfg), use_graph=False)
+    return Engine(h, w, TrainConfig(**cfg), use_graph=False, conv_impl=impl)
+
+
+IMPLS = [pytest.param(1, id="simt"), pytest.param(2, id="tcgen05")]
 
 
 def _arena(eng, which):
@@ -57,13 +60,14 @@ def test_seeded_init_matches_oracle(oracle, hw):
     assert np.array_equal(got, net_to_arena(oracle.init_net(7)))
 
 
+@pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("hw", [(32, 32), (64, 48), (128, 128)])
 @pytest.mark.parametrize("loss", ["bce", "mse"])
-def test_one_step_and_one_epoch(oracle, hw, loss):
+def test_one_step_and_one_epoch(oracle, hw, loss, impl):
     from paper_2108_10209_b200 import _lib
 
     img, _ = _image(*hw)
-    eng = _engine(*hw, seed=7, loss=loss)
+    eng = _engine(*hw, impl=impl, seed=7, loss=loss)
     _prepare(eng, img)
     net = oracle.init_net(7)
     norm, lo, hi, _ = oracle.normalize(img)
@@ -112,9 +116,10 @@ def _oracle_arenas(net):
     return [np.ascontiguousarray(np.concatenate(x), dtype=np.float32) for x in (ps, ms, vs)]
 
 
+@pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("hw", [(64, 48), (128, 128), (256, 256)])
 @pytest.mark.parametrize("loss", ["bce", "mse"])
-def test_fixed_weight_steps(oracle, hw, loss):
+def test_fixed_weight_steps(oracle, hw, loss, impl):
     """Each of the 4 steps of an epoch from IDENTICAL state (weights, Adam
     moments, t) on both sides: logits, gradients and the Adam update agree
     within 1e-3 (per-layer norm-relative), isolating per-step error from the
@@ -122,7 +127,7 @@ def test_fixed_weight_steps(oracle, hw, loss):
     from paper_2108_10209_b200 import _lib
 
     img, _ = _image(*hw)
-    eng = _engine(*hw, seed=7, loss=loss)
+    eng = _engine(*hw, impl=impl, seed=7, loss=loss)
     _prepare(eng, img)
     net = oracle.init_net(7)
     n32 = oracle.normalize(img)[0].astype(np.float32)
@@ -170,8 +175,9 @@ def test_fit_api_errors_and_degenerate():
     assert r.denoised.dtype == np.float64 and np.array_equal(r.denoised, const)
 
 
+@pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("use_graph", [True, False])
-def test_short_fit_matches_oracle_protocol(oracle, use_graph):
+def test_short_fit_matches_oracle_protocol(oracle, use_graph, impl):
     """max_epochs-bounded fit: epoch accounting, telemetry, histories ~ oracle."""
     from paper_2108_10209_b200 import TrainConfig, train_single_channel
     from paper_2108_10209_b200 import trainer as T
@@ -179,7 +185,7 @@ def test_short_fit_matches_oracle_protocol(oracle, use_graph):
     img, clean = _image(32, 40)
     cfg = TrainConfig(seed=3, patience_epochs=50, avg_window=3, max_epochs=5)
     ref = oracle.fit_denoise(img, seed=3, patience=50, window=3, max_epochs=5)
-    eng = T.Engine(32, 40, cfg, use_graph=use_graph)
+    eng = T.Engine(32, 40, cfg, use_graph=use_graph, conv_impl=impl)
     out, r, hist, losses, _ = eng.fit_host(np.ascontiguousarray(img))
     eng.close()
     assert r.epochs_run == ref.epochs_run == 5 and r.stop_reason == 1
@@ -189,7 +195,7 @@ def test_short_fit_matches_oracle_protocol(oracle, use_graph):
     np.testing.assert_allclose(hist, ref.val_history, rtol=2e-2)
     np.testing.assert_allclose(losses, ref.train_losses, rtol=2e-2)
     assert norm_rel(out, ref.denoised) < 1e-2
-    if use_graph:  # the public API on the same config: result types + telemetry schema
+    if use_graph and impl == 2:  # the public API (default impl): result types + telemetry schema
         sink = io.StringIO()
         res = train_single_channel(img, cfg, telemetry=sink, telemetry_tags={"slice": 0})
         assert res.epochs_run == 5 and res.stop_reason == "max_epochs"

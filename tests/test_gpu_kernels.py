@@ -85,9 +85,16 @@ CONV_SHAPES = [(1, 32, 3), (32, 32, 3), (32, 64, 3), (64, 64, 3), (64, 128, 3), 
                (128, 256, 3), (256, 256, 3), (256, 1, 1)]
 
 
+def _tc_ok(cin, cout, k):
+    return k == 3 and cin % 32 == 0 and cout in (32, 64, 128, 256)
+
+
+@pytest.mark.parametrize("impl", [1, 2])
 @pytest.mark.parametrize("cin,cout,k", CONV_SHAPES)
-@pytest.mark.parametrize("hw", [(13, 17), (40, 24)])
-def test_conv_forward(lib, oracle, cin, cout, k, hw):
+@pytest.mark.parametrize("hw", [(13, 17), (40, 24), (64, 96)])
+def test_conv_forward(lib, oracle, cin, cout, k, hw, impl):
+    if impl == 2 and not _tc_ok(cin, cout, k):
+        pytest.skip("tcgen05 path covers the 3x3 layers with cin >= 32")
     rng = np.random.default_rng(cin * 1000 + cout + hw[0])
     x = rng.standard_normal((cin, *hw)).astype(np.float32)
     w = (rng.standard_normal((cout, cin, k, k)) / np.sqrt(cin * k * k)).astype(np.float32)
@@ -98,14 +105,17 @@ def test_conv_forward(lib, oracle, cin, cout, k, hw):
         y = empty(hw[0] * hw[1] * cout)
         d_x, d_w, d_b = dev(chw_to_hwc(x)), dev(oihw_to_engine(w)), dev(b)  # keep alive
         _call(lib, "n2f_conv_fwd", d_x.data_ptr(), d_w.data_ptr(), d_b.data_ptr(), y.data_ptr(),
-              hw[0], hw[1], cin, cout, k, relu, 0, None)
+              hw[0], hw[1], cin, cout, k, relu, impl, None)
         got = hwc_to_chw(host(y).reshape(*hw, cout))
         np.testing.assert_allclose(got, ref, rtol=0, atol=1e-5 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("impl", [1, 2])
 @pytest.mark.parametrize("cin,cout,k", CONV_SHAPES)
-@pytest.mark.parametrize("hw", [(13, 17), (40, 24)])
-def test_conv_backward(lib, oracle, cin, cout, k, hw):
+@pytest.mark.parametrize("hw", [(13, 17), (40, 24), (64, 96)])
+def test_conv_backward(lib, oracle, cin, cout, k, hw, impl):
+    if impl == 2 and not _tc_ok(cout, cin, k):
+        pytest.skip("tcgen05 dgrad covers 3x3 layers with cin in {32..256}")
     rng = np.random.default_rng(cin * 77 + cout + hw[1])
     x = np.maximum(rng.standard_normal((cin, *hw)), 0).astype(np.float32)  # post-ReLU input
     w = (rng.standard_normal((cout, cin, k, k)) / np.sqrt(cin * k * k)).astype(np.float32)
@@ -121,7 +131,7 @@ def test_conv_backward(lib, oracle, cin, cout, k, hw):
     _call(lib, "n2f_conv_bwd", d_g.data_ptr(), d_x.data_ptr(),
           d_w.data_ptr(), d_x.data_ptr() if need_dx else None,
           d_dx.data_ptr() if need_dx else None, d_dw.data_ptr(), d_db.data_ptr(), hw[0], hw[1],
-          cin, cout, k, 0, None)
+          cin, cout, k, impl, None)
     dw = engine_to_oihw(host(d_dw), cout, cin, k)
     np.testing.assert_allclose(dw, dw_ref, rtol=0, atol=1e-5 * np.abs(dw_ref).max())
     np.testing.assert_allclose(host(d_db), db_ref, rtol=0, atol=1e-5 * np.abs(db_ref).max())
@@ -247,3 +257,29 @@ def test_window_mean_bitwise(lib, oracle, n, window, first):
     _call(lib, "n2f_window_mean", d_r.data_ptr(), window, first, n, plane, -1.5, 7.25,
           out.data_ptr(), None)
     assert np.array_equal(host(out), ref)
+
+
+@pytest.mark.parametrize("cin,cout", [(64, 64), (256, 256)])
+def test_conv_accuracy_vs_f64(lib, oracle, cin, cout):
+    """Error of each conv implementation against an f64 evaluation of the same
+    fp32 inputs (prints the numbers; bounds are the fp32-reassociation level)."""
+    rng = np.random.default_rng(cin)
+    h, w = 64, 96
+    x = np.maximum(rng.standard_normal((cin, h, w)), 0).astype(np.float32)
+    wt = (rng.standard_normal((cout, cin, 3, 3)) * np.sqrt(2.0 / (9 * cin))).astype(np.float32)
+    b = np.zeros(cout, np.float32)
+    exact = oracle.conv_forward(x.astype(np.float64), wt.astype(np.float64), b.astype(np.float64))
+    blas = oracle.conv_forward(x, wt, b)
+    scale = np.abs(exact).max()
+    errs = {"oracle_fp32": np.abs(blas - exact).max() / scale}
+    d_x, d_w, d_b = dev(chw_to_hwc(x)), dev(oihw_to_engine(wt)), dev(b)
+    for impl in (1, 2):
+        y = empty(h * w * cout)
+        _call(lib, "n2f_conv_fwd", d_x.data_ptr(), d_w.data_ptr(), d_b.data_ptr(), y.data_ptr(),
+              h, w, cin, cout, 3, 0, impl, None)
+        got = hwc_to_chw(host(y).reshape(h, w, cout))
+        errs[f"impl{impl}"] = np.abs(got - exact).max() / scale
+        # signed bias: mean of (got - exact) * sign(exact), relative to mean |exact|
+        errs[f"impl{impl}_bias"] = float(np.mean((got - exact) * np.sign(exact)) / np.mean(np.abs(exact)))
+    print(f"cin={cin} cout={cout} max-err/scale: {errs}")
+    assert errs["impl1"] < 1e-5 and errs["impl2"] < 3e-5
