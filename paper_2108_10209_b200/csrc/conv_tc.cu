@@ -41,14 +41,21 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // ---------------------------------------------------------------------------
 constexpr int kTW = 32, kTH = 4;
 constexpr int kThreadsTc = 320;
-constexpr int kGroup = 2;  // K chunks (of 32 channels) per TMEM accumulation group
+// K chunks (of 32 channels) per TMEM accumulation group.  With one chunk per
+// group and the 8 small cross-term MMAs issued before the 4 hi*hi MMAs, only
+// 4 truncating accumulates per group act on a large accumulator value.
+constexpr int kGroup = 1;
 
 template <int BN>
 struct FwdCfg {
   static constexpr int kStageA = 128 * 128;
   static constexpr int kStageB = BN * 128;
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
-  static constexpr int kStages = (190 * 1024) / kStageBytes > 4 ? 4 : (190 * 1024) / kStageBytes;
+  // wide layers: as many stages as fit one CTA per SM; narrow layers (short K
+  // loops, per-tile overhead dominates): 2 stages so two CTAs share an SM and
+  // one's prologue/epilogue overlaps the other's MMAs
+  static constexpr int kStages =
+      BN >= 128 ? ((200 * 1024) / kStageBytes > 4 ? 4 : (200 * 1024) / kStageBytes) : 2;
   static constexpr int kSmem = kStages * kStageBytes + 1024;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two group buffers
   static constexpr int kHalf = BN / 2;                         // columns per epilogue warp
@@ -138,16 +145,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           tc_fence_after();
           const uint32_t a = smem_u32(base + s * Cfg::kStageBytes);
           const uint32_t al = a + Cfg::kStageA, bh = a + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
+          // small cross terms first (accumulator still tiny), then hi*hi
+          const bool fresh = kb == g * kGroup;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint64_t dah = sw128_desc(a + 32 * k, 16, 1024);
-            const uint64_t dal = sw128_desc(al + 32 * k, 16, 1024);
-            const uint64_t dbh = sw128_desc(bh + 32 * k, 16, 1024);
-            const uint64_t dbl = sw128_desc(bl + 32 * k, 16, 1024);
-            mma_tf32(d, dah, dbh, idesc, (kb != g * kGroup) || k != 0);
-            mma_tf32(d, dah, dbl, idesc, 1);
-            mma_tf32(d, dal, dbh, idesc, 1);
+            mma_tf32(d, sw128_desc(a + 32 * k, 16, 1024), sw128_desc(bl + 32 * k, 16, 1024), idesc,
+                     !(fresh && k == 0));
+            mma_tf32(d, sw128_desc(al + 32 * k, 16, 1024), sw128_desc(bh + 32 * k, 16, 1024), idesc, 1);
           }
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_tf32(d, sw128_desc(a + 32 * k, 16, 1024), sw128_desc(bh + 32 * k, 16, 1024), idesc, 1);
           mma_commit(&empty[s]);
         }
         mma_commit(&tfull[b]);
@@ -333,16 +341,17 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           tc_fence_after();
           const uint32_t a = smem_u32(base + s * Cfg::kStageBytes);
           const uint32_t al = a + Cfg::kStageA, bh = a + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
+          const bool fresh = kb == g * kGroup;
+          auto mn = [](uint32_t base_addr, int k) {
+            return sw128_desc(base_addr + 1024 * k, 4096, 512, kLayoutSw128Base32);
+          };
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint64_t dah = sw128_desc(a + 1024 * k, 4096, 512, kLayoutSw128Base32);
-            const uint64_t dal = sw128_desc(al + 1024 * k, 4096, 512, kLayoutSw128Base32);
-            const uint64_t dbh = sw128_desc(bh + 1024 * k, 4096, 512, kLayoutSw128Base32);
-            const uint64_t dbl = sw128_desc(bl + 1024 * k, 4096, 512, kLayoutSw128Base32);
-            mma_tf32(d, dah, dbh, idesc, (kb != g * kGroup) || k != 0);
-            mma_tf32(d, dah, dbl, idesc, 1);
-            mma_tf32(d, dal, dbh, idesc, 1);
+            mma_tf32(d, mn(a, k), mn(bl, k), idesc, !(fresh && k == 0));
+            mma_tf32(d, mn(al, k), mn(bh, k), idesc, 1);
           }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) mma_tf32(d, mn(a, k), mn(bh, k), idesc, 1);
           mma_commit(&empty[s]);
         }
         mma_commit(&tfull[b]);

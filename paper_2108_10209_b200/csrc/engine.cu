@@ -110,6 +110,8 @@ struct n2f_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   int bias_tiles[2]{};
+  float* grad_red = nullptr;
+  ColReduceArgs grad_reduce[3]{};  // [0,1] tcgen05 shape classes, [2] SIMT path
   int wsplit[2][kLayers]{};
   int last_sc = 0;  // shape class of the last enqueued step (parity readback)
 };
@@ -217,6 +219,7 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
   }
   PROF(kPWgradFirst, 0, conv_flop(P, 0),
        wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
+  PROF(kPAdam, 0, 0.0, launch_col_reduce(c->grad_reduce[sc], st));
   PROF(kPAdam, 0, 0.0, launch_adam(c->adam_sc[sc], c->step_counter, 0, st));
   return N2F_OK;
 }
@@ -267,6 +270,7 @@ int enqueue_step(n2f_ctx* c, int k) {
     gn = t;
   }
   N2F_TRY(wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
+  N2F_TRY(launch_col_reduce(c->grad_reduce[2], st));
   N2F_TRY(launch_adam(c->adam, c->step_counter, 0, st));
   return N2F_OK;
 }
@@ -327,6 +331,29 @@ int build_graph(n2f_ctx* c) {
   if (s != N2F_OK) return s;
   N2F_CUDA(e);
   N2F_CUDA(cudaGraphInstantiate(&c->exec, c->graph, 0));
+  return N2F_OK;
+}
+
+// Move every Adam tensor with more than kMaxInlineSplits partials onto a
+// k_col_reduce pass (output slot = the tensor's arena offset in grad_red).
+constexpr int kMaxInlineSplits = 32;
+int route_reductions(n2f_ctx* c, AdamArgs& a, ColReduceArgs& r) {
+  r.n = 0;
+  r.prefix[0] = 0;
+  for (int q = 0; q < a.ntensors; ++q) {
+    AdamTensor& T = a.t[q];
+    if (T.nsplit <= kMaxInlineSplits) continue;
+    if (r.n == kMaxColReduce) return fail(N2F_ERR_ARG, "too many reductions");
+    ColReduce& t = r.t[r.n];
+    t.part = T.part;
+    t.out = c->grad_red + T.off;
+    t.rows = T.nsplit;
+    t.cols = (int)T.n;
+    r.prefix[r.n + 1] = r.prefix[r.n] + (int)((T.n + 31) / 32);
+    ++r.n;
+    T.part = c->grad_red + T.off;
+    T.nsplit = 1;
+  }
   return N2F_OK;
 }
 
@@ -491,12 +518,23 @@ int setup(n2f_ctx* c) {
       a.t[2 * li].want_lo = 1;
       a.t[2 * li].wtlo = c->wt_lo[li];
     }
+    // bias gradients of layers 1..7 are per-tile column sums (dgrad epilogue,
+    // head); weights use the tcgen05 wgrad's split count
     for (int sc = 0; sc < 2; ++sc) {
       c->adam_sc[sc] = a;
-      for (int li = 1; li <= 6; ++li) c->adam_sc[sc].t[2 * li + 1].nsplit = c->bias_tiles[sc];
-      c->adam_sc[sc].t[2 * 7 + 1].nsplit = c->nblk_head;
-      for (int li = 1; li <= 7; ++li) c->adam_sc[sc].t[2 * li].nsplit = c->wsplit[sc][li];
+      for (int li = 1; li <= 7; ++li) {
+        c->adam_sc[sc].t[2 * li + 1].nsplit = li == 7 ? c->nblk_head : c->bias_tiles[sc];
+        c->adam_sc[sc].t[2 * li].nsplit = c->wsplit[sc][li];
+      }
     }
+  }
+  // Tensors with many split-K partials (per-tile bias sums, the head, the
+  // first layer) are reduced by one parallel k_col_reduce launch into
+  // grad_red before Adam, which then reads a single partial.
+  N2F_TRY(dalloc(c, &c->grad_red, c->ptotal));
+  N2F_TRY(route_reductions(c, c->adam, c->grad_reduce[2]));
+  if (c->tc) {
+    for (int sc = 0; sc < 2; ++sc) N2F_TRY(route_reductions(c, c->adam_sc[sc], c->grad_reduce[sc]));
   }
 
   N2F_CUDA(cudaMallocHost(&c->h_mm, 4 * sizeof(double)));

@@ -239,6 +239,31 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
+// Column sums of per-tile partials [rows][cols] for several tensors in one
+// launch (the bias gradients): block = (tensor, 32-column chunk), 32 row
+// lanes x 32 columns, fixed-order tree over the row lanes (deterministic).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_col_reduce(ColReduceArgs a) {
+  __shared__ float sm[32][33];
+  const int b = blockIdx.x;
+  int k = 0;
+  while (k + 1 < a.n && b >= a.prefix[k + 1]) ++k;
+  const ColReduce& T = a.t[k];
+  const int col = (b - a.prefix[k]) * 32 + (threadIdx.x & 31);
+  const int r0 = threadIdx.x >> 5;
+  float s = 0.f;
+  if (col < T.cols)
+    for (int r = r0; r < T.rows; r += 32) s += T.part[(int64_t)r * T.cols + col];
+  sm[r0][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (r0 == 0 && col < T.cols) {
+    float t = sm[0][threadIdx.x];
+    for (int q = 1; q < 32; ++q) t += sm[q][threadIdx.x];
+    T.out[col] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // End-of-epoch bookkeeping (trainer.py:78-94): reduce the validation and loss
 // partials in fixed order, record history, strict-improvement patience rule,
 // and drive the graph's while-condition.
@@ -418,6 +443,13 @@ int launch_head_val(const float* a8, const float* w9, const float* b9, const flo
 int launch_adam(const AdamArgs& args, const int* step_counter, int fixed_t, cudaStream_t st) {
   k_adam<<<(unsigned)((args.total + kThreads - 1) / kThreads), kThreads, 0, st>>>(args, step_counter,
                                                                                    fixed_t);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_col_reduce(const ColReduceArgs& a, cudaStream_t st) {
+  if (a.n == 0) return N2F_OK;
+  k_col_reduce<<<a.prefix[a.n], 1024, 0, st>>>(a);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

@@ -47,6 +47,19 @@ struct AdamArgs {
   float beta1, one_minus_beta1, beta2, one_minus_beta2, lr, eps;
 };
 
+struct ColReduce {
+  const float* part;  // [rows][cols]
+  float* out;         // [cols]
+  int rows, cols;
+};
+constexpr int kMaxColReduce = 16;
+struct ColReduceArgs {
+  ColReduce t[kMaxColReduce];
+  int n;
+  int prefix[kMaxColReduce + 1];  // block offsets: tensor k owns blocks [prefix[k], prefix[k+1])
+};
+int launch_col_reduce(const ColReduceArgs& a, cudaStream_t st);
+
 int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
                       float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
                       int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st,

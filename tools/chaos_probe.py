@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--size", type=int, default=64)
     ap.add_argument("--runs", type=int, default=4)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--rel-noise", type=float, default=0.0,
+                    help="instead of 1-ulp nudges, multiply every weight by (1 + N(0, rel_noise))")
     args = ap.parse_args()
     clean = synthetic.blob_rect_image(args.size, args.size, 100 + args.seed)
     noisy = synthetic.gaussian_noisy(clean, 25 / 255, 200 + args.seed).astype(np.float64)
@@ -31,7 +33,10 @@ def main():
     out = []
     for r in range(args.runs):
         net = o.init_net(args.seed)
-        if r > 0:  # nudge 8 random weights of L8 by one ulp
+        if r > 0 and args.rel_noise > 0:
+            for w in net.weights:
+                w *= (1 + rng.normal(0, args.rel_noise, w.shape)).astype(np.float32)
+        elif r > 0:  # nudge 8 random weights of L8 by one ulp
             w = net.weights[7].reshape(-1)
             idx = rng.integers(0, w.size, 8)
             w[idx] = np.nextafter(w[idx], np.float32(np.inf))
