@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libn2f.so")
+LIB_PATH = os.environ.get("N2F_LIB") or os.path.join(_HERE, "libn2f.so")  # N2F_LIB: A/B variants
 
 N2F_OK, N2F_ERR_ARG, N2F_ERR_NONFINITE, N2F_ERR_CUDA, N2F_ERR_OOM, N2F_ERR_UNSUPPORTED = range(6)
 N2F_F32, N2F_F64 = 0, 1

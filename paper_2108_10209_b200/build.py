@@ -18,15 +18,16 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(ROOT, "build", "n2f")
-LIB = os.path.join(PKG, "libn2f.so")
+LIB = os.environ.get("N2F_LIB_OUT") or os.path.join(PKG, "libn2f.so")
+BUILD = os.path.join(ROOT, "build", "n2f" if "N2F_LIB_OUT" not in os.environ else
+                     "n2f_" + os.path.basename(LIB).replace(".so", ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
     "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-warn-spills",
-]
+] + os.environ.get("N2F_EXTRA_FLAGS", "").split()  # experiment variants (A/B builds)
 
 
 def _sources():

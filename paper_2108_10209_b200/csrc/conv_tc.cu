@@ -41,15 +41,24 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 // ---------------------------------------------------------------------------
 constexpr int kTW = 32, kTH = 4;
 constexpr int kThreadsTc = 320;
-// K chunks (of 32 channels) per TMEM accumulation group.  With one chunk per
-// group and the 8 small cross-term MMAs issued before the 4 hi*hi MMAs, only
-// 4 truncating accumulates per group act on a large accumulator value.
-constexpr int kGroup = 1;
+// Each pipeline stage carries K = kKC (channels for fwd/dgrad, pixels for
+// wgrad) and kGroup stages form one TMEM accumulation group; within a group
+// the small cross-term MMAs are issued first, then the hi*hi MMAs, so only 4
+// truncating accumulates per group act on a large accumulator value.
+// Measured on the box: 32-channel stages (128-byte rows, SWIZZLE_128B),
+// kGroup = 1 beat 16-channel stages with 4-6 stages in flight and kGroup = 2
+// (L8 fwd 229 vs 217 TF/s, L8 wgrad 214 vs 119 TF/s).
+constexpr int kKC = 32;
+#ifndef N2F_KGROUP
+#define N2F_KGROUP 1
+#endif
+constexpr int kGroup = N2F_KGROUP;
+constexpr int kRowBytes = kKC * 4;
 
 template <int BN>
 struct FwdCfg {
-  static constexpr int kStageA = 128 * 128;
-  static constexpr int kStageB = BN * 128;
+  static constexpr int kStageA = 128 * kRowBytes;
+  static constexpr int kStageB = BN * kRowBytes;
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
   // wide layers: as many stages as fit one CTA per SM; narrow layers (short K
   // loops, per-tile overhead dominates): 2 stages so two CTAs share an SM and
@@ -61,6 +70,15 @@ struct FwdCfg {
   static constexpr int kHalf = BN / 2;                         // columns per epilogue warp
 };
 
+// K-major operand, rows of kRowBytes: SWIZZLE_128B (32 ch) or SWIZZLE_64B (16 ch)
+__device__ __forceinline__ uint64_t kdesc(uint32_t addr) {
+  return kKC == 32 ? sw128_desc(addr, 16, 1024, 2) : sw128_desc(addr, 16, 512, 4);
+}
+// MN-major operand (SW128_BASE32B), blocks of kKC pixel rows x 128 B
+__device__ __forceinline__ uint64_t mndesc(uint32_t addr) {
+  return sw128_desc(addr, kKC * 128, 512, kLayoutSw128Base32);
+}
+
 __device__ __forceinline__ float4 lo4(float4 v) {
   float4 r;
   float h;
@@ -71,7 +89,12 @@ __device__ __forceinline__ float4 lo4(float4 v) {
   return r;
 }
 
-template <int BN>
+// CS = thread-block-cluster size along the tile dimension: the CS CTAs of a
+// cluster share every weight slice; each loads BN/CS rows of it and TMA
+// multicasts them to all, cutting L2->SM weight traffic CS-fold.  Slot reuse
+// then needs every CTA's consumer: empty[s] counts CS arrivals, delivered by
+// a multicast tcgen05.commit.
+template <int BN, int CS>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
@@ -81,6 +104,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   using Cfg = FwdCfg<BN>;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
+  constexpr uint16_t kMask = (uint16_t)((1u << CS) - 1u);
+  constexpr int kRows = BN / CS;  // weight rows each CTA loads and multicasts
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
@@ -89,13 +114,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tiles_x = (W + kTW - 1) / kTW;
   const int x0 = (blockIdx.x % tiles_x) * kTW, y0 = (blockIdx.x / tiles_x) * kTH;
-  const int cpt = C / 32, KB = 9 * cpt;
-  const int NG = (KB + kGroup - 1) / kGroup;
+  const int cpt = C / kKC, KB = 9 * cpt;  // C % 32 == 0, so KB is even
+  const int NG = KB / kGroup;
+  const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CS);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -110,6 +136,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(&tslot);
   tc_fence_before();
   __syncthreads();
+  if (CS > 1) cluster_sync();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t taddr = tslot;
 
@@ -119,44 +146,51 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       for (int kb = 0; kb < KB; ++kb) {
         const int s = kb % S, round = kb / S;
         if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-        const int tap = kb / cpt, c0 = (kb - tap * cpt) * 32;
+        const int tap = kb / cpt, c0 = (kb - tap * cpt) * kKC;
         const int ky = tap / 3, kx = tap - 3 * ky;
         uint8_t* st = base + s * Cfg::kStageBytes;
         mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
         tma_load_3d(st, &mx, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
         tma_load_3d(st + Cfg::kStageA, &mxl, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
-        tma_load_2d(st + 2 * Cfg::kStageA, &mw, &full[s], tap * C + c0, 0);
-        tma_load_2d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, &full[s], tap * C + c0, 0);
+        if (CS == 1) {
+          tma_load_2d(st + 2 * Cfg::kStageA, &mw, &full[s], tap * C + c0, 0);
+          tma_load_2d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, &full[s], tap * C + c0, 0);
+        } else {
+          const int r0 = crank * kRows;
+          tma_load_2d_mc(st + 2 * Cfg::kStageA + r0 * kRowBytes, &mw, &full[s], tap * C + c0, r0,
+                         kMask);
+          tma_load_2d_mc(st + 2 * Cfg::kStageA + Cfg::kStageB + r0 * kRowBytes, &mwl, &full[s],
+                         tap * C + c0, r0, kMask);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---- MMA issuer
+      // ---- MMA issuer: one group = kGroup stages (K = 32) into a fresh buffer
       constexpr uint32_t idesc = idesc_tf32(128, BN, false, false);
       for (int g = 0; g < NG; ++g) {
         const int b = g & 1;
         if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-        tc_fence_after();
         const uint32_t d = taddr + b * BN;
-        const int kb_end = (g + 1) * kGroup < KB ? (g + 1) * kGroup : KB;
-        for (int kb = g * kGroup; kb < kb_end; ++kb) {
-          const int s = kb % S, round = kb / S;
-          mbar_wait(&full[s], round & 1);
+        // per stage: the small cross terms first (accumulator still tiny), then hi*hi
+        for (int j = 0; j < kGroup; ++j) {
+          const int kb = g * kGroup + j, s = kb % S;
+          mbar_wait(&full[s], (kb / S) & 1);
           tc_fence_after();
-          const uint32_t a = smem_u32(base + s * Cfg::kStageBytes);
-          const uint32_t al = a + Cfg::kStageA, bh = a + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
-          // small cross terms first (accumulator still tiny), then hi*hi
-          const bool fresh = kb == g * kGroup;
+          const uint32_t ah = smem_u32(base + s * Cfg::kStageBytes), al = ah + Cfg::kStageA,
+                         bh = ah + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            mma_tf32(d, sw128_desc(a + 32 * k, 16, 1024), sw128_desc(bl + 32 * k, 16, 1024), idesc,
-                     !(fresh && k == 0));
-            mma_tf32(d, sw128_desc(al + 32 * k, 16, 1024), sw128_desc(bh + 32 * k, 16, 1024), idesc, 1);
+          for (int k = 0; k < kKC / 8; ++k) {
+            mma_tf32(d, kdesc(ah + 32 * k), kdesc(bl + 32 * k), idesc, (j | k) != 0);
+            mma_tf32(d, kdesc(al + 32 * k), kdesc(bh + 32 * k), idesc, 1);
           }
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            mma_tf32(d, sw128_desc(a + 32 * k, 16, 1024), sw128_desc(bh + 32 * k, 16, 1024), idesc, 1);
-          mma_commit(&empty[s]);
+          for (int k = 0; k < kKC / 8; ++k)
+            mma_tf32(d, kdesc(ah + 32 * k), kdesc(bh + 32 * k), idesc, 1);
+          if (CS == 1)
+            mma_commit(&empty[s]);
+          else
+            mma_commit_mc(&empty[s], kMask);  // release the slot in every CTA of the cluster
         }
         mma_commit(&tfull[b]);
       }
@@ -241,6 +275,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     for (int n = tid; n < BN; n += kThreadsTc)
       colsum[(int64_t)blockIdx.x * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
   }
+  if (CS > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
   if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(taddr);
 }
 
@@ -256,14 +291,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 // reduces the partials in fixed order.  Accumulation is grouped exactly like
 // the forward kernel (fresh TMEM buffer per group, fp32 register sums).
 // ---------------------------------------------------------------------------
-constexpr int kSegW = 32;
+constexpr int kSegW = kKC;  // pixels per stage (one image-row segment)
 
 template <int BN>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_wgrad3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                   const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mgl,
                   float* __restrict__ part, int H, int W, int C, int nsplit) {
-  using Cfg = FwdCfg<BN>;  // same stage geometry: A = 128 x 128 B, B = BN x 128 B
+  using Cfg = FwdCfg<BN>;  // same stage bytes: A = 4 x 16 px x 128 B, B = BN/32 x 16 px x 128 B
+  constexpr int kBlk = kSegW * 128;  // bytes of one 32-channel MN block
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
   extern __shared__ uint8_t smem_raw[];
@@ -281,7 +317,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int NG = (KB + kGroup - 1) / kGroup;
   int nblk_a = (K9 - m0 + 31) / 32;
   if (nblk_a > 4) nblk_a = 4;
-  const uint32_t stage_bytes = (uint32_t)nblk_a * 4096u * 2u + (uint32_t)Cfg::kStageB * 2u;
+  const uint32_t stage_bytes = (uint32_t)nblk_a * kBlk * 2u + (uint32_t)Cfg::kStageB * 2u;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -316,12 +352,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         for (int j = 0; j < nblk_a; ++j) {
           const int mm = m0 + 32 * j, tap = mm / C, c = mm - tap * C;
           const int ky = tap / 3, kx = tap - 3 * ky;
-          tma_load_3d(st + j * 4096, &mx, &full[s], c, x0 + kx - 1, y0 + ky - 1);
-          tma_load_3d(st + Cfg::kStageA + j * 4096, &mxl, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+          tma_load_3d(st + j * kBlk, &mx, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+          tma_load_3d(st + Cfg::kStageA + j * kBlk, &mxl, &full[s], c, x0 + kx - 1, y0 + ky - 1);
         }
         for (int jn = 0; jn < BN / 32; ++jn) {
-          tma_load_3d(st + 2 * Cfg::kStageA + jn * 4096, &mg, &full[s], 32 * jn, x0, y0);
-          tma_load_3d(st + 2 * Cfg::kStageA + Cfg::kStageB + jn * 4096, &mgl, &full[s], 32 * jn, x0,
+          tma_load_3d(st + 2 * Cfg::kStageA + jn * kBlk, &mg, &full[s], 32 * jn, x0, y0);
+          tma_load_3d(st + 2 * Cfg::kStageA + Cfg::kStageB + jn * kBlk, &mgl, &full[s], 32 * jn, x0,
                       y0);
         }
       }
@@ -332,26 +368,22 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       for (int g = 0; g < NG; ++g) {
         const int b = g & 1;
         if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-        tc_fence_after();
+        const int ng = (g + 1) * kGroup <= KB ? kGroup : KB - g * kGroup;
         const uint32_t d = taddr + b * BN;
-        const int kb_end = (g + 1) * kGroup < KB ? (g + 1) * kGroup : KB;
-        for (int kb = g * kGroup; kb < kb_end; ++kb) {
-          const int s = kb % S, round = kb / S;
-          mbar_wait(&full[s], round & 1);
+        for (int j = 0; j < ng; ++j) {  // per stage: cross terms first, then hi*hi
+          const int kb = g * kGroup + j, s = kb % S;
+          mbar_wait(&full[s], (kb / S) & 1);
           tc_fence_after();
-          const uint32_t a = smem_u32(base + s * Cfg::kStageBytes);
-          const uint32_t al = a + Cfg::kStageA, bh = a + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
-          const bool fresh = kb == g * kGroup;
-          auto mn = [](uint32_t base_addr, int k) {
-            return sw128_desc(base_addr + 1024 * k, 4096, 512, kLayoutSw128Base32);
-          };
+          const uint32_t ah = smem_u32(base + s * Cfg::kStageBytes), al = ah + Cfg::kStageA,
+                         bh = ah + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            mma_tf32(d, mn(a, k), mn(bl, k), idesc, !(fresh && k == 0));
-            mma_tf32(d, mn(al, k), mn(bh, k), idesc, 1);
+          for (int k = 0; k < kSegW / 8; ++k) {
+            mma_tf32(d, mndesc(ah + 1024 * k), mndesc(bl + 1024 * k), idesc, (j | k) != 0);
+            mma_tf32(d, mndesc(al + 1024 * k), mndesc(bh + 1024 * k), idesc, 1);
           }
 #pragma unroll
-          for (int k = 0; k < 4; ++k) mma_tf32(d, mn(a, k), mn(bh, k), idesc, 1);
+          for (int k = 0; k < kSegW / 8; ++k)
+            mma_tf32(d, mndesc(ah + 1024 * k), mndesc(bh + 1024 * k), idesc, 1);
           mma_commit(&empty[s]);
         }
         mma_commit(&tfull[b]);
@@ -435,14 +467,15 @@ int map_act(CUtensorMap* m, const float* p, int C, int W, int H, int bc, int bw,
 }
 
 // Row-major matrix [rows][cols] fp32 viewed as 2-D (cols, rows).
-int map_mat(CUtensorMap* m, const float* p, int cols, int rows, int bc, int br) {
+int map_mat(CUtensorMap* m, const float* p, int cols, int rows, int bc, int br,
+            CUtensorMapSwizzle sw) {
   N2F_TRY(encoder());
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
   const cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
   const cuuint32_t es[2] = {1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), dims, strides,
-                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(mat) failed: %d", (int)r);
   return N2F_OK;
@@ -450,18 +483,42 @@ int map_mat(CUtensorMap* m, const float* p, int cols, int rows, int bc, int br) 
 
 template <int BN>
 int set_attr_bn() {
-  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 FwdCfg<BN>::kSmem));
+  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                FwdCfg<BN>::kSmem));
+  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                FwdCfg<BN>::kSmem));
+  return N2F_OK;
+}
+
+template <int BN, int CS>
+int launch_conv_tc_cs(const ConvTcPlan& pl, const float* bias, const float* mask, float* y,
+                      float* ylo, float* colsum, int epi, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kThreadsTc);
+  cfg.dynamicSmemBytes = FwdCfg<BN>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_tc<BN, CS>, pl.mx, pl.mxl, pl.mw, pl.mwl, bias, mask,
+                              y, ylo, colsum, pl.H, pl.W, pl.C, epi));
+  N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
 
 template <int BN>
 int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const float* mask, float* y,
                       float* ylo, float* colsum, int epi, cudaStream_t st) {
-  k_conv3x3_tc<BN><<<pl.grid, kThreadsTc, FwdCfg<BN>::kSmem, st>>>(
-      pl.mx, pl.mxl, pl.mw, pl.mwl, bias, mask, y, ylo, colsum, pl.H, pl.W, pl.C, epi);
-  N2F_LAUNCH_CHECK();
-  return N2F_OK;
+  if (pl.cs == 4) return launch_conv_tc_cs<BN, 4>(pl, bias, mask, y, ylo, colsum, epi, st);
+  if (pl.cs == 2) return launch_conv_tc_cs<BN, 2>(pl, bias, mask, y, ylo, colsum, epi, st);
+  return launch_conv_tc_cs<BN, 1>(pl, bias, mask, y, ylo, colsum, epi, st);
 }
 
 template <int BN>
@@ -510,10 +567,22 @@ int conv_tc_plan(ConvTcPlan* pl, const float* x, const float* xlo, const float* 
   pl->C = C;
   pl->N = N;
   pl->grid = conv_tc_tiles(H, W);
-  N2F_TRY(map_act(&pl->mx, x, C, W, H, 32, kTW, kTH, CU_TENSOR_MAP_SWIZZLE_128B));
-  N2F_TRY(map_act(&pl->mxl, xlo, C, W, H, 32, kTW, kTH, CU_TENSOR_MAP_SWIZZLE_128B));
-  N2F_TRY(map_mat(&pl->mw, w, 9 * C, N, 32, N));
-  N2F_TRY(map_mat(&pl->mwl, wlo, 9 * C, N, 32, N));
+  // cluster size: weight multicast over 4 (or 2) neighbouring tiles when the
+  // grid divides and each CTA's weight slice stays >= 8 rows (one swizzle atom)
+  const char* env = getenv("N2F_TC_CLUSTER");
+  int want = env ? atoi(env) : 1;
+  if (want > 4) want = 4;  // kernels are instantiated for 1, 2, 4
+  pl->cs = 1;
+  for (int cs = want; cs > 1; cs /= 2)
+    if (pl->grid % cs == 0 && N / cs >= 8) {
+      pl->cs = cs;
+      break;
+    }
+  const CUtensorMapSwizzle sw = kKC == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  N2F_TRY(map_act(&pl->mx, x, C, W, H, kKC, kTW, kTH, sw));
+  N2F_TRY(map_act(&pl->mxl, xlo, C, W, H, kKC, kTW, kTH, sw));
+  N2F_TRY(map_mat(&pl->mw, w, 9 * C, N, kKC, N / pl->cs, sw));
+  N2F_TRY(map_mat(&pl->mwl, wlo, 9 * C, N, kKC, N / pl->cs, sw));
   return N2F_OK;
 }
 

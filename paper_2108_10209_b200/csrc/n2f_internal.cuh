@@ -71,6 +71,7 @@ int wgrad_nsplit(int64_t pixels, int cin, int cout);
 struct ConvTcPlan {
   CUtensorMap mx, mxl, mw, mwl;
   int H, W, C, N, grid;
+  int cs;  // thread-block cluster size (weight multicast)
 };
 bool tc_supported(int cin, int cout);
 int conv_tc_plan(ConvTcPlan* pl, const float* x, const float* xlo, const float* w, const float* wlo,
