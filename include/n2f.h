@@ -161,6 +161,9 @@ int n2f_ctx_set_arena(n2f_ctx* ctx, int which, const float* host, int adam_step)
  * kind::tf32 MMA chain with K-major (0) or MN-major (1) SWIZZLE_128B operands. */
 int n2f_tc_selftest(const float* a, const float* b, float* d, int n, int a_mn, int b_mn,
                     void* stream);
+/* kind::f16 self-test: fp16 A[128 x 64], B[n x 64] (K-major 0 / MN-major 1). */
+int n2f_tc_selftest_f16(const uint16_t* a, const uint16_t* b, float* d, int n, int a_mn, int b_mn,
+                        void* stream);
 int n2f_ctx_step(n2f_ctx* ctx, int pair, float* logits_host);
 int n2f_ctx_epoch(n2f_ctx* ctx, int* stopped);
 /* Profile one epoch: per (class, layer) device ms / algorithmic FLOPs / launches

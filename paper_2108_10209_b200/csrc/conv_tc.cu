@@ -89,12 +89,12 @@ __device__ __forceinline__ float4 lo4(float4 v) {
   return r;
 }
 
-// CS = thread-block-cluster size along the tile dimension: the CS CTAs of a
-// cluster share every weight slice; each loads BN/CS rows of it and TMA
-// multicasts them to all, cutting L2->SM weight traffic CS-fold.  Slot reuse
-// then needs every CTA's consumer: empty[s] counts CS arrivals, delivered by
-// a multicast tcgen05.commit.
-template <int BN, int CS>
+// Persistent: each CTA (one per SM) walks tiles blockIdx.x, +gridDim.x, ...
+// The producer streams stages across tile boundaries, the MMA issuer keeps the
+// two TMEM group buffers busy across tiles, and the accumulate warps' epilogue
+// of tile t overlaps the first groups of tile t+1; barrier init, TMEM alloc
+// and descriptor prefetch happen once per CTA.
+template <int BN>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
@@ -104,8 +104,6 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   using Cfg = FwdCfg<BN>;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
-  constexpr uint16_t kMask = (uint16_t)((1u << CS) - 1u);
-  constexpr int kRows = BN / CS;  // weight rows each CTA loads and multicasts
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
@@ -113,15 +111,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   uint8_t* base = align1024(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tiles_x = (W + kTW - 1) / kTW;
-  const int x0 = (blockIdx.x % tiles_x) * kTW, y0 = (blockIdx.x / tiles_x) * kTH;
+  const int ntiles = tiles_x * ((H + kTH - 1) / kTH);
   const int cpt = C / kKC, KB = 9 * cpt;  // C % 32 == 0, so KB is even
   const int NG = KB / kGroup;
-  const int crank = CS > 1 ? (int)cluster_ctarank() : 0;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CS);
+      mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -136,31 +133,26 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(&tslot);
   tc_fence_before();
   __syncthreads();
-  if (CS > 1) cluster_sync();  // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t taddr = tslot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---- TMA producer
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % S, round = kb / S;
-        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-        const int tap = kb / cpt, c0 = (kb - tap * cpt) * kKC;
-        const int ky = tap / 3, kx = tap - 3 * ky;
-        uint8_t* st = base + s * Cfg::kStageBytes;
-        mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
-        tma_load_3d(st, &mx, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
-        tma_load_3d(st + Cfg::kStageA, &mxl, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
-        if (CS == 1) {
+      // ---- TMA producer (stage index `it` runs across tiles)
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int x0 = (tile % tiles_x) * kTW, y0 = (tile / tiles_x) * kTH;
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int s = it % S, round = it / S;
+          if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+          const int tap = kb / cpt, c0 = (kb - tap * cpt) * kKC;
+          const int ky = tap / 3, kx = tap - 3 * ky;
+          uint8_t* st = base + s * Cfg::kStageBytes;
+          mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+          tma_load_3d(st, &mx, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
+          tma_load_3d(st + Cfg::kStageA, &mxl, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
           tma_load_2d(st + 2 * Cfg::kStageA, &mw, &full[s], tap * C + c0, 0);
           tma_load_2d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, &full[s], tap * C + c0, 0);
-        } else {
-          const int r0 = crank * kRows;
-          tma_load_2d_mc(st + 2 * Cfg::kStageA + r0 * kRowBytes, &mw, &full[s], tap * C + c0, r0,
-                         kMask);
-          tma_load_2d_mc(st + 2 * Cfg::kStageA + Cfg::kStageB + r0 * kRowBytes, &mwl, &full[s],
-                         tap * C + c0, r0, kMask);
         }
       }
     }
@@ -168,31 +160,31 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     if (lane == 0) {
       // ---- MMA issuer: one group = kGroup stages (K = 32) into a fresh buffer
       constexpr uint32_t idesc = idesc_tf32(128, BN, false, false);
-      for (int g = 0; g < NG; ++g) {
-        const int b = g & 1;
-        if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-        const uint32_t d = taddr + b * BN;
-        // per stage: the small cross terms first (accumulator still tiny), then hi*hi
-        for (int j = 0; j < kGroup; ++j) {
-          const int kb = g * kGroup + j, s = kb % S;
-          mbar_wait(&full[s], (kb / S) & 1);
-          tc_fence_after();
-          const uint32_t ah = smem_u32(base + s * Cfg::kStageBytes), al = ah + Cfg::kStageA,
-                         bh = ah + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
+      int it = 0, gg = 0;  // stage and group counters across tiles
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int g = 0; g < NG; ++g, ++gg) {
+          const int b = gg & 1;
+          if (gg >= 2) mbar_wait(&tempty[b], ((gg >> 1) - 1) & 1);
+          const uint32_t d = taddr + b * BN;
+          // per stage: the small cross terms first (accumulator still tiny), then hi*hi
+          for (int j = 0; j < kGroup; ++j, ++it) {
+            const int s = it % S;
+            mbar_wait(&full[s], (it / S) & 1);
+            tc_fence_after();
+            const uint32_t ah = smem_u32(base + s * Cfg::kStageBytes), al = ah + Cfg::kStageA,
+                           bh = ah + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
 #pragma unroll
-          for (int k = 0; k < kKC / 8; ++k) {
-            mma_tf32(d, kdesc(ah + 32 * k), kdesc(bl + 32 * k), idesc, (j | k) != 0);
-            mma_tf32(d, kdesc(al + 32 * k), kdesc(bh + 32 * k), idesc, 1);
-          }
+            for (int k = 0; k < kKC / 8; ++k) {
+              mma_tf32(d, kdesc(ah + 32 * k), kdesc(bl + 32 * k), idesc, (j | k) != 0);
+              mma_tf32(d, kdesc(al + 32 * k), kdesc(bh + 32 * k), idesc, 1);
+            }
 #pragma unroll
-          for (int k = 0; k < kKC / 8; ++k)
-            mma_tf32(d, kdesc(ah + 32 * k), kdesc(bh + 32 * k), idesc, 1);
-          if (CS == 1)
+            for (int k = 0; k < kKC / 8; ++k)
+              mma_tf32(d, kdesc(ah + 32 * k), kdesc(bh + 32 * k), idesc, 1);
             mma_commit(&empty[s]);
-          else
-            mma_commit_mc(&empty[s], kMask);  // release the slot in every CTA of the cluster
+          }
+          mma_commit(&tfull[b]);
         }
-        mma_commit(&tfull[b]);
       }
     }
   } else {
@@ -200,12 +192,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int q = warp & 3;          // TMEM lane quarter
     const int half = (warp - 2) >> 2;  // column half
     const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * HALF;
+    int gg = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int x0 = (tile % tiles_x) * kTW, y0 = (tile / tiles_x) * kTH;
     float acc[HALF];
 #pragma unroll
     for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
-    for (int g = 0; g < NG; ++g) {
-      const int b = g & 1;
-      mbar_wait(&tfull[b], (g >> 1) & 1);
+    for (int g = 0; g < NG; ++g, ++gg) {
+      const int b = gg & 1;
+      mbar_wait(&tfull[b], (gg >> 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < HALF; c += (HALF < 32 ? HALF : 32)) {
@@ -268,14 +263,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (ylo) *reinterpret_cast<float4*>(ylo + p * BN + n0 + j) = lo4(v);
       }
     }
+    if (colsum) {  // the 8 accumulate warps only (named barrier 1)
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      for (int n = tid - 64; n < BN; n += 256)
+        colsum[(int64_t)tile * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // csum reusable for the next tile
+    }
+    }  // tile loop
   }
   tc_fence_before();
   __syncthreads();
-  if (colsum) {
-    for (int n = tid; n < BN; n += kThreadsTc)
-      colsum[(int64_t)blockIdx.x * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
-  }
-  if (CS > 1) cluster_sync();  // no CTA leaves while peers may still multicast into it
   if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(taddr);
 }
 
@@ -483,42 +480,29 @@ int map_mat(CUtensorMap* m, const float* p, int cols, int rows, int bc, int br,
 
 template <int BN>
 int set_attr_bn() {
-  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 FwdCfg<BN>::kSmem));
-  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FwdCfg<BN>::kSmem));
-  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FwdCfg<BN>::kSmem));
-  return N2F_OK;
-}
-
-template <int BN, int CS>
-int launch_conv_tc_cs(const ConvTcPlan& pl, const float* bias, const float* mask, float* y,
-                      float* ylo, float* colsum, int epi, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.grid);
-  cfg.blockDim = dim3(kThreadsTc);
-  cfg.dynamicSmemBytes = FwdCfg<BN>::kSmem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_tc<BN, CS>, pl.mx, pl.mxl, pl.mw, pl.mwl, bias, mask,
-                              y, ylo, colsum, pl.H, pl.W, pl.C, epi));
-  N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
 
 template <int BN>
 int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const float* mask, float* y,
                       float* ylo, float* colsum, int epi, cudaStream_t st) {
-  if (pl.cs == 4) return launch_conv_tc_cs<BN, 4>(pl, bias, mask, y, ylo, colsum, epi, st);
-  if (pl.cs == 2) return launch_conv_tc_cs<BN, 2>(pl, bias, mask, y, ylo, colsum, epi, st);
-  return launch_conv_tc_cs<BN, 1>(pl, bias, mask, y, ylo, colsum, epi, st);
+  k_conv3x3_tc<BN><<<pl.grid, kThreadsTc, FwdCfg<BN>::kSmem, st>>>(
+      pl.mx, pl.mxl, pl.mw, pl.mwl, bias, mask, y, ylo, colsum, pl.H, pl.W, pl.C, epi);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+      n = 148;
+  }
+  return n;
 }
 
 template <int BN>
@@ -566,23 +550,17 @@ int conv_tc_plan(ConvTcPlan* pl, const float* x, const float* xlo, const float* 
   pl->W = W;
   pl->C = C;
   pl->N = N;
-  pl->grid = conv_tc_tiles(H, W);
-  // cluster size: weight multicast over 4 (or 2) neighbouring tiles when the
-  // grid divides and each CTA's weight slice stays >= 8 rows (one swizzle atom)
-  const char* env = getenv("N2F_TC_CLUSTER");
-  int want = env ? atoi(env) : 1;
-  if (want > 4) want = 4;  // kernels are instantiated for 1, 2, 4
+  // persistent grid: one CTA per SM (two for the narrow layers, whose smem
+  // and register footprints allow it), each walking tiles with a fixed stride
+  const int tiles = conv_tc_tiles(H, W);
+  const int per_sm = N <= 64 ? 2 : 1;
+  pl->grid = tiles < per_sm * sm_count() ? tiles : per_sm * sm_count();
   pl->cs = 1;
-  for (int cs = want; cs > 1; cs /= 2)
-    if (pl->grid % cs == 0 && N / cs >= 8) {
-      pl->cs = cs;
-      break;
-    }
   const CUtensorMapSwizzle sw = kKC == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   N2F_TRY(map_act(&pl->mx, x, C, W, H, kKC, kTW, kTH, sw));
   N2F_TRY(map_act(&pl->mxl, xlo, C, W, H, kKC, kTW, kTH, sw));
-  N2F_TRY(map_mat(&pl->mw, w, 9 * C, N, kKC, N / pl->cs, sw));
-  N2F_TRY(map_mat(&pl->mwl, wlo, 9 * C, N, kKC, N / pl->cs, sw));
+  N2F_TRY(map_mat(&pl->mw, w, 9 * C, N, kKC, N, sw));
+  N2F_TRY(map_mat(&pl->mwl, wlo, 9 * C, N, kKC, N, sw));
   return N2F_OK;
 }
 

@@ -73,10 +73,89 @@ __global__ void __launch_bounds__(128) k_tc_selftest(const float* __restrict__ A
   if (warp == 0) tmem_dealloc<256>(taddr);
 }
 
+// kind::f16 variant: A[128 x 64] fp16, B[N x 64] fp16, four K=16 MMAs.
+// mode 0: K-major SWIZZLE_128B (row = 64 halves = 128 B, K step = 32 B);
+// mode 1: MN-major SWIZZLE_128B (blocks of 64 MN elements x 64 K rows).
+__device__ __forceinline__ uint32_t f16_offset(int mode, int row, int k) {
+  if (mode == 0) return sw128_offset(row, 2 * k);
+  return (row / 64) * 8192 + sw128_offset(k, 2 * (row % 64));
+}
+__device__ __forceinline__ uint64_t f16_desc(int mode, uint32_t base, int s) {
+  if (mode == 0) return sw128_desc(base + s * 32, 16, 1024);
+  return sw128_desc(base + s * 2048, 8192, 1024);
+}
+
+template <int AM, int BM>
+__global__ void __launch_bounds__(128) k_tc_selftest_f16(const uint16_t* __restrict__ A,
+                                                         const uint16_t* __restrict__ B,
+                                                         float* __restrict__ D, int N) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* base = align1024(smem_raw);
+  uint8_t* sA = base;
+  uint8_t* sB = base + 16384;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < 128 * 64; i += 128)
+    *reinterpret_cast<uint16_t*>(sA + f16_offset(AM, i / 64, i % 64)) = A[i];
+  for (int i = tid; i < N * 64; i += 128)
+    *reinterpret_cast<uint16_t*>(sB + f16_offset(BM, i / 64, i % 64)) = B[i];
+  fence_proxy_async();
+  if (warp == 0) tmem_alloc<256>(&tslot);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t taddr = tslot;
+  if (tid == 0) {
+    const uint32_t idesc = idesc_f16(128, N, AM != 0, BM != 0);
+    for (int s = 0; s < 4; ++s)
+      mma_f16(taddr, f16_desc(AM, smem_u32(sA), s), f16_desc(BM, smem_u32(sB), s), idesc, s > 0);
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld32(taddr + ((uint32_t)(warp * 32) << 16) + c0, r);
+    tmem_ld_wait();
+    for (int j = 0; j < 32; ++j) D[(warp * 32 + lane) * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(taddr);
+}
+
 }  // namespace
 }  // namespace n2f
 
 using namespace n2f;
+
+extern "C" int n2f_tc_selftest_f16(const uint16_t* A, const uint16_t* B, float* D, int N, int a_mn,
+                                   int b_mn, void* stream) {
+  if (N < 64 || N > 256 || N % 64) return fail(N2F_ERR_ARG, "selftest_f16 N=%d", N);
+  const int smem = 1024 + 16384 + N * 128;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto launch = [&](auto kern) -> int {
+    N2F_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<1, 128, smem, st>>>(A, B, D, N);
+    N2F_LAUNCH_CHECK();
+    return N2F_OK;
+  };
+  int s;
+  switch ((a_mn ? 2 : 0) + (b_mn ? 1 : 0)) {
+    case 0: s = launch(k_tc_selftest_f16<0, 0>); break;
+    case 1: s = launch(k_tc_selftest_f16<0, 1>); break;
+    case 2: s = launch(k_tc_selftest_f16<1, 0>); break;
+    default: s = launch(k_tc_selftest_f16<1, 1>); break;
+  }
+  if (s != N2F_OK) return s;
+  N2F_CUDA(cudaStreamSynchronize(st));
+  return N2F_OK;
+}
 
 extern "C" int n2f_tc_selftest(const float* A, const float* B, float* D, int N, int a_mn, int b_mn,
                                void* stream) {

@@ -40,6 +40,24 @@ def test_selftest_gemm(a_mn, b_mn, n):
     assert min(et, er) < 1e-4 * np.abs(ref_t).max()
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("n", [64, 256])
+def test_selftest_gemm_f16(a_mn, b_mn, n):
+    """kind::f16 with fp16 operands: K-major and MN-major SWIZZLE_128B."""
+    from paper_2108_10209_b200 import _lib
+
+    rng = np.random.default_rng(7 + n + 3 * a_mn + b_mn)
+    a = rng.standard_normal((128, 64)).astype(np.float16)
+    b = rng.standard_normal((n, 64)).astype(np.float16)
+    da, db, dd = dev(a.view(np.int16)), dev(b.view(np.int16)), empty(128 * n)
+    _lib.call("n2f_tc_selftest_f16", da.data_ptr(), db.data_ptr(), dd.data_ptr(), n, a_mn, b_mn, None)
+    d = host(dd).reshape(128, n)
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    err = np.abs(d - ref).max() / np.abs(ref).max()
+    print(f"f16 a_mn={a_mn} b_mn={b_mn} n={n}: rel err {err:.2e}")
+    assert err < 1e-6
+
+
 def test_split_operands_recover_fp32():
     """hi = tf32-truncated x, lo = x - hi: hi.hi + hi.lo + lo.hi ~ fp32 GEMM."""
     from paper_2108_10209_b200 import _lib
