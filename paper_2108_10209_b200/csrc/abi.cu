@@ -73,6 +73,24 @@ __global__ void k_conv1x1_dw(const float* __restrict__ g, const float* __restric
 
 unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
 
+// Tensor-core operand pair of an fp32 device tensor (scratch-owned).
+int make_operand(Scratch& s, const float* x, int64_t n, bool f16, int exp, TcOperand* op,
+                 cudaStream_t st) {
+  if (!f16) {
+    float* lo;
+    N2F_TRY(s.get(&lo, (size_t)n));
+    N2F_TRY(split_lo(x, lo, n, st));
+    *op = {x, lo, 0};
+    return N2F_OK;
+  }
+  uint16_t *hi, *lo;
+  N2F_TRY(s.get(&hi, (size_t)n));
+  N2F_TRY(s.get(&lo, (size_t)n));
+  N2F_TRY(split_f16(x, hi, lo, exp, n, st));
+  *op = {hi, lo, exp};
+  return N2F_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -133,19 +151,18 @@ int n2f_conv_fwd(const float* x, const float* w, const float* b, float* y, int h
     N2F_LAUNCH_CHECK();
   } else if (k == 3 && cin == 1 && cout % 4 == 0) {
     N2F_TRY(conv_first_simt(x, w, b, y, h, wd, cout, S(stream), relu));
-  } else if (k == 3 && impl == kImplTc && tc_supported(cin, cout)) {
+  } else if (k == 3 && (impl == kImplTc || impl == kImplTcF16) && tc_supported(cin, cout)) {
     static Scratch s;  // kept alive across async calls on an explicit stream
     for (void* q : s.ptrs) cudaFree(q);
     s.ptrs.clear();
-    float *xlo, *wlo;
-    N2F_TRY(s.get(&xlo, (size_t)P * cin));
-    N2F_TRY(s.get(&wlo, (size_t)cout * 9 * cin));
-    N2F_TRY(split_lo(x, xlo, P * cin, S(stream)));
-    N2F_TRY(split_lo(w, wlo, (int64_t)cout * 9 * cin, S(stream)));
+    const bool f16 = impl == kImplTcF16;
+    TcOperand ox, ow;
+    N2F_TRY(make_operand(s, x, P * cin, f16, kExpAct, &ox, S(stream)));
+    N2F_TRY(make_operand(s, w, (int64_t)cout * 9 * cin, f16, kExpW, &ow, S(stream)));
     ConvTcPlan pl;
-    N2F_TRY(conv_tc_plan(&pl, x, xlo, w, wlo, h, wd, cin, cout));
-    N2F_TRY(conv_tc_launch(pl, b, nullptr, y, nullptr, nullptr, relu ? kEpiBiasRelu : kEpiBias,
-                           S(stream)));
+    N2F_TRY(conv_tc_plan(&pl, ox, ow, h, wd, cin, cout, f16));
+    N2F_TRY(conv_tc_launch(pl, b, nullptr, y, nullptr, nullptr, 1.f, nullptr,
+                           relu ? kEpiBiasRelu : kEpiBias, S(stream)));
   } else if (k == 3 && cin % 8 == 0 && cout % 32 == 0) {
     N2F_TRY(conv3x3_simt(x, w, b, nullptr, y, h, wd, cin, cout, relu ? kEpiBiasRelu : kEpiBias,
                          S(stream)));
@@ -187,16 +204,16 @@ int n2f_conv_bwd(const float* g, const float* x, const float* w, const float* ma
       N2F_TRY(wgrad3x3_simt(g, x, pw, pb, h, wd, cin, cout, ns, S(stream)));
     if (dw) N2F_TRY(reduce_partials(pw, dw, ns, (int64_t)cout * 9 * cin, S(stream)));
     if (db) N2F_TRY(reduce_partials(pb, db, ns, cout, S(stream)));
-    if (dw && impl == kImplTc && tc_supported(cin, cout)) {  // dW on the tensor cores
+    const bool tcimpl = impl == kImplTc || impl == kImplTcF16, f16 = impl == kImplTcF16;
+    if (dw && tcimpl && tc_supported(cin, cout)) {  // dW on the tensor cores
       const int nst = wgrad_tc_nsplit(cin, h, wd);
-      float *xlo, *glo, *ptc;
-      N2F_TRY(s.get(&xlo, (size_t)P * cin));
-      N2F_TRY(s.get(&glo, (size_t)P * cout));
+      float* ptc;
       N2F_TRY(s.get(&ptc, (size_t)nst * cout * 9 * cin));
-      N2F_TRY(split_lo(x, xlo, P * cin, S(stream)));
-      N2F_TRY(split_lo(g, glo, P * cout, S(stream)));
+      TcOperand ox, og;
+      N2F_TRY(make_operand(s, x, P * cin, f16, kExpAct, &ox, S(stream)));
+      N2F_TRY(make_operand(s, g, P * cout, f16, kExpAct, &og, S(stream)));
       WgradTcPlan pl;
-      N2F_TRY(wgrad_tc_plan(&pl, x, xlo, g, glo, h, wd, cin, cout, nst));
+      N2F_TRY(wgrad_tc_plan(&pl, ox, og, h, wd, cin, cout, nst, f16));
       N2F_TRY(wgrad_tc_launch(pl, ptc, S(stream)));
       N2F_TRY(reduce_partials(ptc, dw, nst, (int64_t)cout * 9 * cin, S(stream)));
     }
@@ -206,16 +223,20 @@ int n2f_conv_bwd(const float* g, const float* x, const float* w, const float* ma
     float* wt;
     N2F_TRY(s.get(&wt, (size_t)cout * 9 * cin));
     N2F_TRY(transpose_dgrad_weights(w, wt, cin, cout, S(stream)));
-    if (impl == kImplTc && tc_supported(cout, cin)) {
-      float *glo, *wtlo;
-      N2F_TRY(s.get(&glo, (size_t)P * cout));
-      N2F_TRY(s.get(&wtlo, (size_t)cout * 9 * cin));
-      N2F_TRY(split_lo(g, glo, P * cout, S(stream)));
-      N2F_TRY(split_lo(wt, wtlo, (int64_t)cout * 9 * cin, S(stream)));
+    if ((impl == kImplTc || impl == kImplTcF16) && tc_supported(cout, cin)) {
+      const bool f16 = impl == kImplTcF16;
+      TcOperand og, owt, omask;
+      N2F_TRY(make_operand(s, g, P * cout, f16, kExpAct, &og, S(stream)));
+      N2F_TRY(make_operand(s, wt, (int64_t)cout * 9 * cin, f16, kExpW, &owt, S(stream)));
+      const void* mk = mask;
+      if (mask && f16) {  // the FP16 epilogue tests the sign of the fp16 hi tensor
+        N2F_TRY(make_operand(s, mask, P * cin, true, kExpAct, &omask, S(stream)));
+        mk = omask.hi;
+      }
       ConvTcPlan pl;
-      N2F_TRY(conv_tc_plan(&pl, g, glo, wt, wtlo, h, wd, cout, cin));
-      N2F_TRY(conv_tc_launch(pl, nullptr, mask, dx, nullptr, nullptr, mask ? kEpiMask : kEpiNone,
-                             S(stream)));
+      N2F_TRY(conv_tc_plan(&pl, og, owt, h, wd, cout, cin, f16));
+      N2F_TRY(conv_tc_launch(pl, nullptr, mk, dx, nullptr, nullptr, 1.f, nullptr,
+                             mask ? kEpiMask : kEpiNone, S(stream)));
     } else {
       N2F_TRY(conv3x3_simt(g, wt, nullptr, mask, dx, h, wd, cout, cin, mask ? kEpiMask : kEpiNone,
                            S(stream)));

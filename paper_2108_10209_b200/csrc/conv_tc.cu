@@ -1,18 +1,29 @@
-// tcgen05 (5th-gen tensor core) kernels for the 3x3 convolutions, 3xTF32
-// split precision: x = hi + lo (hi = tf32 top bits, lo = exact residual);
-// A.B ~= Ah.Bh + Ah.Bl + Al.Bh.  The tensor core truncates fp32 operands to
-// tf32 by itself, so the raw fp32 tensor IS the "hi" operand and only the lo
-// residual is stored beside it.
+// tcgen05 (5th-gen tensor core) kernels for the 3x3 convolutions in split
+// precision.  Every operand x is held as a pair hi + lo and a product as
+// A.B ~= Ah.Bh + Ah.Bl + Al.Bh (3 MMAs), in one of two precisions:
+//
+//   TF32 (F16 = false, kind::tf32): the tensor core truncates fp32 operands
+//     to tf32, so the raw fp32 tensor IS hi and only lo = round_tf32(x - hi)
+//     is stored beside it (fp32).  ~22 significant bits per operand.
+//   FP16 (F16 = true,  kind::f16): hi = fp16(x * 2^e), lo = fp16(x * 2^e - hi)
+//     with a per-tensor power-of-two scale e (activations/weights 2^8,
+//     gradients 2^(ceil(log2 P) + 8)) keeping both parts in fp16's normal
+//     range; ~22 significant bits, 2x the MMA rate and half the bytes of TF32.
+//     The epilogue removes 2^-(eA + eB) exactly.
 //
 // Accumulation: the tensor core's fp32 accumulation truncates (measured bias
-// -4.9e-6 relative at K = 2304 when one TMEM accumulator takes the whole
-// K loop, tests/test_gpu_kernels.py::test_conv_accuracy_vs_f64), and that
-// systematic shrink compounds through the 7-layer dgrad chain.  So the K loop
-// is cut into groups of kGroup chunks; each group accumulates into a fresh
-// TMEM buffer (ping-pong, 2 x BN columns) and the epilogue warps add the
-// group results into fp32 registers with round-to-nearest while the tensor
-// core runs the next group.
+// -4.9e-6 relative at K = 2304 when one TMEM accumulator takes the whole K
+// loop, tests/test_gpu_kernels.py::test_conv_accuracy_vs_f64), and that
+// systematic shrink compounds through the 7-layer dgrad chain.  The K loop is
+// cut into groups (K = 32 for TF32, 64 for FP16); each group accumulates into
+// a fresh TMEM buffer (ping-pong, 2 x BN columns), the small cross-term MMAs
+// of a group are issued before its hi*hi MMAs (so only 4 truncating adds act
+// on a large accumulator value), and the accumulate warps add the group
+// results into fp32 registers with round-to-nearest while the tensor core
+// runs the next group.
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "n2f_internal.cuh"
 #include "tc_common.cuh"
@@ -26,94 +37,181 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
+// Precision traits.  A pipeline stage carries K = 32 elements per operand row
+// (128 B tf32 / 64 B fp16).  One MMA consumes 32 bytes of K (8 tf32 / 16 fp16),
+// so a K-major operand advances 32 B per MMA and an MN-major one 1 KB (8 rows
+// of 128 B / 16 rows of 64 B).
+template <bool F16>
+struct Prec {
+  static constexpr int kES = F16 ? 2 : 4;           // bytes per element
+  static constexpr int kRow = 32 * kES;             // bytes per 32-element row
+  static constexpr int kKSteps = F16 ? 2 : 4;       // MMAs per 32-element stage row
+  static constexpr uint32_t kLayK = F16 ? 4 : 2;    // SWIZZLE_64B / SWIZZLE_128B (K-major)
+  static constexpr uint32_t kSboK = 8 * kRow;       // 8-row swizzle atom stride
+  static constexpr uint32_t kLayMN = F16 ? 4 : 1;   // SWIZZLE_64B / SWIZZLE_128B_BASE32B (MN-major)
+  static constexpr int kGroup = F16 ? 2 : 1;        // stages per TMEM accumulation group
+  __device__ static uint64_t kdesc(uint32_t addr) { return sw128_desc(addr, 16, kSboK, kLayK); }
+  // MN-major blocks of 32 channels x 32 pixel rows: LBO = block stride
+  __device__ static uint64_t mndesc(uint32_t addr) {
+    return sw128_desc(addr, 32 * kRow, 512, kLayMN);
+  }
+  __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if (F16)
+      mma_f16(d, a, b, idesc, acc);
+    else
+      mma_tf32(d, a, b, idesc, acc);
+  }
+  static constexpr uint32_t idesc(int M, int N, bool amn, bool bmn) {
+    return F16 ? idesc_f16(M, N, amn, bmn) : idesc_tf32(M, N, amn, bmn);
+  }
+};
+
+// Packed fp32 add (FADD2, round-to-nearest like FADD): a += (r0, r1).
+__device__ __forceinline__ void add2(float& a0, float& a1, uint32_t r0, uint32_t r1) {
+  asm("{\n\t.reg .b64 x, y;\n\tmov.b64 x, {%0, %1};\n\tmov.b64 y, {%2, %3};\n\t"
+      "add.rn.f32x2 x, x, y;\n\tmov.b64 {%0, %1}, x;\n\t}"
+      : "+f"(a0), "+f"(a1)
+      : "r"(r0), "r"(r1));
+}
+
+// Add one TMEM group buffer (this warp's 32 lanes x HALF columns at taddr)
+// into the fp32 register accumulators, two tcgen05.ld in flight per wait.
+template <int HALF>
+__device__ __forceinline__ void drain_add(uint32_t taddr, float (&acc)[HALF]) {
+  constexpr int CH = HALF < 32 ? HALF : 32;  // columns per load
+  constexpr int NB = HALF / CH;
+  constexpr int PB = NB >= 2 ? 2 : 1;        // loads per wait
+#pragma unroll
+  for (int c = 0; c < NB; c += PB) {
+    uint32_t r[PB][32];
+#pragma unroll
+    for (int p = 0; p < PB; ++p) {
+      if (CH == 16)
+        tmem_ld16(taddr + (c + p) * CH, r[p]);
+      else
+        tmem_ld32(taddr + (c + p) * CH, r[p]);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int p = 0; p < PB; ++p)
+#pragma unroll
+      for (int j = 0; j < CH; j += 2)
+        add2(acc[(c + p) * CH + j], acc[(c + p) * CH + j + 1], r[p][j], r[p][j + 1]);
+  }
+}
+
 // ---------------------------------------------------------------------------
-// 3x3 conv forward / dgrad as a TMA-fed tcgen05 implicit GEMM.
+// 3x3 conv forward / dgrad as a persistent, TMA-fed tcgen05 implicit GEMM.
 //   M = 128 pixels (a 32 x 4 spatial tile), N = all output channels (BN),
-//   K = 9 taps x C in chunks of 32 channels (128 B rows, SWIZZLE_128B).
-// Per K chunk, TMA loads the shifted input tile for the tap (out-of-bounds
-// coordinates zero-fill = the reference's zero padding, tensor.py:231-238)
-// and its lo residual, plus the weight slice and its lo residual.
-// Warp roles (320 threads): w0.lane0 TMA producer; w1.lane0 MMA issuer (w1
-// owns TMEM); w2..w9 accumulate/epilogue: warp w reads TMEM lane quarter
-// (w % 4) and column half (w - 2) / 4.  Epilogue: fused bias+ReLU (forward)
-// or ReLU-mask of the layer input (dgrad), optional per-tile column sums
-// (the bias gradient of that tensor), output + lo residual stores.
+//   K = 9 taps x C in stages of 32 channels.
+// Per stage, TMA loads the tap-shifted input tile (out-of-bounds coordinates
+// zero-fill = the reference's zero padding, tensor.py:231-238) and its lo
+// part, plus the weight slice and its lo part.  Warp roles (320 threads):
+// w0.lane0 TMA producer; w1.lane0 MMA issuer (w1 owns TMEM); w2..w9
+// accumulate + epilogue: warp w reads TMEM lane quarter (w % 4) and column
+// half (w - 2) / 4.  Epilogue: scale removal, fused bias+ReLU (forward) or
+// ReLU-mask of the layer input (dgrad), optional per-tile column sums (the
+// bias gradient of the produced tensor), fp32 output and/or the operand pair
+// for the next tensor-core consumer.
+// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the producer
+// streams stages across tile boundaries and the epilogue of tile t overlaps
+// the first groups of tile t+1.
 // ---------------------------------------------------------------------------
 constexpr int kTW = 32, kTH = 4;
 constexpr int kThreadsTc = 320;
-// Each pipeline stage carries K = kKC (channels for fwd/dgrad, pixels for
-// wgrad) and kGroup stages form one TMEM accumulation group; within a group
-// the small cross-term MMAs are issued first, then the hi*hi MMAs, so only 4
-// truncating accumulates per group act on a large accumulator value.
-// Measured on the box: 32-channel stages (128-byte rows, SWIZZLE_128B),
-// kGroup = 1 beat 16-channel stages with 4-6 stages in flight and kGroup = 2
-// (L8 fwd 229 vs 217 TF/s, L8 wgrad 214 vs 119 TF/s).
-constexpr int kKC = 32;
-#ifndef N2F_KGROUP
-#define N2F_KGROUP 1
-#endif
-constexpr int kGroup = N2F_KGROUP;
-constexpr int kRowBytes = kKC * 4;
 
-template <int BN>
+template <int BN, bool F16>
 struct FwdCfg {
-  static constexpr int kStageA = 128 * kRowBytes;
-  static constexpr int kStageB = BN * kRowBytes;
+  using P = Prec<F16>;
+  static constexpr int kStageA = 128 * P::kRow;
+  static constexpr int kStageB = BN * P::kRow;
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
-  // wide layers: as many stages as fit one CTA per SM; narrow layers (short K
-  // loops, per-tile overhead dominates): 2 stages so two CTAs share an SM and
-  // one's prologue/epilogue overlaps the other's MMAs
+  static constexpr int kMaxStages = (200 * 1024) / kStageBytes;
+  // wide layers: as many stages as fit one CTA per SM; narrow layers: 2 CTAs
+  // per SM (their smem and registers allow it) with 2 groups' worth of stages
   static constexpr int kStages =
-      BN >= 128 ? ((200 * 1024) / kStageBytes > 4 ? 4 : (200 * 1024) / kStageBytes) : 2;
-  static constexpr int kSmem = kStages * kStageBytes + 1024;
+      BN >= 128 ? (kMaxStages > 6 ? 6 : kMaxStages) : 2 * P::kGroup;
+  // epilogue transpose scratch: 8 warps x 32 pixels x kEpiCols fp32
+  static constexpr int kEpiCols = BN >= 128 ? 16 : 8;
+  static constexpr int kEpiBytes = 8 * 32 * kEpiCols * 4;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two group buffers
   static constexpr int kHalf = BN / 2;                         // columns per epilogue warp
 };
 
-// K-major operand, rows of kRowBytes: SWIZZLE_128B (32 ch) or SWIZZLE_64B (16 ch)
-__device__ __forceinline__ uint64_t kdesc(uint32_t addr) {
-  return kKC == 32 ? sw128_desc(addr, 16, 1024, 2) : sw128_desc(addr, 16, 512, 4);
-}
-// MN-major operand (SW128_BASE32B), blocks of kKC pixel rows x 128 B
-__device__ __forceinline__ uint64_t mndesc(uint32_t addr) {
-  return sw128_desc(addr, kKC * 128, 512, kLayoutSw128Base32);
+// Output of a conv epilogue.  y: fp32 values (may be null).  F16: yhi/ylo fp16
+// pair of y * oscale.  TF32: ylo fp32 residual (y itself is hi; requires y).
+struct ConvOut {
+  float* y;
+  void* yhi;
+  void* ylo;
+  float oscale;
+};
+
+template <bool F16>
+__device__ __forceinline__ void store_pair4(const ConvOut& o, int64_t idx, float4 v) {
+  if (F16) {
+    const float s = o.oscale;
+    const float a[4] = {v.x * s, v.y * s, v.z * s, v.w * s};
+    __half h[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      h[i] = __float2half_rn(a[i]);
+      l[i] = __float2half_rn(__fsub_rn(a[i], __half2float(h[i])));
+    }
+    auto pack = [](__half a, __half b) {
+      return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+    };
+    if (o.yhi)
+      *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(o.yhi) + idx) =
+          make_uint2(pack(h[0], h[1]), pack(h[2], h[3]));
+    if (o.ylo)
+      *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(o.ylo) + idx) =
+          make_uint2(pack(l[0], l[1]), pack(l[2], l[3]));
+  } else if (o.ylo) {
+    float4 r;
+    float h;
+    split_tf32(v.x, h, r.x);
+    split_tf32(v.y, h, r.y);
+    split_tf32(v.z, h, r.z);
+    split_tf32(v.w, h, r.w);
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(o.ylo) + idx) = r;
+  }
 }
 
-__device__ __forceinline__ float4 lo4(float4 v) {
-  float4 r;
-  float h;
-  split_tf32(v.x, h, r.x);
-  split_tf32(v.y, h, r.y);
-  split_tf32(v.z, h, r.z);
-  split_tf32(v.w, h, r.w);
-  return r;
+template <bool F16>
+__device__ __forceinline__ float4 load_mask4(const void* mask, int64_t idx) {
+  if (F16) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(mask) + idx));
+    return make_float4(__half2float(__ushort_as_half((unsigned short)(u.x & 0xFFFFu))),
+                       __half2float(__ushort_as_half((unsigned short)(u.x >> 16))),
+                       __half2float(__ushort_as_half((unsigned short)(u.y & 0xFFFFu))),
+                       __half2float(__ushort_as_half((unsigned short)(u.y >> 16))));
+  }
+  return __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(mask) + idx));
 }
 
-// Persistent: each CTA (one per SM) walks tiles blockIdx.x, +gridDim.x, ...
-// The producer streams stages across tile boundaries, the MMA issuer keeps the
-// two TMEM group buffers busy across tiles, and the accumulate warps' epilogue
-// of tile t overlaps the first groups of tile t+1; barrier init, TMEM alloc
-// and descriptor prefetch happen once per CTA.
-template <int BN>
+template <int BN, bool F16>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
-                 const float* __restrict__ bias, const float* __restrict__ mask,
-                 float* __restrict__ y, float* __restrict__ ylo, float* __restrict__ colsum,
-                 int H, int W, int C, int epi) {
-  using Cfg = FwdCfg<BN>;
+                 const float* __restrict__ bias, const void* __restrict__ mask, ConvOut out,
+                 float* __restrict__ colsum, float unscale, int H, int W, int C, int epi, int dbg) {
+  using Cfg = FwdCfg<BN, F16>;
+  using P = Prec<F16>;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
+  constexpr int G = P::kGroup;
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
-  __shared__ float csum[4][BN];
+  __shared__ __align__(16) float csum[4][BN];
   uint8_t* base = align1024(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tiles_x = (W + kTW - 1) / kTW;
   const int ntiles = tiles_x * ((H + kTH - 1) / kTH);
-  const int cpt = C / kKC, KB = 9 * cpt;  // C % 32 == 0, so KB is even
-  const int NG = KB / kGroup;
+  const int cpt = C / 32, KB = 9 * cpt;  // stages per tile
+  const int NG = (KB + G - 1) / G;       // groups per tile (the last may be short)
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -145,9 +243,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int s = it % S, round = it / S;
           if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-          const int tap = kb / cpt, c0 = (kb - tap * cpt) * kKC;
+          const int tap = kb / cpt, c0 = (kb - tap * cpt) * 32;
           const int ky = tap / 3, kx = tap - 3 * ky;
           uint8_t* st = base + s * Cfg::kStageBytes;
+          if (dbg & 4) {  // profiling experiment: no operand traffic
+            mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
           tma_load_3d(st, &mx, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
           tma_load_3d(st + Cfg::kStageA, &mxl, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
@@ -158,118 +260,141 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---- MMA issuer: one group = kGroup stages (K = 32) into a fresh buffer
-      constexpr uint32_t idesc = idesc_tf32(128, BN, false, false);
+      // ---- MMA issuer: one group = G stages into a fresh TMEM buffer
+      constexpr uint32_t idesc = P::idesc(128, BN, false, false);
       int it = 0, gg = 0;  // stage and group counters across tiles
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int g = 0; g < NG; ++g, ++gg) {
           const int b = gg & 1;
-          if (gg >= 2) mbar_wait(&tempty[b], ((gg >> 1) - 1) & 1);
-          const uint32_t d = taddr + b * BN;
-          // per stage: the small cross terms first (accumulator still tiny), then hi*hi
-          for (int j = 0; j < kGroup; ++j, ++it) {
-            const int s = it % S;
-            mbar_wait(&full[s], (it / S) & 1);
-            tc_fence_after();
-            const uint32_t ah = smem_u32(base + s * Cfg::kStageBytes), al = ah + Cfg::kStageA,
-                           bh = ah + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
-#pragma unroll
-            for (int k = 0; k < kKC / 8; ++k) {
-              mma_tf32(d, kdesc(ah + 32 * k), kdesc(bl + 32 * k), idesc, (j | k) != 0);
-              mma_tf32(d, kdesc(al + 32 * k), kdesc(bh + 32 * k), idesc, 1);
-            }
-#pragma unroll
-            for (int k = 0; k < kKC / 8; ++k)
-              mma_tf32(d, kdesc(ah + 32 * k), kdesc(bh + 32 * k), idesc, 1);
-            mma_commit(&empty[s]);
+          if (gg >= 2 && !(dbg & 16)) mbar_wait(&tempty[b], ((gg >> 1) - 1) & 1);
+          const int ng = (g + 1) * G <= KB ? G : KB - g * G;
+          uint32_t a[G];
+          for (int j = 0; j < ng; ++j) {
+            const int s = (it + j) % S;
+            mbar_wait(&full[s], ((it + j) / S) & 1);
+            a[j] = smem_u32(base + s * Cfg::kStageBytes);
           }
+          tc_fence_after();
+          const uint32_t d = taddr + b * BN;
+          // the small cross terms of the whole group first, then hi*hi
+          for (int j = 0; j < ng && !(dbg & 2); ++j) {
+            const uint32_t ah = a[j], al = ah + Cfg::kStageA, bh = ah + 2 * Cfg::kStageA,
+                           bl = bh + Cfg::kStageB;
+#pragma unroll
+            for (int k = 0; k < P::kKSteps; ++k) {
+              P::mma(d, P::kdesc(ah + 32 * k), P::kdesc(bl + 32 * k), idesc, (j | k) != 0);
+              P::mma(d, P::kdesc(al + 32 * k), P::kdesc(bh + 32 * k), idesc, 1);
+            }
+          }
+          for (int j = 0; j < ng && !(dbg & 2); ++j) {
+            const uint32_t ah = a[j], bh = ah + 2 * Cfg::kStageA;
+#pragma unroll
+            for (int k = 0; k < P::kKSteps; ++k)
+              P::mma(d, P::kdesc(ah + 32 * k), P::kdesc(bh + 32 * k), idesc, 1);
+          }
+          if (dbg & 8) {  // profiling experiment (with 2|4): plain arrives, no commit latency
+            for (int j = 0; j < ng; ++j) mbar_arrive(&empty[(it + j) % S]);
+            it += ng;
+            mbar_arrive(&tfull[b]);
+            continue;
+          }
+          for (int j = 0; j < ng; ++j) mma_commit(&empty[(it + j) % S]);
+          it += ng;
           mma_commit(&tfull[b]);
         }
       }
     }
   } else {
     // ---- group accumulation in registers (round-to-nearest fp32 adds)
-    const int q = warp & 3;          // TMEM lane quarter
+    const int q = warp & 3;            // TMEM lane quarter
     const int half = (warp - 2) >> 2;  // column half
     const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * HALF;
     int gg = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int x0 = (tile % tiles_x) * kTW, y0 = (tile / tiles_x) * kTH;
-    float acc[HALF];
+      const int x0 = (tile % tiles_x) * kTW, y0 = (tile / tiles_x) * kTH;
+      float acc[HALF];
 #pragma unroll
-    for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
-    for (int g = 0; g < NG; ++g, ++gg) {
-      const int b = gg & 1;
-      mbar_wait(&tfull[b], (gg >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < HALF; c += (HALF < 32 ? HALF : 32)) {
-        uint32_t r[32];
-        if (HALF < 32)
-          tmem_ld16(lane_base + b * BN + c, r);
-        else
-          tmem_ld32(lane_base + b * BN + c, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < (HALF < 32 ? HALF : 32); ++j) acc[c + j] += __uint_as_float(r[j]);
+      for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
+      for (int g = 0; g < NG; ++g, ++gg) {
+        const int b = gg & 1;
+        if (dbg & 16) continue;  // profiling experiment: no accumulator handoff
+        mbar_wait(&tfull[b], (gg >> 1) & 1);
+        tc_fence_after();
+        if (!(dbg & 1)) drain_add<HALF>(lane_base + b * BN, acc);  // dbg 1: experiment, no drain
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
-    }
 
-    // ---- epilogue
-    const int m = q * 32 + lane;
-    const int py = y0 + m / kTW, px = x0 + m % kTW;
-    const bool valid = py < H && px < W;
-    const int64_t p = (int64_t)py * W + px;
-    const int n0 = half * HALF;
+      // ---- epilogue.  The drain leaves lane = pixel, registers = channels;
+      // global rows are pixel-major, so EC-column slices are transposed
+      // through a per-warp smem scratch (16-byte chunks XOR-swizzled:
+      // conflict-free both ways) and re-read as (pixel, 4-channel chunk)
+      // pairs: CPR lanes cover EC contiguous channels of one pixel.
+      constexpr int EC = Cfg::kEpiCols, CPR = EC / 4, RPL = 32 / EC;  // rows per 128 B bank line
+      float* scr = reinterpret_cast<float*>(base + S * Cfg::kStageBytes) + (warp - 2) * 32 * EC;
+      const int n0 = half * HALF;
+      const int kk = lane % CPR;  // this lane's 4-channel chunk after the transpose
 #pragma unroll
-    for (int j = 0; j < HALF; j += 4) {
-      float4 v = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-      if (epi == kEpiBiasRelu || epi == kEpiBias) {
-        const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n0 + j));
-        v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
-        if (epi == kEpiBiasRelu) {
-          v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
-        }
-      } else if (epi == kEpiMask) {
-        float4 mk = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid) mk = __ldg(reinterpret_cast<const float4*>(mask + p * BN + n0 + j));
-        v.x = mk.x > 0.f ? v.x : 0.f;
-        v.y = mk.y > 0.f ? v.y : 0.f;
-        v.z = mk.z > 0.f ? v.z : 0.f;
-        v.w = mk.w > 0.f ? v.w : 0.f;
-      }
-      if (!valid) v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (colsum) {  // deterministic per-tile column sums (bias gradient of this tensor)
-        float s0 = v.x, s1 = v.y, s2 = v.z, s3 = v.w;
+      for (int c0 = 0; c0 < HALF; c0 += EC) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-          s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+        for (int k = 0; k < CPR; ++k) {
+          const int pos = k ^ ((lane / RPL) % CPR);
+          *reinterpret_cast<float4*>(scr + lane * EC + pos * 4) =
+              make_float4(acc[c0 + 4 * k] * unscale, acc[c0 + 4 * k + 1] * unscale,
+                          acc[c0 + 4 * k + 2] * unscale, acc[c0 + 4 * k + 3] * unscale);
         }
-        if (lane == 0) {
-          csum[q][n0 + j] = s0;
-          csum[q][n0 + j + 1] = s1;
-          csum[q][n0 + j + 2] = s2;
-          csum[q][n0 + j + 3] = s3;
+        __syncwarp();
+        const int n = n0 + c0 + 4 * kk;  // first channel of this lane's chunk
+        float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (epi == kEpiBiasRelu || epi == kEpiBias) bb = __ldg(reinterpret_cast<const float4*>(bias + n));
+        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+        for (int rr = 0; rr < CPR; ++rr) {  // 32 / CPR pixels per pass
+          const int pr = lane / CPR + rr * (32 / CPR);  // pixel row in the warp's 32
+          float4 v = *reinterpret_cast<const float4*>(scr + pr * EC + (kk ^ ((pr / RPL) % CPR)) * 4);
+          const int m = q * 32 + pr;
+          const int py = y0 + m / kTW, px = x0 + m % kTW;
+          const bool valid = py < H && px < W;
+          const int64_t idx = ((int64_t)py * W + px) * BN + n;
+          if (epi == kEpiBiasRelu || epi == kEpiBias) {
+            v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
+            if (epi == kEpiBiasRelu) {
+              v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
+            }
+          } else if (epi == kEpiMask) {
+            float4 mk = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid) mk = load_mask4<F16>(mask, idx);
+            v.x = mk.x > 0.f ? v.x : 0.f;
+            v.y = mk.y > 0.f ? v.y : 0.f;
+            v.z = mk.z > 0.f ? v.z : 0.f;
+            v.w = mk.w > 0.f ? v.w : 0.f;
+          }
+          if (valid) {
+            cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w;
+            if (out.y) *reinterpret_cast<float4*>(out.y + idx) = v;
+            store_pair4<F16>(out, idx, v);
+          }
         }
+        if (colsum) {  // deterministic per-tile column sums (bias gradient of this tensor)
+#pragma unroll
+          for (int o = CPR; o < 32; o <<= 1) {
+            cs.x += __shfl_xor_sync(0xffffffffu, cs.x, o);
+            cs.y += __shfl_xor_sync(0xffffffffu, cs.y, o);
+            cs.z += __shfl_xor_sync(0xffffffffu, cs.z, o);
+            cs.w += __shfl_xor_sync(0xffffffffu, cs.w, o);
+          }
+          if (lane < CPR) *reinterpret_cast<float4*>(&csum[q][n]) = cs;
+        }
+        __syncwarp();  // scratch reused by the next slice
       }
-      if (valid) {
-        *reinterpret_cast<float4*>(y + p * BN + n0 + j) = v;
-        if (ylo) *reinterpret_cast<float4*>(ylo + p * BN + n0 + j) = lo4(v);
+      if (colsum) {  // the 8 accumulate warps only (named barrier 1)
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        for (int n = tid - 64; n < BN; n += 256)
+          colsum[(int64_t)tile * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // csum reusable for the next tile
       }
     }
-    if (colsum) {  // the 8 accumulate warps only (named barrier 1)
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      for (int n = tid - 64; n < BN; n += 256)
-        colsum[(int64_t)tile * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // csum reusable for the next tile
-    }
-    }  // tile loop
   }
   tc_fence_before();
   __syncthreads();
@@ -280,25 +405,27 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 // 3x3 conv wgrad as a tcgen05 GEMM with both operands MN-major:
 //   D[m = (tap, c)][n = o] = sum_p X[p + d(tap)][c] * G[p][o]
 //   M = 128 (tap, c) rows (4 blocks of 32 channels, each within one tap),
-//   N = Cout, K = pixels in chunks of 32 (one image-row segment).
-// TMA boxes (32 ch x 32 px) land as [pixel][32 ch] rows with the 32-byte
-// swizzle atom (SWIZZLE_128B_ATOM_32B), the MN-major tf32 operand layout
-// (UMMA SWIZZLE_128B_BASE32B).  The pixel range is split across CTAs
-// (deterministic split-K); each CTA writes its partial dW[o][tap][c] and Adam
-// reduces the partials in fixed order.  Accumulation is grouped exactly like
-// the forward kernel (fresh TMEM buffer per group, fp32 register sums).
+//   N = Cout, K = pixels in stages of 32 (one image-row segment).
+// TMA boxes (32 ch x 32 px) land as [pixel][32 ch] rows: the MN-major
+// operand layout (TF32: 128-byte rows with the 32-byte swizzle atom,
+// SWIZZLE_128B_BASE32B; FP16: 64-byte rows, SWIZZLE_64B).  The pixel range is
+// split across CTAs (deterministic split-K); each CTA writes its partial
+// dW[o][tap][c] (scale removed) and the partials are reduced in fixed order
+// before Adam.  Accumulation is grouped exactly like the forward kernel.
 // ---------------------------------------------------------------------------
-constexpr int kSegW = kKC;  // pixels per stage (one image-row segment)
+constexpr int kSegW = 32;  // pixels per stage (one image-row segment)
 
-template <int BN>
+template <int BN, bool F16>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_wgrad3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                   const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mgl,
-                  float* __restrict__ part, int H, int W, int C, int nsplit) {
-  using Cfg = FwdCfg<BN>;  // same stage bytes: A = 4 x 16 px x 128 B, B = BN/32 x 16 px x 128 B
-  constexpr int kBlk = kSegW * 128;  // bytes of one 32-channel MN block
+                  float* __restrict__ part, float unscale, int H, int W, int C, int nsplit) {
+  using Cfg = FwdCfg<BN, F16>;  // same stage bytes: A = 4 x 32 px rows, B = BN/32 x 32 px rows
+  using P = Prec<F16>;
+  constexpr int kBlk = kSegW * P::kRow;  // bytes of one 32-channel MN block
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
+  constexpr int G = P::kGroup;
   extern __shared__ uint8_t smem_raw[];
   __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
@@ -311,7 +438,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int nseg = segs_x * H;
   const int s0 = (int)((int64_t)nseg * split / nsplit), s1 = (int)((int64_t)nseg * (split + 1) / nsplit);
   const int KB = s1 - s0;
-  const int NG = (KB + kGroup - 1) / kGroup;
+  const int NG = (KB + G - 1) / G;
   int nblk_a = (K9 - m0 + 31) / 32;
   if (nblk_a > 4) nblk_a = 4;
   const uint32_t stage_bytes = (uint32_t)nblk_a * kBlk * 2u + (uint32_t)Cfg::kStageB * 2u;
@@ -361,28 +488,37 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(128, BN, true, true);
+      constexpr uint32_t idesc = P::idesc(128, BN, true, true);
+      int it = 0;
       for (int g = 0; g < NG; ++g) {
         const int b = g & 1;
         if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-        const int ng = (g + 1) * kGroup <= KB ? kGroup : KB - g * kGroup;
-        const uint32_t d = taddr + b * BN;
-        for (int j = 0; j < ng; ++j) {  // per stage: cross terms first, then hi*hi
-          const int kb = g * kGroup + j, s = kb % S;
-          mbar_wait(&full[s], (kb / S) & 1);
-          tc_fence_after();
-          const uint32_t ah = smem_u32(base + s * Cfg::kStageBytes), al = ah + Cfg::kStageA,
-                         bh = ah + 2 * Cfg::kStageA, bl = bh + Cfg::kStageB;
-#pragma unroll
-          for (int k = 0; k < kSegW / 8; ++k) {
-            mma_tf32(d, mndesc(ah + 1024 * k), mndesc(bl + 1024 * k), idesc, (j | k) != 0);
-            mma_tf32(d, mndesc(al + 1024 * k), mndesc(bh + 1024 * k), idesc, 1);
-          }
-#pragma unroll
-          for (int k = 0; k < kSegW / 8; ++k)
-            mma_tf32(d, mndesc(ah + 1024 * k), mndesc(bh + 1024 * k), idesc, 1);
-          mma_commit(&empty[s]);
+        const int ng = (g + 1) * G <= KB ? G : KB - g * G;
+        uint32_t a[G];
+        for (int j = 0; j < ng; ++j) {
+          const int s = (it + j) % S;
+          mbar_wait(&full[s], ((it + j) / S) & 1);
+          a[j] = smem_u32(base + s * Cfg::kStageBytes);
         }
+        tc_fence_after();
+        const uint32_t d = taddr + b * BN;
+        for (int j = 0; j < ng; ++j) {  // cross terms of the group first, then hi*hi
+          const uint32_t ah = a[j], al = ah + Cfg::kStageA, bh = ah + 2 * Cfg::kStageA,
+                         bl = bh + Cfg::kStageB;
+#pragma unroll
+          for (int k = 0; k < P::kKSteps; ++k) {
+            P::mma(d, P::mndesc(ah + 1024 * k), P::mndesc(bl + 1024 * k), idesc, (j | k) != 0);
+            P::mma(d, P::mndesc(al + 1024 * k), P::mndesc(bh + 1024 * k), idesc, 1);
+          }
+        }
+        for (int j = 0; j < ng; ++j) {
+          const uint32_t ah = a[j], bh = ah + 2 * Cfg::kStageA;
+#pragma unroll
+          for (int k = 0; k < P::kKSteps; ++k)
+            P::mma(d, P::mndesc(ah + 1024 * k), P::mndesc(bh + 1024 * k), idesc, 1);
+        }
+        for (int j = 0; j < ng; ++j) mma_commit(&empty[(it + j) % S]);
+        it += ng;
         mma_commit(&tfull[b]);
       }
     }
@@ -397,17 +533,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const int b = g & 1;
       mbar_wait(&tfull[b], (g >> 1) & 1);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < HALF; c += (HALF < 32 ? HALF : 32)) {
-        uint32_t r[32];
-        if (HALF < 32)
-          tmem_ld16(lane_base + b * BN + c, r);
-        else
-          tmem_ld32(lane_base + b * BN + c, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < (HALF < 32 ? HALF : 32); ++j) acc[c + j] += __uint_as_float(r[j]);
-      }
+      drain_add<HALF>(lane_base + b * BN, acc);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[b]);
@@ -416,7 +542,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     if (m < K9) {
       float* dst = part + (int64_t)split * BN * K9 + m;
 #pragma unroll
-      for (int j = 0; j < HALF; ++j) dst[(int64_t)(half * HALF + j) * K9] = acc[j];
+      for (int j = 0; j < HALF; ++j) dst[(int64_t)(half * HALF + j) * K9] = acc[j] * unscale;
     }
   }
   tc_fence_before();
@@ -429,6 +555,17 @@ __global__ void k_split_lo(const float* __restrict__ x, float* __restrict__ lo, 
        i += (int64_t)gridDim.x * blockDim.x) {
     float h;
     split_tf32(x[i], h, lo[i]);
+  }
+}
+
+__global__ void k_split_f16(const float* __restrict__ x, __half* __restrict__ hi,
+                            __half* __restrict__ lo, float scale, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float a = x[i] * scale;
+    const __half h = __float2half_rn(a);
+    hi[i] = h;
+    lo[i] = __float2half_rn(__fsub_rn(a, __half2float(h)));
   }
 }
 
@@ -448,50 +585,104 @@ int encoder() {
   return N2F_OK;
 }
 
-// NHWC activation [H][W][C] fp32 viewed as 3-D (C, W, H).
-int map_act(CUtensorMap* m, const float* p, int C, int W, int H, int bc, int bw, int bh,
+// NHWC activation [H][W][C] viewed as 3-D (C, W, H).
+int map_act(CUtensorMap* m, const void* p, bool f16, int C, int W, int H, int bc, int bw, int bh,
             CUtensorMapSwizzle sw) {
   N2F_TRY(encoder());
+  const cuuint64_t es = f16 ? 2 : 4;
   const cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H};
-  const cuuint64_t strides[2] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4};
+  const cuuint64_t strides[2] = {(cuuint64_t)C * es, (cuuint64_t)W * C * es};
   const cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh};
-  const cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p), dims, strides,
-                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        3, const_cast<void*>(p), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(act) failed: %d", (int)r);
   return N2F_OK;
 }
 
-// Row-major matrix [rows][cols] fp32 viewed as 2-D (cols, rows).
-int map_mat(CUtensorMap* m, const float* p, int cols, int rows, int bc, int br,
+// Row-major matrix [rows][cols] viewed as 2-D (cols, rows).
+int map_mat(CUtensorMap* m, const void* p, bool f16, int cols, int rows, int bc, int br,
             CUtensorMapSwizzle sw) {
   N2F_TRY(encoder());
+  const cuuint64_t es = f16 ? 2 : 4;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * es};
   const cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
-  const cuuint32_t es[2] = {1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(p), dims, strides,
-                        box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        2, const_cast<void*>(p), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(mat) failed: %d", (int)r);
   return N2F_OK;
 }
 
-template <int BN>
-int set_attr_bn() {
-  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FwdCfg<BN>::kSmem));
+template <int BN, bool F16>
+int set_attr_one() {
+  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                FwdCfg<BN, F16>::kSmem));
+  N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                FwdCfg<BN, F16>::kSmem));
   return N2F_OK;
 }
 
-template <int BN>
-int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const float* mask, float* y,
-                      float* ylo, float* colsum, int epi, cudaStream_t st) {
-  k_conv3x3_tc<BN><<<pl.grid, kThreadsTc, FwdCfg<BN>::kSmem, st>>>(
-      pl.mx, pl.mxl, pl.mw, pl.mwl, bias, mask, y, ylo, colsum, pl.H, pl.W, pl.C, epi);
+int set_attrs_once() {
+  static bool done = false;
+  if (done) return N2F_OK;
+  N2F_TRY((set_attr_one<32, false>()));
+  N2F_TRY((set_attr_one<64, false>()));
+  N2F_TRY((set_attr_one<128, false>()));
+  N2F_TRY((set_attr_one<256, false>()));
+  N2F_TRY((set_attr_one<32, true>()));
+  N2F_TRY((set_attr_one<64, true>()));
+  N2F_TRY((set_attr_one<128, true>()));
+  N2F_TRY((set_attr_one<256, true>()));
+  done = true;
+  return N2F_OK;
+}
+
+template <int BN, bool F16>
+int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask, const ConvOut& o,
+                      float* colsum, int epi, cudaStream_t st) {
+  k_conv3x3_tc<BN, F16><<<pl.grid, kThreadsTc, FwdCfg<BN, F16>::kSmem, st>>>(
+      pl.mx, pl.mxl, pl.mw, pl.mwl, bias, mask, o, colsum, pl.unscale, pl.H, pl.W, pl.C, epi,
+      pl.dbg);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
+}
+
+template <bool F16>
+int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, const ConvOut& o,
+                     float* colsum, int epi, cudaStream_t st) {
+  switch (pl.N) {
+    case 32: return launch_conv_tc_bn<32, F16>(pl, bias, mask, o, colsum, epi, st);
+    case 64: return launch_conv_tc_bn<64, F16>(pl, bias, mask, o, colsum, epi, st);
+    case 128: return launch_conv_tc_bn<128, F16>(pl, bias, mask, o, colsum, epi, st);
+    case 256: return launch_conv_tc_bn<256, F16>(pl, bias, mask, o, colsum, epi, st);
+  }
+  return fail(N2F_ERR_ARG, "conv_tc_launch: N=%d", pl.N);
+}
+
+template <int BN, bool F16>
+int launch_wgrad_tc_bn(const WgradTcPlan& pl, float* part, cudaStream_t st) {
+  dim3 grid(pl.mblocks, pl.nsplit);
+  k_wgrad3x3_tc<BN, F16><<<grid, kThreadsTc, FwdCfg<BN, F16>::kSmem, st>>>(
+      pl.mx, pl.mxl, pl.mg, pl.mgl, part, pl.unscale, pl.H, pl.W, pl.C, pl.nsplit);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+template <bool F16>
+int launch_wgrad_tc_p(const WgradTcPlan& pl, float* part, cudaStream_t st) {
+  switch (pl.N) {
+    case 32: return launch_wgrad_tc_bn<32, F16>(pl, part, st);
+    case 64: return launch_wgrad_tc_bn<64, F16>(pl, part, st);
+    case 128: return launch_wgrad_tc_bn<128, F16>(pl, part, st);
+    case 256: return launch_wgrad_tc_bn<256, F16>(pl, part, st);
+  }
+  return fail(N2F_ERR_ARG, "wgrad_tc_launch: N=%d", pl.N);
 }
 
 int sm_count() {
@@ -505,76 +696,47 @@ int sm_count() {
   return n;
 }
 
-template <int BN>
-int set_attr_wg() {
-  N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FwdCfg<BN>::kSmem));
-  return N2F_OK;
-}
-
-template <int BN>
-int launch_wgrad_tc_bn(const WgradTcPlan& pl, float* part, cudaStream_t st) {
-  dim3 grid(pl.mblocks, pl.nsplit);
-  k_wgrad3x3_tc<BN><<<grid, kThreadsTc, FwdCfg<BN>::kSmem, st>>>(pl.mx, pl.mxl, pl.mg, pl.mgl, part,
-                                                                pl.H, pl.W, pl.C, pl.nsplit);
-  N2F_LAUNCH_CHECK();
-  return N2F_OK;
-}
-
-int set_attrs_once() {
-  static bool done = false;
-  if (done) return N2F_OK;
-  N2F_TRY(set_attr_bn<32>());
-  N2F_TRY(set_attr_bn<64>());
-  N2F_TRY(set_attr_bn<128>());
-  N2F_TRY(set_attr_bn<256>());
-  N2F_TRY(set_attr_wg<32>());
-  N2F_TRY(set_attr_wg<64>());
-  N2F_TRY(set_attr_wg<128>());
-  N2F_TRY(set_attr_wg<256>());
-  done = true;
-  return N2F_OK;
-}
-
 }  // namespace
 
 bool tc_supported(int cin, int cout) {
   return cin % 32 == 0 && (cout == 32 || cout == 64 || cout == 128 || cout == 256);
 }
 
-int conv_tc_plan(ConvTcPlan* pl, const float* x, const float* xlo, const float* w, const float* wlo,
-                 int H, int W, int C, int N) {
+int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, int W, int C, int N,
+                 bool f16) {
   if (!tc_supported(C, N)) return fail(N2F_ERR_ARG, "conv_tc_plan: C=%d N=%d", C, N);
   N2F_TRY(set_attrs_once());  // outside any stream capture
   pl->H = H;
   pl->W = W;
   pl->C = C;
   pl->N = N;
+  pl->f16 = f16;
+  pl->unscale = ldexpf(1.f, -(x.exp + w.exp));
+  // N2F_TC_DEBUG: kernel-structure experiments for profiling only (results
+  // are wrong when set): 1 skip the TMEM drain, 2 skip the MMAs, 4 skip TMA
+  const char* dbg = getenv("N2F_TC_DEBUG");
+  pl->dbg = dbg ? atoi(dbg) : 0;
   // persistent grid: one CTA per SM (two for the narrow layers, whose smem
   // and register footprints allow it), each walking tiles with a fixed stride
   const int tiles = conv_tc_tiles(H, W);
   const int per_sm = N <= 64 ? 2 : 1;
   pl->grid = tiles < per_sm * sm_count() ? tiles : per_sm * sm_count();
-  pl->cs = 1;
-  const CUtensorMapSwizzle sw = kKC == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  N2F_TRY(map_act(&pl->mx, x, C, W, H, kKC, kTW, kTH, sw));
-  N2F_TRY(map_act(&pl->mxl, xlo, C, W, H, kKC, kTW, kTH, sw));
-  N2F_TRY(map_mat(&pl->mw, w, 9 * C, N, kKC, N, sw));
-  N2F_TRY(map_mat(&pl->mwl, wlo, 9 * C, N, kKC, N, sw));
+  const CUtensorMapSwizzle sw = f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  N2F_TRY(map_act(&pl->mx, x.hi, f16, C, W, H, 32, kTW, kTH, sw));
+  N2F_TRY(map_act(&pl->mxl, x.lo, f16, C, W, H, 32, kTW, kTH, sw));
+  N2F_TRY(map_mat(&pl->mw, w.hi, f16, 9 * C, N, 32, N, sw));
+  N2F_TRY(map_mat(&pl->mwl, w.lo, f16, 9 * C, N, 32, N, sw));
   return N2F_OK;
 }
 
 int conv_tc_tiles(int H, int W) { return ((W + kTW - 1) / kTW) * ((H + kTH - 1) / kTH); }
 
-int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const float* mask, float* y, float* ylo,
-                   float* colsum, int epi, cudaStream_t st) {
-  switch (pl.N) {
-    case 32: return launch_conv_tc_bn<32>(pl, bias, mask, y, ylo, colsum, epi, st);
-    case 64: return launch_conv_tc_bn<64>(pl, bias, mask, y, ylo, colsum, epi, st);
-    case 128: return launch_conv_tc_bn<128>(pl, bias, mask, y, ylo, colsum, epi, st);
-    case 256: return launch_conv_tc_bn<256>(pl, bias, mask, y, ylo, colsum, epi, st);
-  }
-  return fail(N2F_ERR_ARG, "conv_tc_launch: N=%d", pl.N);
+int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* y, void* yhi,
+                   void* ylo, float oscale, float* colsum, int epi, cudaStream_t st) {
+  const ConvOut o{y, yhi, ylo, oscale};
+  if (!pl.f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
+  return pl.f16 ? launch_conv_tc_p<true>(pl, bias, mask, o, colsum, epi, st)
+                : launch_conv_tc_p<false>(pl, bias, mask, o, colsum, epi, st);
 }
 
 int wgrad_tc_nsplit(int cin, int H, int W) {
@@ -586,8 +748,8 @@ int wgrad_tc_nsplit(int cin, int H, int W) {
   return n;
 }
 
-int wgrad_tc_plan(WgradTcPlan* pl, const float* x, const float* xlo, const float* g, const float* glo,
-                  int H, int W, int C, int N, int nsplit) {
+int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H, int W, int C,
+                  int N, int nsplit, bool f16) {
   if (!tc_supported(C, N)) return fail(N2F_ERR_ARG, "wgrad_tc_plan: C=%d N=%d", C, N);
   N2F_TRY(set_attrs_once());
   pl->H = H;
@@ -596,28 +758,33 @@ int wgrad_tc_plan(WgradTcPlan* pl, const float* x, const float* xlo, const float
   pl->N = N;
   pl->mblocks = (9 * C + 127) / 128;
   pl->nsplit = nsplit;
-  const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-  N2F_TRY(map_act(&pl->mx, x, C, W, H, 32, kSegW, 1, sw));
-  N2F_TRY(map_act(&pl->mxl, xlo, C, W, H, 32, kSegW, 1, sw));
-  N2F_TRY(map_act(&pl->mg, g, N, W, H, 32, kSegW, 1, sw));
-  N2F_TRY(map_act(&pl->mgl, glo, N, W, H, 32, kSegW, 1, sw));
+  pl->f16 = f16;
+  pl->unscale = ldexpf(1.f, -(x.exp + g.exp));
+  const CUtensorMapSwizzle sw = f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+  N2F_TRY(map_act(&pl->mx, x.hi, f16, C, W, H, 32, kSegW, 1, sw));
+  N2F_TRY(map_act(&pl->mxl, x.lo, f16, C, W, H, 32, kSegW, 1, sw));
+  N2F_TRY(map_act(&pl->mg, g.hi, f16, N, W, H, 32, kSegW, 1, sw));
+  N2F_TRY(map_act(&pl->mgl, g.lo, f16, N, W, H, 32, kSegW, 1, sw));
   return N2F_OK;
 }
 
 int wgrad_tc_launch(const WgradTcPlan& pl, float* part, cudaStream_t st) {
-  switch (pl.N) {
-    case 32: return launch_wgrad_tc_bn<32>(pl, part, st);
-    case 64: return launch_wgrad_tc_bn<64>(pl, part, st);
-    case 128: return launch_wgrad_tc_bn<128>(pl, part, st);
-    case 256: return launch_wgrad_tc_bn<256>(pl, part, st);
-  }
-  return fail(N2F_ERR_ARG, "wgrad_tc_launch: N=%d", pl.N);
+  return pl.f16 ? launch_wgrad_tc_p<true>(pl, part, st) : launch_wgrad_tc_p<false>(pl, part, st);
 }
 
 int split_lo(const float* x, float* lo, int64_t n, cudaStream_t st) {
   int64_t blocks = (n + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   k_split_lo<<<(unsigned)blocks, 256, 0, st>>>(x, lo, n);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int split_f16(const float* x, void* hi, void* lo, int exp2, int64_t n, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  k_split_f16<<<(unsigned)blocks, 256, 0, st>>>(x, reinterpret_cast<__half*>(hi),
+                                                reinterpret_cast<__half*>(lo), ldexpf(1.f, exp2), n);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

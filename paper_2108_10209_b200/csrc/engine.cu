@@ -94,6 +94,16 @@ struct n2f_ctx {
   float* gB_lo = nullptr;
   float* vA_lo = nullptr;
   float* vB_lo = nullptr;
+  // FP16 tensor-core mode (conv_impl 3): fp16 (hi, lo) pairs of the scaled
+  // operands replace the tf32 residuals; activations and weights carry
+  // 2^kExpAct / 2^kExpW, gradients 2^exp_g (see setup)
+  bool f16 = false;
+  int exp_g = 0;
+  __half* w16[2] = {};            // hi, lo arenas (same layout as params)
+  __half* wt16[2][kLayers] = {};  // dgrad-transposed pairs
+  __half* act16[2][kLayers] = {}; // layer outputs 0..6
+  __half* g16[2][2] = {};         // [A/B][hi/lo] gradient ping-pong
+  __half* v16[2][2] = {};         // [A/B][hi/lo] validation ping-pong
   ConvTcPlan fwd_plan[2][kLayers]{};
   ConvTcPlan dgrad_plan[2][kLayers]{};
   ConvTcPlan val_plan[kLayers]{};
@@ -194,28 +204,49 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
   const int64_t P = (int64_t)h * w;
   const float* x0 = c->pin + k * c->plane;
   const float* tgt = c->ptgt + k * c->plane;
-  PROF(kPFirst, 0, conv_flop(P, 0),
-       conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1, c->act_lo[0]));
-  for (int li = 1; li < 8; ++li)
+  const bool f16 = c->f16;
+  const float sa = ldexpf(1.f, kExpAct), sg = ldexpf(1.f, c->exp_g);
+  if (f16) {
+    PROF(kPFirst, 0, conv_flop(P, 0),
+         conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1));
+    PROF(kPFirst, 0, 0.0,
+         split_f16(c->act[0], c->act16[0][0], c->act16[1][0], kExpAct, P * kCout[0], st));
+  } else {
+    PROF(kPFirst, 0, conv_flop(P, 0),
+         conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1, c->act_lo[0]));
+  }
+  for (int li = 1; li < 8; ++li) {
+    float* y = (!f16 || li == 7) ? c->act[li] : nullptr;
+    void* yhi = (f16 && li < 7) ? c->act16[0][li] : nullptr;
+    void* ylo = li < 7 ? (f16 ? (void*)c->act16[1][li] : (void*)c->act_lo[li]) : nullptr;
     PROF(kPFwd, li, conv_flop(P, li),
-         conv_tc_launch(c->fwd_plan[sc][li], B_(c, li), nullptr, c->act[li],
-                        li < 7 ? c->act_lo[li] : nullptr, nullptr, kEpiBiasRelu, st));
+         conv_tc_launch(c->fwd_plan[sc][li], B_(c, li), nullptr, y, yhi, ylo, sa, nullptr,
+                        kEpiBiasRelu, st));
+  }
   PROF(kPHead, 8, 6.0 * P * kMaxC,
-       launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, c->gA, c->part_w[8], c->part_b[8],
-                         c->part_loss + (int64_t)k * c->nblk_head, c->z, P, c->nblk_head,
-                         c->cfg.loss, c->step_counter, st, c->gA_lo, c->part_b[7]));
+       launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, f16 ? nullptr : c->gA, c->part_w[8],
+                         c->part_b[8], c->part_loss + (int64_t)k * c->nblk_head, c->z, P,
+                         c->nblk_head, c->cfg.loss, c->step_counter, st,
+                         f16 ? nullptr : c->gA_lo, c->part_b[7], f16 ? c->g16[0][0] : nullptr,
+                         f16 ? c->g16[0][1] : nullptr, sg));
   float* g = c->gA;
   float* gn = c->gB;
-  float* gnl = c->gB_lo;
   for (int li = 7; li >= 1; --li) {
     PROF(kPWgrad, li, conv_flop(P, li), wgrad_tc_launch(c->wgrad_plan[sc][li], c->part_w[li], st));
+    // output pair goes to the buffer this layer does not read: gB when li is odd
+    const int nb = (li & 1) ? 1 : 0;
+    void *yhi = nullptr, *ylo = nullptr;
+    if (li > 1) {
+      yhi = f16 ? c->g16[nb][0] : nullptr;
+      ylo = f16 ? (void*)c->g16[nb][1] : (void*)(nb ? c->gB_lo : c->gA_lo);
+    }
+    const void* mask = f16 ? (const void*)c->act16[0][li - 1] : (const void*)c->act[li - 1];
     PROF(kPDgrad, li, conv_flop(P, li),
-         conv_tc_launch(c->dgrad_plan[sc][li], nullptr, c->act[li - 1], gn, li > 1 ? gnl : nullptr,
-                        li > 1 ? c->part_b[li - 1] : nullptr, kEpiMask, st));
+         conv_tc_launch(c->dgrad_plan[sc][li], nullptr, mask, (!f16 || li == 1) ? gn : nullptr, yhi,
+                        ylo, sg, li > 1 ? c->part_b[li - 1] : nullptr, kEpiMask, st));
     float* t = g;
     g = gn;
     gn = t;
-    gnl = (gnl == c->gB_lo) ? c->gA_lo : c->gB_lo;
   }
   PROF(kPWgradFirst, 0, conv_flop(P, 0),
        wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
@@ -226,14 +257,25 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
 
 int enqueue_validate_tc(n2f_ctx* c) {
   cudaStream_t st = c->stream;
-  PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
-       conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1, c->vA_lo));
+  const bool f16 = c->f16;
+  if (f16) {
+    PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
+         conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1));
+    PROF(kPValFirst, 0, 0.0,
+         split_f16(c->vA, c->v16[0][0], c->v16[0][1], kExpAct, c->Pv * kCout[0], st));
+  } else {
+    PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
+         conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1,
+                         c->vA_lo));
+  }
   for (int li = 1; li < 8; ++li) {
-    float* out = (li & 1) ? c->vB : c->vA;
-    float* outl = (li & 1) ? c->vB_lo : c->vA_lo;
+    const int ob = (li & 1) ? 1 : 0;  // layer li writes vB when odd
+    float* out = (!f16 || li == 7) ? (ob ? c->vB : c->vA) : nullptr;
+    void* yhi = (f16 && li < 7) ? c->v16[ob][0] : nullptr;
+    void* ylo = li < 7 ? (f16 ? (void*)c->v16[ob][1] : (void*)(ob ? c->vB_lo : c->vA_lo)) : nullptr;
     PROF(kPValConv, li, conv_flop(c->Pv, li),
-         conv_tc_launch(c->val_plan[li], B_(c, li), nullptr, out, li < 7 ? outl : nullptr, nullptr,
-                        kEpiBiasRelu, st));
+         conv_tc_launch(c->val_plan[li], B_(c, li), nullptr, out, yhi, ylo, ldexpf(1.f, kExpAct),
+                        nullptr, kEpiBiasRelu, st));
   }
   // layer 7 (odd) wrote vB
   PROF(kPHeadVal, 8, 2.0 * c->Pv * kMaxC,
@@ -427,7 +469,7 @@ int setup(n2f_ctx* c) {
     N2F_TRY(dalloc(c, &c->part_w[li], nw * c->pnum[2 * li]));
     N2F_TRY(dalloc(c, &c->part_b[li], nb * c->pnum[2 * li + 1]));
   }
-  if (c->tc) {
+  if (c->tc && !c->f16) {
     N2F_TRY(dalloc(c, &c->params_lo, c->ptotal));
     for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt_lo[li], c->pnum[2 * li]));
     for (int li = 0; li < 7; ++li) N2F_TRY(dalloc(c, &c->act_lo[li], c->Pt * kCout[li]));
@@ -435,27 +477,67 @@ int setup(n2f_ctx* c) {
     N2F_TRY(dalloc(c, &c->gB_lo, c->Pt * kMaxC));
     N2F_TRY(dalloc(c, &c->vA_lo, c->Pv * kMaxC));
     N2F_TRY(dalloc(c, &c->vB_lo, c->Pv * kMaxC));
+  }
+  if (c->f16) {
+    // gradient scale: |dL/dz| <= 1/P per pixel, so 2^ceil(log2 P) lifts the
+    // head gradient to O(1); kExpAct more keeps small entries out of the
+    // fp16 subnormal range
+    int lg = 0;
+    while ((int64_t(1) << lg) < c->Pt) ++lg;
+    c->exp_g = lg + kExpAct;
+    for (int q = 0; q < 2; ++q) {
+      N2F_TRY(dalloc(c, &c->w16[q], c->ptotal));
+      for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt16[q][li], c->pnum[2 * li]));
+      for (int li = 0; li < 7; ++li) N2F_TRY(dalloc(c, &c->act16[q][li], c->Pt * kCout[li]));
+      for (int ab = 0; ab < 2; ++ab) {
+        N2F_TRY(dalloc(c, &c->g16[ab][q], c->Pt * kMaxC));
+        N2F_TRY(dalloc(c, &c->v16[ab][q], c->Pv * kMaxC));
+      }
+    }
+  }
+  if (c->tc) {
+    const bool f16 = c->f16;
+    // operand pairs of layer li's input activation, its weights (forward and
+    // dgrad-transposed) and the gradient buffer A (ab 0) or B (ab 1)
+    auto act_op = [&](int li) -> TcOperand {
+      return f16 ? TcOperand{c->act16[0][li], c->act16[1][li], kExpAct}
+                 : TcOperand{c->act[li], c->act_lo[li], 0};
+    };
+    auto w_op = [&](int li) -> TcOperand {
+      const int64_t o = c->poff[2 * li];
+      return f16 ? TcOperand{c->w16[0] + o, c->w16[1] + o, kExpW}
+                 : TcOperand{c->params + o, c->params_lo + o, 0};
+    };
+    auto wt_op = [&](int li) -> TcOperand {
+      return f16 ? TcOperand{c->wt16[0][li], c->wt16[1][li], kExpW}
+                 : TcOperand{c->wt[li], c->wt_lo[li], 0};
+    };
+    auto g_op = [&](int ab) -> TcOperand {
+      if (f16) return TcOperand{c->g16[ab][0], c->g16[ab][1], c->exp_g};
+      return ab ? TcOperand{c->gB, c->gB_lo, 0} : TcOperand{c->gA, c->gA_lo, 0};
+    };
+    auto v_op = [&](int ab) -> TcOperand {
+      if (f16) return TcOperand{c->v16[ab][0], c->v16[ab][1], kExpAct};
+      return ab ? TcOperand{c->vB, c->vB_lo, 0} : TcOperand{c->vA, c->vA_lo, 0};
+    };
     for (int sc = 0; sc < 2; ++sc) {
       const int h = c->ph[2 * sc], w = c->pw[2 * sc];
       for (int li = 1; li < 8; ++li) {
-        N2F_TRY(conv_tc_plan(&c->fwd_plan[sc][li], c->act[li - 1], c->act_lo[li - 1],
-                             c->params + c->poff[2 * li], c->params_lo + c->poff[2 * li], h, w,
-                             kCin[li], kCout[li]));
-        const bool odd = li & 1;  // L8 (li 7) reads gA (head output), then alternate
-        N2F_TRY(conv_tc_plan(&c->dgrad_plan[sc][li], odd ? c->gA : c->gB, odd ? c->gA_lo : c->gB_lo,
-                             c->wt[li], c->wt_lo[li], h, w, kCout[li], kCin[li]));
-        N2F_TRY(wgrad_tc_plan(&c->wgrad_plan[sc][li], c->act[li - 1], c->act_lo[li - 1],
-                              odd ? c->gA : c->gB, odd ? c->gA_lo : c->gB_lo, h, w, kCin[li],
-                              kCout[li], wsplit[sc][li]));
+        N2F_TRY(conv_tc_plan(&c->fwd_plan[sc][li], act_op(li - 1), w_op(li), h, w, kCin[li],
+                             kCout[li], f16));
+        const int ab = (li & 1) ? 0 : 1;  // L8 (li 7) reads gA (head output), then alternate
+        N2F_TRY(conv_tc_plan(&c->dgrad_plan[sc][li], g_op(ab), wt_op(li), h, w, kCout[li],
+                             kCin[li], f16));
+        N2F_TRY(wgrad_tc_plan(&c->wgrad_plan[sc][li], act_op(li - 1), g_op(ab), h, w, kCin[li],
+                              kCout[li], wsplit[sc][li], f16));
       }
     }
     for (int sc = 0; sc < 2; ++sc)
       for (int li = 1; li < 8; ++li) c->wsplit[sc][li] = wsplit[sc][li];
     for (int li = 1; li < 8; ++li) {
-      const bool odd = li & 1;  // L1 writes vA; layer li reads vA when li is odd
-      N2F_TRY(conv_tc_plan(&c->val_plan[li], odd ? c->vA : c->vB, odd ? c->vA_lo : c->vB_lo,
-                           c->params + c->poff[2 * li], c->params_lo + c->poff[2 * li], c->H, c->W,
-                           kCin[li], kCout[li]));
+      const int ab = (li & 1) ? 0 : 1;  // L1 writes vA; layer li reads vA when li is odd
+      N2F_TRY(conv_tc_plan(&c->val_plan[li], v_op(ab), w_op(li), c->H, c->W, kCin[li], kCout[li],
+                           f16));
     }
     c->bias_tiles[0] = tiles[0];
     c->bias_tiles[1] = tiles[1];
@@ -514,9 +596,20 @@ int setup(n2f_ctx* c) {
   }
   if (c->tc) {
     a.plo = c->params_lo;
+    a.phi16 = c->w16[0];
+    a.plo16 = c->w16[1];
+    a.wscale = ldexpf(1.f, kExpW);
     for (int li = 1; li < 8; ++li) {
-      a.t[2 * li].want_lo = 1;
-      a.t[2 * li].wtlo = c->wt_lo[li];
+      AdamTensor& T = a.t[2 * li];
+      if (c->f16) {
+        T.want16 = 1;
+        T.wt = nullptr;  // the FP16 path reads only the fp16 pair of wt
+        T.wth16 = c->wt16[0][li];
+        T.wtl16 = c->wt16[1][li];
+      } else {
+        T.want_lo = 1;
+        T.wtlo = c->wt_lo[li];
+      }
     }
     // bias gradients of layers 1..7 are per-tile column sums (dgrad epilogue,
     // head); weights use the tcgen05 wgrad's split count
@@ -563,7 +656,12 @@ int refresh_derived(n2f_ctx* c) {
   for (int li = 1; li < 8; ++li)
     N2F_TRY(transpose_dgrad_weights(c->params + c->poff[2 * li], c->wt[li], kCin[li], kCout[li],
                                     c->stream));
-  if (c->tc) {
+  if (c->f16) {
+    N2F_TRY(split_f16(c->params, c->w16[0], c->w16[1], kExpW, c->ptotal, c->stream));
+    for (int li = 1; li < 8; ++li)
+      N2F_TRY(split_f16(c->wt[li], c->wt16[0][li], c->wt16[1][li], kExpW, c->pnum[2 * li],
+                        c->stream));
+  } else if (c->tc) {
     N2F_TRY(split_lo(c->params, c->params_lo, c->ptotal, c->stream));
     for (int li = 1; li < 8; ++li)
       N2F_TRY(split_lo(c->wt[li], c->wt_lo[li], c->pnum[2 * li], c->stream));
@@ -644,10 +742,12 @@ int n2f_create(int device, int height, int width, const n2f_config* cfg, n2f_ctx
   N2F_TRY(check_cfg(cfg));
   if (height < 4 || width < 4)
     return fail(N2F_ERR_ARG, "image must be at least 4x4, got (%d, %d)", height, width);
-  if (cfg->conv_impl < kImplAuto || cfg->conv_impl > kImplTc)
-    return fail(N2F_ERR_ARG, "conv_impl must be 0 (auto), 1 (SIMT) or 2 (tcgen05)");
+  if (cfg->conv_impl < kImplAuto || cfg->conv_impl > kImplTcF16)
+    return fail(N2F_ERR_ARG,
+                "conv_impl must be 0 (auto), 1 (SIMT), 2 (tcgen05 3xTF32) or 3 (tcgen05 FP16x3)");
   n2f_ctx* c = new n2f_ctx();
   c->tc = cfg->conv_impl != kImplSimt;  // auto = tcgen05
+  c->f16 = cfg->conv_impl == kImplTcF16;
   c->device = device;
   c->H = height;
   c->W = width;

@@ -49,7 +49,10 @@ constexpr int kKsz[kLayers] = {3, 3, 3, 3, 3, 3, 3, 3, 1};
 constexpr int kMaxC = 256;
 
 // ---- conv implementations ---------------------------------------------------
-enum ConvImpl { kImplAuto = 0, kImplSimt = 1, kImplTc = 2 };
+enum ConvImpl { kImplAuto = 0, kImplSimt = 1, kImplTc = 2, kImplTcF16 = 3 };
+// power-of-two operand scales of the FP16 split (activations, weights);
+// gradients use ceil(log2(pixels)) + kExpAct (see conv_tc.cu)
+constexpr int kExpAct = 8, kExpW = 8;
 
 // Epilogue modes of the 3x3 implicit GEMM.
 enum Epi { kEpiBiasRelu = 0, kEpiMask = 1, kEpiBias = 2, kEpiNone = 3 };
@@ -68,26 +71,42 @@ int wgrad_nsplit(int64_t pixels, int cin, int cout);
 // tcgen05 kernels (conv_tc.cu).  A plan holds the TMA descriptors of one
 // (input buffer, weight buffer, shape) combination; it is built once and
 // launched many times (graph-capturable: maps are kernel parameters).
+// A tensor-core operand: the (hi, lo) pair in TF32 mode (hi = the fp32
+// tensor, lo = fp32 residual; exp = 0) or FP16 mode (fp16 pair of x * 2^exp).
+struct TcOperand {
+  const void* hi;
+  const void* lo;
+  int exp;
+};
 struct ConvTcPlan {
   CUtensorMap mx, mxl, mw, mwl;
   int H, W, C, N, grid;
-  int cs;  // thread-block cluster size (weight multicast)
+  bool f16;
+  float unscale;  // 2^-(exp_x + exp_w)
+  int dbg;        // profiling experiments only (N2F_TC_DEBUG)
 };
 bool tc_supported(int cin, int cout);
-int conv_tc_plan(ConvTcPlan* pl, const float* x, const float* xlo, const float* w, const float* wlo,
-                 int H, int W, int C, int N);
-int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const float* mask, float* y, float* ylo,
-                   float* colsum, int epi, cudaStream_t st);
+int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, int W, int C, int N,
+                 bool f16);
+// Outputs: y fp32 (may be null); FP16 plans write the fp16 pair of y * oscale
+// into yhi/ylo (either may be null); TF32 plans write the fp32 residual into
+// ylo (y required).  mask: layer-input tensor for the ReLU mask (fp32 in TF32
+// mode, fp16 hi in FP16 mode).
+int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* y, void* yhi,
+                   void* ylo, float oscale, float* colsum, int epi, cudaStream_t st);
 int conv_tc_tiles(int H, int W);
 struct WgradTcPlan {
   CUtensorMap mx, mxl, mg, mgl;
   int H, W, C, N, mblocks, nsplit;
+  bool f16;
+  float unscale;
 };
 int wgrad_tc_nsplit(int cin, int H, int W);
-int wgrad_tc_plan(WgradTcPlan* pl, const float* x, const float* xlo, const float* g, const float* glo,
-                  int H, int W, int C, int N, int nsplit);
+int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H, int W, int C,
+                  int N, int nsplit, bool f16);
 int wgrad_tc_launch(const WgradTcPlan& pl, float* part, cudaStream_t st);
 int split_lo(const float* x, float* lo, int64_t n, cudaStream_t st);
+int split_f16(const float* x, void* hi, void* lo, int exp2, int64_t n, cudaStream_t st);
 
 // utility kernels (prep.cu / train.cu)
 int reduce_partials(const float* part, float* out, int nsplit, int64_t n, cudaStream_t st);

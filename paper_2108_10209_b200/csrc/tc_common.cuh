@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace n2f {
@@ -243,6 +244,12 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
     hi = __uint_as_float(u & 0xFFFFE000u);
     lo = round_tf32(__fsub_rn(x, hi));
   }
+}
+
+// FP16 split of an (already scaled) fp32 value: hi = fp16(x), lo = fp16(x - hi).
+__device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn(__fsub_rn(x, __half2float(hi)));
 }
 
 }  // namespace tc

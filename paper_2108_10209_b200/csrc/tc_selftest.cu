@@ -76,13 +76,19 @@ __global__ void __launch_bounds__(128) k_tc_selftest(const float* __restrict__ A
 // kind::f16 variant: A[128 x 64] fp16, B[N x 64] fp16, four K=16 MMAs.
 // mode 0: K-major SWIZZLE_128B (row = 64 halves = 128 B, K step = 32 B);
 // mode 1: MN-major SWIZZLE_128B (blocks of 64 MN elements x 64 K rows).
+// mode 2: MN-major SWIZZLE_64B (blocks of 32 MN elements = 64-byte rows).
+__device__ __forceinline__ uint32_t sw64_offset(uint32_t row, uint32_t b) {
+  return row * 64u + ((((b >> 4) ^ ((row >> 1) & 3u)) << 4) | (b & 15u));
+}
 __device__ __forceinline__ uint32_t f16_offset(int mode, int row, int k) {
   if (mode == 0) return sw128_offset(row, 2 * k);
-  return (row / 64) * 8192 + sw128_offset(k, 2 * (row % 64));
+  if (mode == 1) return (row / 64) * 8192 + sw128_offset(k, 2 * (row % 64));
+  return (row / 32) * 4096 + sw64_offset(k, 2 * (row % 32));
 }
 __device__ __forceinline__ uint64_t f16_desc(int mode, uint32_t base, int s) {
   if (mode == 0) return sw128_desc(base + s * 32, 16, 1024);
-  return sw128_desc(base + s * 2048, 8192, 1024);
+  if (mode == 1) return sw128_desc(base + s * 2048, 8192, 1024);
+  return sw128_desc(base + s * 1024, 4096, 512, 4);
 }
 
 template <int AM, int BM>
@@ -145,12 +151,18 @@ extern "C" int n2f_tc_selftest_f16(const uint16_t* A, const uint16_t* B, float* 
     N2F_LAUNCH_CHECK();
     return N2F_OK;
   };
+  if (a_mn < 0 || a_mn > 2 || b_mn < 0 || b_mn > 2) return fail(N2F_ERR_ARG, "selftest_f16 modes");
   int s;
-  switch ((a_mn ? 2 : 0) + (b_mn ? 1 : 0)) {
+  switch (a_mn * 3 + b_mn) {
     case 0: s = launch(k_tc_selftest_f16<0, 0>); break;
     case 1: s = launch(k_tc_selftest_f16<0, 1>); break;
-    case 2: s = launch(k_tc_selftest_f16<1, 0>); break;
-    default: s = launch(k_tc_selftest_f16<1, 1>); break;
+    case 2: s = launch(k_tc_selftest_f16<0, 2>); break;
+    case 3: s = launch(k_tc_selftest_f16<1, 0>); break;
+    case 4: s = launch(k_tc_selftest_f16<1, 1>); break;
+    case 5: s = launch(k_tc_selftest_f16<1, 2>); break;
+    case 6: s = launch(k_tc_selftest_f16<2, 0>); break;
+    case 7: s = launch(k_tc_selftest_f16<2, 1>); break;
+    default: s = launch(k_tc_selftest_f16<2, 2>); break;
   }
   if (s != N2F_OK) return s;
   N2F_CUDA(cudaStreamSynchronize(st));

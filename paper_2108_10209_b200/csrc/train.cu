@@ -50,7 +50,8 @@ __global__ void __launch_bounds__(kThreads)
                  float* __restrict__ gp8, float* __restrict__ part_w, float* __restrict__ part_b,
                  double* __restrict__ part_loss, float* __restrict__ zout, int64_t P, int chunk,
                  int loss, int* __restrict__ step_counter, float* __restrict__ gp8lo,
-                 float* __restrict__ colsum) {
+                 float* __restrict__ colsum, __half* __restrict__ gp8h, __half* __restrict__ gp8l,
+                 float gscale) {
   __shared__ float red_w[kWarps][kMaxC];
   __shared__ float red_c[kWarps][kMaxC];
   float gcs[8];
@@ -92,9 +93,26 @@ __global__ void __launch_bounds__(kThreads)
       g[c] = a[c] > 0.f ? __fmul_rn(w[c], dz) : 0.f;
       gw[c] = fmaf(dz, a[c], gw[c]);
     }
-    float* grow = gp8 + p * kMaxC + 8 * lane;
-    *reinterpret_cast<float4*>(grow) = make_float4(g[0], g[1], g[2], g[3]);
-    *reinterpret_cast<float4*>(grow + 4) = make_float4(g[4], g[5], g[6], g[7]);
+    if (gp8) {
+      float* grow = gp8 + p * kMaxC + 8 * lane;
+      *reinterpret_cast<float4*>(grow) = make_float4(g[0], g[1], g[2], g[3]);
+      *reinterpret_cast<float4*>(grow + 4) = make_float4(g[4], g[5], g[6], g[7]);
+    }
+    if (gp8h) {  // fp16 pair of g * gscale for the FP16 tcgen05 dgrad / wgrad of L8
+      uint4 hv, lv;
+      uint32_t* hw = reinterpret_cast<uint32_t*>(&hv);
+      uint32_t* lw = reinterpret_cast<uint32_t*>(&lv);
+#pragma unroll
+      for (int c = 0; c < 8; c += 2) {
+        __half h2[2], l2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) tc::split_f16(__fmul_rn(g[c + e], gscale), h2[e], l2[e]);
+        hw[c / 2] = (uint32_t)__half_as_ushort(h2[0]) | ((uint32_t)__half_as_ushort(h2[1]) << 16);
+        lw[c / 2] = (uint32_t)__half_as_ushort(l2[0]) | ((uint32_t)__half_as_ushort(l2[1]) << 16);
+      }
+      *reinterpret_cast<uint4*>(gp8h + p * kMaxC + 8 * lane) = hv;
+      *reinterpret_cast<uint4*>(gp8l + p * kMaxC + 8 * lane) = lv;
+    }
     if (gp8lo) {  // tf32 residuals for the tcgen05 dgrad of L8
       float l[8], hh;
 #pragma unroll
@@ -228,13 +246,23 @@ __global__ void __launch_bounds__(kThreads)
   float hi, lo = 0.f;
   if (T.want_lo || T.wtlo) tc::split_tf32(p, hi, lo);
   if (T.want_lo) args.plo[i] = lo;  // tf32 residual of the forward operand
-  if (T.wt) {  // wt[c][8-tap][o] = w[o][tap][c]
+  __half h16, l16;
+  if (T.want16) {  // FP16 pair of p * 2^kExpW for the FP16 tensor-core path
+    tc::split_f16(__fmul_rn(p, args.wscale), h16, l16);
+    args.phi16[i] = h16;
+    args.plo16[i] = l16;
+  }
+  if (T.wt || T.wth16) {  // wt[c][8-tap][o] = w[o][tap][c]
     const int c = (int)(j % T.cin);
     const int tap = (int)((j / T.cin) % 9);
     const int o = (int)(j / ((int64_t)T.cin * 9));
     const int64_t q = ((int64_t)c * 9 + (8 - tap)) * T.cout + o;
-    T.wt[q] = p;
+    if (T.wt) T.wt[q] = p;
     if (T.wtlo) T.wtlo[q] = lo;
+    if (T.wth16) {
+      T.wth16[q] = h16;
+      T.wtl16[q] = l16;
+    }
   }
 }
 
@@ -423,10 +451,12 @@ __global__ void k_reset_state(DevState* st) {
 int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
                       float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
                       int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st,
-                      float* gp8lo, float* colsum) {
+                      float* gp8lo, float* colsum, void* gp8h, void* gp8l, float gscale) {
   const int chunk = (int)((P + nblk - 1) / nblk);
   k_head_train<<<nblk, kThreads, 0, st>>>(a8, w9, b9, tgt, gp8, part_w, part_b, part_loss, zout, P,
-                                          chunk, loss, step_counter, gp8lo, colsum);
+                                          chunk, loss, step_counter, gp8lo, colsum,
+                                          reinterpret_cast<__half*>(gp8h),
+                                          reinterpret_cast<__half*>(gp8l), gscale);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

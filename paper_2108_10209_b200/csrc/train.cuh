@@ -1,5 +1,7 @@
 // Device-side state and launchers of the training-loop kernels (train.cu).
 #pragma once
+#include <cuda_fp16.h>
+
 #include "n2f_internal.cuh"
 
 namespace n2f {
@@ -28,6 +30,9 @@ struct AdamTensor {
   float* wt;          // optional dgrad-transposed copy (3x3 weights), else null
   float* wtlo;        // optional tf32 residual of wt
   int want_lo;        // write the tf32 residual of p into AdamArgs::plo
+  int want16;         // write the fp16 pair of p * wscale into AdamArgs::phi16/plo16
+  __half* wth16;      // optional fp16 pair of the dgrad-transposed copy (scaled)
+  __half* wtl16;
   int cin, cout;
 };
 
@@ -39,6 +44,9 @@ struct AdamArgs {
   int64_t total;
   float* p;
   float* plo;  // tf32 residual arena (same layout as p), for tensors with want_lo
+  __half* phi16;  // fp16 pair arenas (same layout as p), for tensors with want16
+  __half* plo16;
+  float wscale;   // 2^kExpW
   float* m;
   float* v;
   const float* bc1;  // fl32(1 - beta1^t), t = 1..table_len
@@ -63,7 +71,8 @@ int launch_col_reduce(const ColReduceArgs& a, cudaStream_t st);
 int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
                       float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
                       int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st,
-                      float* gp8lo = nullptr, float* colsum = nullptr);
+                      float* gp8lo = nullptr, float* colsum = nullptr, void* gp8h = nullptr,
+                      void* gp8l = nullptr, float gscale = 1.f);
 int launch_head_val(const float* a8, const float* w9, const float* b9, const float* norm,
                     float* ring, int64_t P, int nblk, const DevState* dst, int window,
                     double* part_se, cudaStream_t st);

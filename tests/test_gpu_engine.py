@@ -25,7 +25,7 @@ def _engine(h, w, impl=0, **cfg):
     return Engine(h, w, TrainConfig(**cfg), use_graph=False, conv_impl=impl)
 
 
-IMPLS = [pytest.param(1, id="simt"), pytest.param(2, id="tcgen05")]
+IMPLS = [pytest.param(1, id="simt"), pytest.param(2, id="tf32x3"), pytest.param(3, id="f16x3")]
 
 
 def _arena(eng, which):

@@ -89,11 +89,11 @@ def _tc_ok(cin, cout, k):
     return k == 3 and cin % 32 == 0 and cout in (32, 64, 128, 256)
 
 
-@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("impl", [1, 2, 3])
 @pytest.mark.parametrize("cin,cout,k", CONV_SHAPES)
 @pytest.mark.parametrize("hw", [(13, 17), (40, 24), (64, 96)])
 def test_conv_forward(lib, oracle, cin, cout, k, hw, impl):
-    if impl == 2 and not _tc_ok(cin, cout, k):
+    if impl >= 2 and not _tc_ok(cin, cout, k):
         pytest.skip("tcgen05 path covers the 3x3 layers with cin >= 32")
     rng = np.random.default_rng(cin * 1000 + cout + hw[0])
     x = rng.standard_normal((cin, *hw)).astype(np.float32)
@@ -110,11 +110,11 @@ def test_conv_forward(lib, oracle, cin, cout, k, hw, impl):
         np.testing.assert_allclose(got, ref, rtol=0, atol=1e-5 * np.abs(ref).max())
 
 
-@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("impl", [1, 2, 3])
 @pytest.mark.parametrize("cin,cout,k", CONV_SHAPES)
 @pytest.mark.parametrize("hw", [(13, 17), (40, 24), (64, 96)])
 def test_conv_backward(lib, oracle, cin, cout, k, hw, impl):
-    if impl == 2 and not _tc_ok(cout, cin, k):
+    if impl >= 2 and not _tc_ok(cout, cin, k):
         pytest.skip("tcgen05 dgrad covers 3x3 layers with cin in {32..256}")
     rng = np.random.default_rng(cin * 77 + cout + hw[1])
     x = np.maximum(rng.standard_normal((cin, *hw)), 0).astype(np.float32)  # post-ReLU input
@@ -273,7 +273,7 @@ def test_conv_accuracy_vs_f64(lib, oracle, cin, cout):
     scale = np.abs(exact).max()
     errs = {"oracle_fp32": np.abs(blas - exact).max() / scale}
     d_x, d_w, d_b = dev(chw_to_hwc(x)), dev(oihw_to_engine(wt)), dev(b)
-    for impl in (1, 2):
+    for impl in (1, 2, 3):
         y = empty(h * w * cout)
         _call(lib, "n2f_conv_fwd", d_x.data_ptr(), d_w.data_ptr(), d_b.data_ptr(), y.data_ptr(),
               h, w, cin, cout, 3, 0, impl, None)
@@ -282,4 +282,4 @@ def test_conv_accuracy_vs_f64(lib, oracle, cin, cout):
         # signed bias: mean of (got - exact) * sign(exact), relative to mean |exact|
         errs[f"impl{impl}_bias"] = float(np.mean((got - exact) * np.sign(exact)) / np.mean(np.abs(exact)))
     print(f"cin={cin} cout={cout} max-err/scale: {errs}")
-    assert errs["impl1"] < 1e-5 and errs["impl2"] < 3e-5
+    assert errs["impl1"] < 1e-5 and errs["impl2"] < 3e-5 and errs["impl3"] < 3e-5

@@ -40,10 +40,11 @@ def test_selftest_gemm(a_mn, b_mn, n):
     assert min(et, er) < 1e-4 * np.abs(ref_t).max()
 
 
-@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1), (2, 0), (0, 2), (2, 2)])
 @pytest.mark.parametrize("n", [64, 256])
 def test_selftest_gemm_f16(a_mn, b_mn, n):
-    """kind::f16 with fp16 operands: K-major and MN-major SWIZZLE_128B."""
+    """kind::f16 with fp16 operands: K-major SW128 (0), MN-major SW128 (1),
+    MN-major SW64 (2, 32-element blocks)."""
     from paper_2108_10209_b200 import _lib
 
     rng = np.random.default_rng(7 + n + 3 * a_mn + b_mn)
