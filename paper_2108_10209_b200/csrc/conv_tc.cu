@@ -33,8 +33,11 @@ namespace {
 
 using namespace tc;
 
+// Align the dynamic smem base to 1 KB (SWIZZLE_128B atoms) by pointer
+// arithmetic on the __shared__ array itself, so that the compiler keeps the
+// shared address space (st.shared / ld.shared, not generic ST.E / LD.E).
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
 // Precision traits.  A pipeline stage carries K = 32 elements per operand row
@@ -235,73 +238,87 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const uint32_t taddr = tslot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---- TMA producer (stage index `it` runs across tiles)
-      int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int x0 = (tile % tiles_x) * kTW, y0 = (tile / tiles_x) * kTH;
-        for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int s = it % S, round = it / S;
-          if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-          const int tap = kb / cpt, c0 = (kb - tap * cpt) * 32;
-          const int ky = tap / 3, kx = tap - 3 * ky;
-          uint8_t* st = base + s * Cfg::kStageBytes;
+    // ---- TMA producer (stage index `it` runs across tiles).  The whole warp
+    // walks the schedule; one elected lane issues.
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int x0 = (tile % tiles_x) * kTW, y0 = (tile / tiles_x) * kTH;
+      for (int kb = 0; kb < KB; ++kb, ++it) {
+        const int s = it % S, round = it / S;
+        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+        const int tap = kb / cpt, c0 = (kb - tap * cpt) * 32;
+        const int ky = tap / 3, kx = tap - 3 * ky;
+        uint8_t* st = base + s * Cfg::kStageBytes;
+        if (elect_one_sync()) {
           if (dbg & 4) {  // profiling experiment: no operand traffic
             mbar_arrive(&full[s]);
-            continue;
+          } else {
+            mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+            tma_load_3d(st, &mx, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
+            tma_load_3d(st + Cfg::kStageA, &mxl, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
+            tma_load_2d(st + 2 * Cfg::kStageA, &mw, &full[s], tap * C + c0, 0);
+            tma_load_2d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, &full[s], tap * C + c0, 0);
           }
-          mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
-          tma_load_3d(st, &mx, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
-          tma_load_3d(st + Cfg::kStageA, &mxl, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
-          tma_load_2d(st + 2 * Cfg::kStageA, &mw, &full[s], tap * C + c0, 0);
-          tma_load_2d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, &full[s], tap * C + c0, 0);
         }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- MMA issuer: one group = G stages into a fresh TMEM buffer
-      constexpr uint32_t idesc = P::idesc(128, BN, false, false);
-      int it = 0, gg = 0;  // stage and group counters across tiles
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int g = 0; g < NG; ++g, ++gg) {
-          const int b = gg & 1;
-          if (gg >= 2 && !(dbg & 16)) mbar_wait(&tempty[b], ((gg >> 1) - 1) & 1);
-          const int ng = (g + 1) * G <= KB ? G : KB - g * G;
-          uint32_t a[G];
-          for (int j = 0; j < ng; ++j) {
-            const int s = (it + j) % S;
-            mbar_wait(&full[s], ((it + j) / S) & 1);
-            a[j] = smem_u32(base + s * Cfg::kStageBytes);
-          }
-          tc_fence_after();
+    // ---- MMA issuer: one group = G stages into a fresh TMEM buffer.  The
+    // whole warp walks the schedule and waits; one elected lane issues.
+    constexpr uint32_t idesc = P::idesc(128, BN, false, false);
+    // descriptor offsets (16-byte units) inside a stage: A-lo, B-hi, B-lo
+    constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
+                       kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
+    const uint64_t desc0 = P::kdesc(smem_u32(base));
+    int it = 0, gg = 0;  // stage and group counters across tiles
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int g = 0; g < NG; ++g, ++gg) {
+        const int b = gg & 1;
+        if (gg >= 2 && !(dbg & 16)) mbar_wait(&tempty[b], ((gg >> 1) - 1) & 1);
+        const int ng = (g + 1) * G <= KB ? G : KB - g * G;
+        for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
+        tc_fence_after();
+        if (elect_one_sync()) {
           const uint32_t d = taddr + b * BN;
-          // the small cross terms of the whole group first, then hi*hi
-          for (int j = 0; j < ng && !(dbg & 2); ++j) {
-            const uint32_t ah = a[j], al = ah + Cfg::kStageA, bh = ah + 2 * Cfg::kStageA,
-                           bl = bh + Cfg::kStageB;
+          uint64_t ah[G];  // A-hi descriptor of the group's stages
 #pragma unroll
-            for (int k = 0; k < P::kKSteps; ++k) {
-              P::mma(d, P::kdesc(ah + 32 * k), P::kdesc(bl + 32 * k), idesc, (j | k) != 0);
-              P::mma(d, P::kdesc(al + 32 * k), P::kdesc(bh + 32 * k), idesc, 1);
+          for (int j = 0; j < G; ++j) ah[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
+          if (!(dbg & 2)) {
+            // the small cross terms of the whole group first, then hi*hi;
+            // one K step = 32 bytes = 2 descriptor units
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+              if (j < ng) {
+#pragma unroll
+                for (int k = 0; k < P::kKSteps; ++k) {
+                  const uint64_t a = ah[j] + 2 * k;
+                  P::mma(d, a, a + kBl, idesc, (j | k) != 0);
+                  P::mma(d, a + kAl, a + kBh, idesc, 1);
+                }
+              }
             }
-          }
-          for (int j = 0; j < ng && !(dbg & 2); ++j) {
-            const uint32_t ah = a[j], bh = ah + 2 * Cfg::kStageA;
 #pragma unroll
-            for (int k = 0; k < P::kKSteps; ++k)
-              P::mma(d, P::kdesc(ah + 32 * k), P::kdesc(bh + 32 * k), idesc, 1);
+            for (int j = 0; j < G; ++j) {
+              if (j < ng) {
+#pragma unroll
+                for (int k = 0; k < P::kKSteps; ++k) {
+                  const uint64_t a = ah[j] + 2 * k;
+                  P::mma(d, a, a + kBh, idesc, 1);
+                }
+              }
+            }
           }
           if (dbg & 8) {  // profiling experiment (with 2|4): plain arrives, no commit latency
             for (int j = 0; j < ng; ++j) mbar_arrive(&empty[(it + j) % S]);
-            it += ng;
             mbar_arrive(&tfull[b]);
-            continue;
+          } else {
+            for (int j = 0; j < ng; ++j) mma_commit(&empty[(it + j) % S]);
+            mma_commit(&tfull[b]);
           }
-          for (int j = 0; j < ng; ++j) mma_commit(&empty[(it + j) % S]);
-          it += ng;
-          mma_commit(&tfull[b]);
         }
+        __syncwarp();
+        it += ng;
       }
     }
   } else {
@@ -465,13 +482,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const uint32_t taddr = tslot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % S, round = kb / S;
-        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-        const int seg = s0 + kb;
-        const int y0 = seg / segs_x, x0 = (seg - y0 * segs_x) * kSegW;
-        uint8_t* st = base + s * Cfg::kStageBytes;
+    // ---- TMA producer (whole warp walks the schedule, one elected lane issues)
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % S, round = kb / S;
+      if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+      const int seg = s0 + kb;
+      const int y0 = seg / segs_x, x0 = (seg - y0 * segs_x) * kSegW;
+      uint8_t* st = base + s * Cfg::kStageBytes;
+      if (elect_one_sync()) {
         mbar_arrive_expect_tx(&full[s], stage_bytes);
         for (int j = 0; j < nblk_a; ++j) {
           const int mm = m0 + 32 * j, tap = mm / C, c = mm - tap * C;
@@ -485,42 +503,53 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                       y0);
         }
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = P::idesc(128, BN, true, true);
-      int it = 0;
-      for (int g = 0; g < NG; ++g) {
-        const int b = g & 1;
-        if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-        const int ng = (g + 1) * G <= KB ? G : KB - g * G;
-        uint32_t a[G];
-        for (int j = 0; j < ng; ++j) {
-          const int s = (it + j) % S;
-          mbar_wait(&full[s], ((it + j) / S) & 1);
-          a[j] = smem_u32(base + s * Cfg::kStageBytes);
-        }
-        tc_fence_after();
+    // ---- MMA issuer (whole warp waits, one elected lane issues)
+    constexpr uint32_t idesc = P::idesc(128, BN, true, true);
+    constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
+                       kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
+    const uint64_t desc0 = P::mndesc(smem_u32(base));
+    int it = 0;
+    for (int g = 0; g < NG; ++g) {
+      const int b = g & 1;
+      if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+      const int ng = (g + 1) * G <= KB ? G : KB - g * G;
+      for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
+      tc_fence_after();
+      if (elect_one_sync()) {
         const uint32_t d = taddr + b * BN;
-        for (int j = 0; j < ng; ++j) {  // cross terms of the group first, then hi*hi
-          const uint32_t ah = a[j], al = ah + Cfg::kStageA, bh = ah + 2 * Cfg::kStageA,
-                         bl = bh + Cfg::kStageB;
+        uint64_t ah[G];
 #pragma unroll
-          for (int k = 0; k < P::kKSteps; ++k) {
-            P::mma(d, P::mndesc(ah + 1024 * k), P::mndesc(bl + 1024 * k), idesc, (j | k) != 0);
-            P::mma(d, P::mndesc(al + 1024 * k), P::mndesc(bh + 1024 * k), idesc, 1);
+        for (int j = 0; j < G; ++j) ah[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
+        // cross terms of the group first, then hi*hi; one K step = 1 KB = 64 units
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+          if (j < ng) {
+#pragma unroll
+            for (int k = 0; k < P::kKSteps; ++k) {
+              const uint64_t a = ah[j] + 64 * k;
+              P::mma(d, a, a + kBl, idesc, (j | k) != 0);
+              P::mma(d, a + kAl, a + kBh, idesc, 1);
+            }
           }
         }
-        for (int j = 0; j < ng; ++j) {
-          const uint32_t ah = a[j], bh = ah + 2 * Cfg::kStageA;
 #pragma unroll
-          for (int k = 0; k < P::kKSteps; ++k)
-            P::mma(d, P::mndesc(ah + 1024 * k), P::mndesc(bh + 1024 * k), idesc, 1);
+        for (int j = 0; j < G; ++j) {
+          if (j < ng) {
+#pragma unroll
+            for (int k = 0; k < P::kKSteps; ++k) {
+              const uint64_t a = ah[j] + 64 * k;
+              P::mma(d, a, a + kBh, idesc, 1);
+            }
+          }
         }
         for (int j = 0; j < ng; ++j) mma_commit(&empty[(it + j) % S]);
-        it += ng;
         mma_commit(&tfull[b]);
       }
+      __syncwarp();
+      it += ng;
     }
   } else {
     const int q = warp & 3;
