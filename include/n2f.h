@@ -164,6 +164,9 @@ int n2f_tc_selftest(const float* a, const float* b, float* d, int n, int a_mn, i
 /* kind::f16 self-test: fp16 A[128 x 64], B[n x 64] (K-major 0 / MN-major 1). */
 int n2f_tc_selftest_f16(const uint16_t* a, const uint16_t* b, float* d, int n, int a_mn, int b_mn,
                         void* stream);
+/* 2-SM (cta_group::2, cluster of 2) kind::f16 self-test: D[256 x n] = A[256 x 64] . B[n x 64]^T,
+ * K-major SWIZZLE_128B, CTA r staging A rows [128r, 128r+128) and B rows [rn/2, (r+1)n/2). */
+int n2f_tc_selftest_2sm(const uint16_t* a, const uint16_t* b, float* d, int n, void* stream);
 int n2f_ctx_step(n2f_ctx* ctx, int pair, float* logits_host);
 int n2f_ctx_epoch(n2f_ctx* ctx, int* stopped);
 /* Profile one epoch: per (class, layer) device ms / algorithmic FLOPs / launches

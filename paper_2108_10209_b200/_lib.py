@@ -89,6 +89,7 @@ SIGNATURES = {
     "n2f_ctx_set_arena": [_P, _I, _P, _I],
     "n2f_tc_selftest": [_P, _P, _P, _I, _I, _I, _P],
     "n2f_tc_selftest_f16": [_P, _P, _P, _I, _I, _I, _P],
+    "n2f_tc_selftest_2sm": [_P, _P, _P, _I, _P],
     "n2f_ctx_step": [_P, _I, _P],
     "n2f_ctx_epoch": [_P, _P],
     "n2f_ctx_profile_epoch": [_P, _P, _P, _P],

@@ -28,6 +28,11 @@
 #include "n2f_internal.cuh"
 #include "tc_common.cuh"
 
+// Build with -DN2F_TC_TRACE=1 for per-warp cycle accounting (N2F_TC_DEBUG=64).
+#ifndef N2F_TC_TRACE
+#define N2F_TC_TRACE 0
+#endif
+
 namespace n2f {
 namespace {
 
@@ -58,11 +63,19 @@ struct Prec {
   __device__ static uint64_t mndesc(uint32_t addr) {
     return sw128_desc(addr, 32 * kRow, 512, kLayMN);
   }
+  template <int CS = 1>
   __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    if (F16)
-      mma_f16(d, a, b, idesc, acc);
-    else
-      mma_tf32(d, a, b, idesc, acc);
+    if (CS == 2) {
+      if (F16)
+        mma_f16_2sm(d, a, b, idesc, acc);
+      else
+        mma_tf32_2sm(d, a, b, idesc, acc);
+    } else {
+      if (F16)
+        mma_f16(d, a, b, idesc, acc);
+      else
+        mma_tf32(d, a, b, idesc, acc);
+    }
   }
   static constexpr uint32_t idesc(int M, int N, bool amn, bool bmn) {
     return F16 ? idesc_f16(M, N, amn, bmn) : idesc_tf32(M, N, amn, bmn);
@@ -123,23 +136,26 @@ __device__ __forceinline__ void drain_add(uint32_t taddr, float (&acc)[HALF]) {
 constexpr int kTW = 32, kTH = 4;
 constexpr int kThreadsTc = 320;
 
-template <int BN, bool F16>
+template <int BN, bool F16, int CS = 1>
 struct FwdCfg {
   using P = Prec<F16>;
   static constexpr int kStageA = 128 * P::kRow;
-  static constexpr int kStageB = BN * P::kRow;
+  static constexpr int kStageB = (BN / CS) * P::kRow;  // this CTA's share of the weight rows
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
   static constexpr int kMaxStages = (200 * 1024) / kStageBytes;
-  // wide layers: as many stages as fit one CTA per SM; narrow layers: 2 CTAs
-  // per SM (their smem and registers allow it) with 2 groups' worth of stages
-  static constexpr int kStages =
-      BN >= 128 ? (kMaxStages > 6 ? 6 : kMaxStages) : 2 * P::kGroup;
+  // narrow layers run 2 CTAs per SM (their smem, registers and TMEM allow it)
+  // with 2 groups' worth of stages; the others take as many stages as fit
+  static constexpr bool kTwoPerSm = CS == 1 && BN <= 64;
+  static constexpr int kStages = kTwoPerSm ? 2 * P::kGroup : (kMaxStages > 8 ? 8 : kMaxStages);
   // epilogue transpose scratch: 8 warps x 32 pixels x kEpiCols fp32
   static constexpr int kEpiCols = BN >= 128 ? 16 : 8;
   static constexpr int kEpiBytes = 8 * 32 * kEpiCols * 4;
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
-  static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // two group buffers
-  static constexpr int kHalf = BN / 2;                         // columns per epilogue warp
+  // TMEM group buffers: as many as the CTA's column budget holds (<= 4)
+  static constexpr int kTmemBudget = kTwoPerSm ? 256 : 512;
+  static constexpr int kBufs = kTmemBudget / BN > 4 ? 4 : kTmemBudget / BN;
+  static constexpr int kTmemCols = kBufs * BN < 32 ? 32 : kBufs * BN;
+  static constexpr int kHalf = BN / 2;  // columns per epilogue warp
 };
 
 // Output of a conv epilogue.  y: fp32 values (may be null).  F16: yhi/ylo fp16
@@ -194,25 +210,29 @@ __device__ __forceinline__ float4 load_mask4(const void* mask, int64_t idx) {
   return __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(mask) + idx));
 }
 
-template <int BN, bool F16>
+template <int BN, bool F16, int CS>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
                  const float* __restrict__ bias, const void* __restrict__ mask, ConvOut out,
                  float* __restrict__ colsum, float unscale, int H, int W, int C, int epi, int dbg) {
-  using Cfg = FwdCfg<BN, F16>;
+  using Cfg = FwdCfg<BN, F16, CS>;
   using P = Prec<F16>;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
   constexpr int G = P::kGroup;
+  constexpr int NB = Cfg::kBufs;
+  constexpr int UH = kTH * CS;  // rows of a cluster tile (CTA r owns rows [kTH r, kTH r + kTH))
   extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
+  __shared__ uint64_t full[S], empty[S], tfull[NB], tempty[NB];
   __shared__ uint32_t tslot;
   __shared__ __align__(16) float csum[4][BN];
   uint8_t* base = align1024(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
   const int tiles_x = (W + kTW - 1) / kTW;
-  const int ntiles = tiles_x * ((H + kTH - 1) / kTH);
+  const int nunits = tiles_x * ((H + UH - 1) / UH);
   const int cpt = C / 32, KB = 9 * cpt;  // stages per tile
   const int NG = (KB + G - 1) / G;       // groups per tile (the last may be short)
 
@@ -221,9 +241,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);  // one arrive per accumulate warp
+      mbar_init(&tempty[b], 8 * CS);  // one arrive per accumulate warp of the cluster
     }
     fence_barrier_init();
     tma_prefetch(&mx);
@@ -231,18 +251,29 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     tma_prefetch(&mw);
     tma_prefetch(&mwl);
   }
-  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(&tslot);
+  if (warp == 1) {
+    if (CS == 2)
+      tmem_alloc_2sm<Cfg::kTmemCols>(&tslot);
+    else
+      tmem_alloc<Cfg::kTmemCols>(&tslot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CS == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t taddr = tslot;
 
   if (warp == 0) {
     // ---- TMA producer (stage index `it` runs across tiles).  The whole warp
-    // walks the schedule; one elected lane issues.
+    // walks the schedule; one elected lane issues.  In a CTA pair both CTAs
+    // load their own pixel rows and their half of the weight rows, and the
+    // bytes complete on the leader's full barrier.
+    const uint32_t full0 = CS == 2 ? mapa_shared(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
     int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int x0 = (tile % tiles_x) * kTW, y0 = (tile / tiles_x) * kTH;
+    for (int ut = cid; ut < nunits; ut += ncl) {
+      const int x0 = (ut % tiles_x) * kTW, y0 = (ut / tiles_x) * UH + kTH * (int)rank;
       for (int kb = 0; kb < KB; ++kb, ++it) {
         const int s = it % S, round = it / S;
         if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
@@ -251,97 +282,147 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         uint8_t* st = base + s * Cfg::kStageBytes;
         if (elect_one_sync()) {
           if (dbg & 4) {  // profiling experiment: no operand traffic
-            mbar_arrive(&full[s]);
-          } else {
+            if (rank == 0) mbar_arrive(&full[s]);
+          } else if (CS == 1) {
             mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
             tma_load_3d(st, &mx, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
             tma_load_3d(st + Cfg::kStageA, &mxl, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
             tma_load_2d(st + 2 * Cfg::kStageA, &mw, &full[s], tap * C + c0, 0);
             tma_load_2d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, &full[s], tap * C + c0, 0);
+          } else {
+            const uint32_t fb = full0 + 8u * s;
+            const int n0 = (int)rank * (BN / CS);
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], CS * Cfg::kStageBytes);
+            tma_load_3d_2sm(st, &mx, fb, c0, x0 + kx - 1, y0 + ky - 1);
+            tma_load_3d_2sm(st + Cfg::kStageA, &mxl, fb, c0, x0 + kx - 1, y0 + ky - 1);
+            tma_load_2d_2sm(st + 2 * Cfg::kStageA, &mw, fb, tap * C + c0, n0);
+            tma_load_2d_2sm(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, fb, tap * C + c0, n0);
           }
         }
         __syncwarp();
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: one group = G stages into a fresh TMEM buffer.  The
-    // whole warp walks the schedule and waits; one elected lane issues.
-    constexpr uint32_t idesc = P::idesc(128, BN, false, false);
-    // descriptor offsets (16-byte units) inside a stage: A-lo, B-hi, B-lo
-    constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
-                       kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
-    const uint64_t desc0 = P::kdesc(smem_u32(base));
-    int it = 0, gg = 0;  // stage and group counters across tiles
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      for (int g = 0; g < NG; ++g, ++gg) {
-        const int b = gg & 1;
-        if (gg >= 2 && !(dbg & 16)) mbar_wait(&tempty[b], ((gg >> 1) - 1) & 1);
-        const int ng = (g + 1) * G <= KB ? G : KB - g * G;
-        for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
-        tc_fence_after();
-        if (elect_one_sync()) {
-          const uint32_t d = taddr + b * BN;
-          uint64_t ah[G];  // A-hi descriptor of the group's stages
+    // ---- MMA issuer (the leader CTA of a pair issues for both): one group =
+    // G stages into a fresh TMEM buffer.  The whole warp walks the schedule
+    // and waits; one elected lane issues.
+    if (rank == 0) {
+      constexpr uint32_t idesc = P::idesc(128 * CS, BN, false, false);
+      // descriptor offsets (16-byte units) inside a stage: A-lo, B-hi, B-lo
+      constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
+                         kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
+      const uint64_t desc0 = P::kdesc(smem_u32(base));
+      int it = 0, gg = 0;  // stage and group counters across tiles
+      long long tw_e = 0, tw_f = 0, t_is = 0, t_0 = clock64();  // dbg 64: cycle accounting
+      for (int ut = cid; ut < nunits; ut += ncl) {
+        for (int g = 0; g < NG; ++g, ++gg) {
+          const int b = gg % NB;
+          const long long c0 = clock64();
+          if (gg >= NB && !(dbg & 16)) mbar_wait(&tempty[b], ((gg / NB) - 1) & 1);
+          const long long c1 = clock64();
+          const int ng = (g + 1) * G <= KB ? G : KB - g * G;
+          for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
+          const long long c2 = clock64();
+          tw_e += c1 - c0;
+          tw_f += c2 - c1;
+          tc_fence_after();
+          if (elect_one_sync()) {
+            const uint32_t d = taddr + b * BN;
+            uint64_t ah[G];  // A-hi descriptor of the group's stages
 #pragma unroll
-          for (int j = 0; j < G; ++j) ah[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
-          if (!(dbg & 2)) {
-            // the small cross terms of the whole group first, then hi*hi;
-            // one K step = 32 bytes = 2 descriptor units
+            for (int j = 0; j < G; ++j)
+              ah[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
+            if (!(dbg & 2)) {
+              // the small cross terms of the whole group first, then hi*hi;
+              // one K step = 32 bytes = 2 descriptor units
 #pragma unroll
-            for (int j = 0; j < G; ++j) {
-              if (j < ng) {
+              for (int j = 0; j < G; ++j) {
+                if (j < ng) {
 #pragma unroll
-                for (int k = 0; k < P::kKSteps; ++k) {
-                  const uint64_t a = ah[j] + 2 * k;
-                  P::mma(d, a, a + kBl, idesc, (j | k) != 0);
-                  P::mma(d, a + kAl, a + kBh, idesc, 1);
+                  for (int k = 0; k < P::kKSteps; ++k) {
+                    const uint64_t a = ah[j] + 2 * k;
+                    P::template mma<CS>(d, a, a + kBl, idesc, (j | k) != 0);
+                    P::template mma<CS>(d, a + kAl, a + kBh, idesc, 1);
+                  }
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < G; ++j) {
+                if (j < ng) {
+#pragma unroll
+                  for (int k = 0; k < P::kKSteps; ++k) {
+                    const uint64_t a = ah[j] + 2 * k;
+                    P::template mma<CS>(d, a, a + kBh, idesc, 1);
+                  }
                 }
               }
             }
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
-              if (j < ng) {
-#pragma unroll
-                for (int k = 0; k < P::kKSteps; ++k) {
-                  const uint64_t a = ah[j] + 2 * k;
-                  P::mma(d, a, a + kBh, idesc, 1);
-                }
-              }
+            for (int j = 0; j < ng; ++j) {
+              if (CS == 2)
+                mma_commit_2sm(&empty[(it + j) % S]);
+              else
+                mma_commit(&empty[(it + j) % S]);
             }
+            if (CS == 2)
+              mma_commit_2sm(&tfull[b]);
+            else
+              mma_commit(&tfull[b]);
           }
-          if (dbg & 8) {  // profiling experiment (with 2|4): plain arrives, no commit latency
-            for (int j = 0; j < ng; ++j) mbar_arrive(&empty[(it + j) % S]);
-            mbar_arrive(&tfull[b]);
-          } else {
-            for (int j = 0; j < ng; ++j) mma_commit(&empty[(it + j) % S]);
-            mma_commit(&tfull[b]);
-          }
+          __syncwarp();
+          t_is += clock64() - c2;
+          it += ng;
         }
-        __syncwarp();
-        it += ng;
       }
+      if ((dbg & 64) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 100))
+        printf("[mma cta %d] C %d BN %d CS %d HxW %dx%d groups %d total %lld wait_tempty %lld "
+               "wait_full %lld issue %lld\n",
+               blockIdx.x, C, BN, CS, H, W, gg, clock64() - t_0, tw_e, tw_f, t_is);
     }
   } else {
     // ---- group accumulation in registers (round-to-nearest fp32 adds)
     const int q = warp & 3;            // TMEM lane quarter
     const int half = (warp - 2) >> 2;  // column half
     const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * HALF;
+    // the leader's tempty barriers (shared::cluster addresses)
+    const uint32_t tempty0 = CS == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     int gg = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int x0 = (tile % tiles_x) * kTW, y0 = (tile / tiles_x) * kTH;
+#if N2F_TC_TRACE
+    long long tw = 0, td = 0, te = 0, t_0 = clock64();  // cycle accounting
+#endif
+    for (int ut = cid; ut < nunits; ut += ncl) {
+      const int x0 = (ut % tiles_x) * kTW, y0 = (ut / tiles_x) * UH + kTH * (int)rank;
+      const int tile = ut * CS + (int)rank;  // this CTA's 128-pixel tile (colsum row)
       float acc[HALF];
 #pragma unroll
       for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
       for (int g = 0; g < NG; ++g, ++gg) {
-        const int b = gg & 1;
+        const int b = gg % NB;
         if (dbg & 16) continue;  // profiling experiment: no accumulator handoff
-        mbar_wait(&tfull[b], (gg >> 1) & 1);
+#if N2F_TC_TRACE
+        const long long c0 = clock64();
+#endif
+        mbar_wait(&tfull[b], (gg / NB) & 1);
+#if N2F_TC_TRACE
+        const long long c1 = clock64();
+        tw += c1 - c0;
+#endif
         tc_fence_after();
         if (!(dbg & 1)) drain_add<HALF>(lane_base + b * BN, acc);  // dbg 1: experiment, no drain
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[b]);
+        if (lane == 0) {
+          if (CS == 2)
+            mbar_arrive_cluster(tempty0 + 8u * b);
+          else
+            mbar_arrive(&tempty[b]);
+        }
+#if N2F_TC_TRACE
+        td += clock64() - c1;
+#endif
       }
+#if N2F_TC_TRACE
+      const long long ce = clock64();
+#endif
 
       // ---- epilogue.  The drain leaves lane = pixel, registers = channels;
       // global rows are pixel-major, so EC-column slices are transposed
@@ -411,11 +492,28 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           colsum[(int64_t)tile * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
         asm volatile("bar.sync 1, 256;" ::: "memory");  // csum reusable for the next tile
       }
+#if N2F_TC_TRACE
+      te += clock64() - ce;
+#endif
     }
+#if N2F_TC_TRACE
+    if ((dbg & 64) && lane == 0 && (warp == 2 || warp == 9) && (blockIdx.x == 0 || blockIdx.x == 100))
+      printf("[acc cta %d warp %d] C %d BN %d CS %d HxW %dx%d groups %d total %lld wait_tfull %lld "
+             "drain %lld epilogue %lld\n",
+             blockIdx.x, warp, C, BN, CS, H, W, gg, clock64() - t_0, tw, td, te);
+#endif
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(taddr);
+  if (CS == 2)
+    cluster_sync();  // the peer's TMEM / smem / barriers stay live until the pair is done
+  else
+    __syncthreads();
+  if (warp == 1) {
+    if (CS == 2)
+      tmem_dealloc_2sm<Cfg::kTmemCols>(taddr);
+    else
+      tmem_dealloc<Cfg::kTmemCols>(taddr);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -475,7 +573,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     tma_prefetch(&mg);
     tma_prefetch(&mgl);
   }
-  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(&tslot);
+  constexpr int kWCols = 2 * BN < 32 ? 32 : 2 * BN;  // two group buffers
+  if (warp == 1) tmem_alloc<kWCols>(&tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -576,7 +675,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(taddr);
+  if (warp == 1) tmem_dealloc<kWCols>(taddr);
 }
 
 __global__ void k_split_lo(const float* __restrict__ x, float* __restrict__ lo, int64_t n) {
@@ -650,8 +749,13 @@ int map_mat(CUtensorMap* m, const void* p, bool f16, int cols, int rows, int bc,
 
 template <int BN, bool F16>
 int set_attr_one() {
-  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FwdCfg<BN, F16>::kSmem));
+  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, F16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                FwdCfg<BN, F16, 1>::kSmem));
+  if (BN >= 128) {
+    N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, F16, 2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  FwdCfg<BN, F16, 2>::kSmem));
+  }
   N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 FwdCfg<BN, F16>::kSmem));
   return N2F_OK;
@@ -672,12 +776,23 @@ int set_attrs_once() {
   return N2F_OK;
 }
 
-template <int BN, bool F16>
+template <int BN, bool F16, int CS>
 int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask, const ConvOut& o,
                       float* colsum, int epi, cudaStream_t st) {
-  k_conv3x3_tc<BN, F16><<<pl.grid, kThreadsTc, FwdCfg<BN, F16>::kSmem, st>>>(
-      pl.mx, pl.mxl, pl.mw, pl.mwl, bias, mask, o, colsum, pl.unscale, pl.H, pl.W, pl.C, epi,
-      pl.dbg);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kThreadsTc);
+  cfg.dynamicSmemBytes = FwdCfg<BN, F16, CS>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_tc<BN, F16, CS>, pl.mx, pl.mxl, pl.mw, pl.mwl, bias,
+                              mask, o, colsum, pl.unscale, pl.H, pl.W, pl.C, epi, pl.dbg));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
@@ -685,11 +800,16 @@ int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask,
 template <bool F16>
 int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, const ConvOut& o,
                      float* colsum, int epi, cudaStream_t st) {
+  const bool two = pl.cs == 2;
   switch (pl.N) {
-    case 32: return launch_conv_tc_bn<32, F16>(pl, bias, mask, o, colsum, epi, st);
-    case 64: return launch_conv_tc_bn<64, F16>(pl, bias, mask, o, colsum, epi, st);
-    case 128: return launch_conv_tc_bn<128, F16>(pl, bias, mask, o, colsum, epi, st);
-    case 256: return launch_conv_tc_bn<256, F16>(pl, bias, mask, o, colsum, epi, st);
+    case 32: return launch_conv_tc_bn<32, F16, 1>(pl, bias, mask, o, colsum, epi, st);
+    case 64: return launch_conv_tc_bn<64, F16, 1>(pl, bias, mask, o, colsum, epi, st);
+    case 128:
+      return two ? launch_conv_tc_bn<128, F16, 2>(pl, bias, mask, o, colsum, epi, st)
+                 : launch_conv_tc_bn<128, F16, 1>(pl, bias, mask, o, colsum, epi, st);
+    case 256:
+      return two ? launch_conv_tc_bn<256, F16, 2>(pl, bias, mask, o, colsum, epi, st)
+                 : launch_conv_tc_bn<256, F16, 1>(pl, bias, mask, o, colsum, epi, st);
   }
   return fail(N2F_ERR_ARG, "conv_tc_launch: N=%d", pl.N);
 }
@@ -745,20 +865,30 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
   // are wrong when set): 1 skip the TMEM drain, 2 skip the MMAs, 4 skip TMA
   const char* dbg = getenv("N2F_TC_DEBUG");
   pl->dbg = dbg ? atoi(dbg) : 0;
+  // wide layers (N >= 128) run as CTA pairs (cta_group::2, M = 256: each CTA
+  // stages its own 128 pixels and half of the weight rows); N2F_TC_CLUSTER=1
+  // forces single CTAs
+  const char* cl = getenv("N2F_TC_CLUSTER");
+  pl->cs = (N >= 128 && !(cl && atoi(cl) == 1)) ? 2 : 1;
   // persistent grid: one CTA per SM (two for the narrow layers, whose smem
-  // and register footprints allow it), each walking tiles with a fixed stride
-  const int tiles = conv_tc_tiles(H, W);
+  // and register footprints allow it), each walking cluster tiles with a
+  // fixed stride
+  const int units = ((W + kTW - 1) / kTW) * ((H + kTH * pl->cs - 1) / (kTH * pl->cs));
   const int per_sm = N <= 64 ? 2 : 1;
-  pl->grid = tiles < per_sm * sm_count() ? tiles : per_sm * sm_count();
+  const int max_units = per_sm * sm_count() / pl->cs;
+  pl->grid = pl->cs * (units < max_units ? units : max_units);
+  pl->tiles = units * pl->cs;
   const CUtensorMapSwizzle sw = f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   N2F_TRY(map_act(&pl->mx, x.hi, f16, C, W, H, 32, kTW, kTH, sw));
   N2F_TRY(map_act(&pl->mxl, x.lo, f16, C, W, H, 32, kTW, kTH, sw));
-  N2F_TRY(map_mat(&pl->mw, w.hi, f16, 9 * C, N, 32, N, sw));
-  N2F_TRY(map_mat(&pl->mwl, w.lo, f16, 9 * C, N, 32, N, sw));
+  N2F_TRY(map_mat(&pl->mw, w.hi, f16, 9 * C, N, 32, N / pl->cs, sw));
+  N2F_TRY(map_mat(&pl->mwl, w.lo, f16, 9 * C, N, 32, N / pl->cs, sw));
   return N2F_OK;
 }
 
-int conv_tc_tiles(int H, int W) { return ((W + kTW - 1) / kTW) * ((H + kTH - 1) / kTH); }
+int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any cluster size
+  return ((W + kTW - 1) / kTW) * 2 * ((H + 2 * kTH - 1) / (2 * kTH));
+}
 
 int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* y, void* yhi,
                    void* ylo, float oscale, float* colsum, int epi, cudaStream_t st) {

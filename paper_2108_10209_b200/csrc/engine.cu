@@ -616,7 +616,7 @@ int setup(n2f_ctx* c) {
     for (int sc = 0; sc < 2; ++sc) {
       c->adam_sc[sc] = a;
       for (int li = 1; li <= 7; ++li) {
-        c->adam_sc[sc].t[2 * li + 1].nsplit = li == 7 ? c->nblk_head : c->bias_tiles[sc];
+        c->adam_sc[sc].t[2 * li + 1].nsplit = li == 7 ? c->nblk_head : c->dgrad_plan[sc][li + 1].tiles;
         c->adam_sc[sc].t[2 * li].nsplit = c->wsplit[sc][li];
       }
     }

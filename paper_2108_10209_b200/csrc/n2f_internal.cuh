@@ -84,6 +84,8 @@ struct ConvTcPlan {
   bool f16;
   float unscale;  // 2^-(exp_x + exp_w)
   int dbg;        // profiling experiments only (N2F_TC_DEBUG)
+  int cs;         // CTAs per cluster (2: cta_group::2 pair, M = 256)
+  int tiles;      // 128-pixel tiles = rows of the colsum output
 };
 bool tc_supported(int cin, int cout);
 int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, int W, int C, int N,
@@ -94,7 +96,7 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
 // mode, fp16 hi in FP16 mode).
 int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* y, void* yhi,
                    void* ylo, float oscale, float* colsum, int epi, cudaStream_t st);
-int conv_tc_tiles(int H, int W);
+int conv_tc_tiles(int H, int W);  // upper bound of ConvTcPlan::tiles
 struct WgradTcPlan {
   CUtensorMap mx, mxl, mg, mgl;
   int H, W, C, N, mblocks, nsplit;

@@ -135,6 +135,77 @@ __global__ void __launch_bounds__(128) k_tc_selftest_f16(const uint16_t* __restr
   if (warp == 0) tmem_dealloc<256>(taddr);
 }
 
+
+// 2-SM variant (cluster of 2 CTAs, tcgen05.mma.cta_group::2, M = 256):
+// CTA r stages A rows [128 r, 128 r + 128) and B rows [N/2 r, N/2 r + N/2)
+// (K-major SW128, K = 64 fp16); CTA 0 issues four K = 16 MMAs; each CTA
+// reads its 128 accumulator lanes = D rows [128 r, 128 r + 128).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
+    k_tc_selftest_2sm(const uint16_t* __restrict__ A, const uint16_t* __restrict__ B,
+                      float* __restrict__ D, int N) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  uint8_t* base = align1024(smem_raw);
+  uint8_t* sA = base;
+  uint8_t* sB = base + 16384;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int nh = N / 2;
+  for (int i = tid; i < 128 * 64; i += 128)
+    *reinterpret_cast<uint16_t*>(sA + sw128_offset(i / 64, 2 * (i % 64))) = A[128 * rank * 64 + i];
+  for (int i = tid; i < nh * 64; i += 128)
+    *reinterpret_cast<uint16_t*>(sB + sw128_offset(i / 64, 2 * (i % 64))) = B[nh * rank * 64 + i];
+  fence_proxy_async();
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+                     smem_u32(&tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t taddr = tslot;
+  if (rank == 0 && warp == 0) {
+    if (elect_one_sync()) {
+      const uint32_t idesc = idesc_f16(256, N, false, false);
+      for (int s = 0; s < 4; ++s) {
+        const uint64_t a = sw128_desc(smem_u32(sA) + s * 32, 16, 1024);
+        const uint64_t b = sw128_desc(smem_u32(sB) + s * 32, 16, 1024);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(taddr),
+            "l"(a), "l"(b), "r"(idesc), "r"(s)
+            : "memory");
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+          "[%0], %1;" ::"r"(smem_u32(&bar)),
+          "h"((uint16_t)3)
+          : "memory");
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld32(taddr + ((uint32_t)(warp * 32) << 16) + c0, r);
+    tmem_ld_wait();
+    for (int j = 0; j < 32; ++j)
+      D[(int64_t)(128 * rank + warp * 32 + lane) * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(taddr) : "memory");
+}
+
 }  // namespace
 }  // namespace n2f
 
@@ -194,6 +265,18 @@ extern "C" int n2f_tc_selftest(const float* A, const float* B, float* D, int N, 
     default: s = launch(k_tc_selftest<2, 2>); break;
   }
   if (s != N2F_OK) return s;
+  N2F_CUDA(cudaStreamSynchronize(st));
+  return N2F_OK;
+}
+
+extern "C" int n2f_tc_selftest_2sm(const uint16_t* A, const uint16_t* B, float* D, int N,
+                                   void* stream) {
+  if (N < 32 || N > 256 || N % 32) return fail(N2F_ERR_ARG, "selftest_2sm N=%d", N);
+  const int smem = 1024 + 16384 + (N / 2) * 128;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  N2F_CUDA(cudaFuncSetAttribute(k_tc_selftest_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_tc_selftest_2sm<<<2, 128, smem, st>>>(A, B, D, N);
+  N2F_LAUNCH_CHECK();
   N2F_CUDA(cudaStreamSynchronize(st));
   return N2F_OK;
 }

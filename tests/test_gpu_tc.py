@@ -59,6 +59,23 @@ def test_selftest_gemm_f16(a_mn, b_mn, n):
     assert err < 1e-6
 
 
+@pytest.mark.parametrize("n", [64, 128, 256])
+def test_selftest_gemm_2sm(n):
+    """cta_group::2 (cluster of 2 CTAs, M = 256): A split by rows, B by N halves."""
+    from paper_2108_10209_b200 import _lib
+
+    rng = np.random.default_rng(11 + n)
+    a = rng.standard_normal((256, 64)).astype(np.float16)
+    b = rng.standard_normal((n, 64)).astype(np.float16)
+    da, db, dd = dev(a.view(np.int16)), dev(b.view(np.int16)), empty(256 * n)
+    _lib.call("n2f_tc_selftest_2sm", da.data_ptr(), db.data_ptr(), dd.data_ptr(), n, None)
+    d = host(dd).reshape(256, n)
+    ref = a.astype(np.float64) @ b.astype(np.float64).T
+    err = np.abs(d - ref).max() / np.abs(ref).max()
+    print(f"2sm n={n}: rel err {err:.2e}")
+    assert err < 1e-6
+
+
 def test_split_operands_recover_fp32():
     """hi = tf32-truncated x, lo = x - hi: hi.hi + hi.lo + lo.hi ~ fp32 GEMM."""
     from paper_2108_10209_b200 import _lib
