@@ -147,6 +147,9 @@ struct FwdCfg {
   // with 2 groups' worth of stages; the others take as many stages as fit
   static constexpr bool kTwoPerSm = CS == 1 && BN <= 64;
   static constexpr int kStages = kTwoPerSm ? 2 * P::kGroup : (kMaxStages > 8 ? 8 : kMaxStages);
+  // stages per TMEM accumulation group (K = 64 FP16, 32 TF32; measured: a
+  // 3-stage FP16 group for BN 256 was slower and doubled the truncation bias)
+  static constexpr int kGroup = P::kGroup;
   // epilogue transpose scratch: 8 warps x 32 pixels x kEpiCols fp32
   static constexpr int kEpiCols = BN >= 128 ? 16 : 8;
   static constexpr int kEpiBytes = 8 * 32 * kEpiCols * 4;
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   using P = Prec<F16>;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
-  constexpr int G = P::kGroup;
+  constexpr int G = Cfg::kGroup;
   constexpr int NB = Cfg::kBufs;
   constexpr int UH = kTH * CS;  // rows of a cluster tile (CTA r owns rows [kTH r, kTH r + kTH))
   extern __shared__ uint8_t smem_raw[];
@@ -534,7 +537,7 @@ template <int BN, bool F16>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_wgrad3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                   const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mgl,
-                  float* __restrict__ part, float unscale, int H, int W, int C, int nsplit) {
+                  float* __restrict__ part, float unscale, int H, int W, int C, int nsplit, int xblk) {
   using Cfg = FwdCfg<BN, F16>;  // same stage bytes: A = 4 x 32 px rows, B = BN/32 x 32 px rows
   using P = Prec<F16>;
   constexpr int kBlk = kSegW * P::kRow;  // bytes of one 32-channel MN block
@@ -590,17 +593,21 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       uint8_t* st = base + s * Cfg::kStageBytes;
       if (elect_one_sync()) {
         mbar_arrive_expect_tx(&full[s], stage_bytes);
-        for (int j = 0; j < nblk_a; ++j) {
-          const int mm = m0 + 32 * j, tap = mm / C, c = mm - tap * C;
+        if (xblk) {  // the 4 blocks share one tap: one 4-D box
+          const int tap = m0 / C, c = m0 - tap * C;
           const int ky = tap / 3, kx = tap - 3 * ky;
-          tma_load_3d(st + j * kBlk, &mx, &full[s], c, x0 + kx - 1, y0 + ky - 1);
-          tma_load_3d(st + Cfg::kStageA + j * kBlk, &mxl, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+          tma_load_4d(st, &mx, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
+          tma_load_4d(st + Cfg::kStageA, &mxl, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
+        } else {
+          for (int j = 0; j < nblk_a; ++j) {
+            const int mm = m0 + 32 * j, tap = mm / C, c = mm - tap * C;
+            const int ky = tap / 3, kx = tap - 3 * ky;
+            tma_load_3d(st + j * kBlk, &mx, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+            tma_load_3d(st + Cfg::kStageA + j * kBlk, &mxl, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+          }
         }
-        for (int jn = 0; jn < BN / 32; ++jn) {
-          tma_load_3d(st + 2 * Cfg::kStageA + jn * kBlk, &mg, &full[s], 32 * jn, x0, y0);
-          tma_load_3d(st + 2 * Cfg::kStageA + Cfg::kStageB + jn * kBlk, &mgl, &full[s], 32 * jn, x0,
-                      y0);
-        }
+        tma_load_4d(st + 2 * Cfg::kStageA, &mg, &full[s], 0, x0, 0, y0);
+        tma_load_4d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mgl, &full[s], 0, x0, 0, y0);
       }
       __syncwarp();
     }
@@ -730,6 +737,25 @@ int map_act(CUtensorMap* m, const void* p, bool f16, int C, int W, int H, int bc
   return N2F_OK;
 }
 
+// NHWC activation viewed as 4-D (32 channels, W, C / 32 blocks, H): a box
+// {32, bw, nblk, 1} lands as [block][pixel][32 channels], i.e. nblk MN-major
+// operand blocks of bw pixel rows in one TMA.
+int map_act_blk(CUtensorMap* m, const void* p, bool f16, int C, int W, int H, int bw, int nblk,
+                CUtensorMapSwizzle sw) {
+  N2F_TRY(encoder());
+  const cuuint64_t es = f16 ? 2 : 4;
+  const cuuint64_t dims[4] = {32, (cuuint64_t)W, (cuuint64_t)(C / 32), (cuuint64_t)H};
+  const cuuint64_t strides[3] = {(cuuint64_t)C * es, 32 * es, (cuuint64_t)W * C * es};
+  const cuuint32_t box[4] = {32, (cuuint32_t)bw, (cuuint32_t)nblk, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        4, const_cast<void*>(p), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(act4) failed: %d", (int)r);
+  return N2F_OK;
+}
+
 // Row-major matrix [rows][cols] viewed as 2-D (cols, rows).
 int map_mat(CUtensorMap* m, const void* p, bool f16, int cols, int rows, int bc, int br,
             CUtensorMapSwizzle sw) {
@@ -818,7 +844,7 @@ template <int BN, bool F16>
 int launch_wgrad_tc_bn(const WgradTcPlan& pl, float* part, cudaStream_t st) {
   dim3 grid(pl.mblocks, pl.nsplit);
   k_wgrad3x3_tc<BN, F16><<<grid, kThreadsTc, FwdCfg<BN, F16>::kSmem, st>>>(
-      pl.mx, pl.mxl, pl.mg, pl.mgl, part, pl.unscale, pl.H, pl.W, pl.C, pl.nsplit);
+      pl.mx, pl.mxl, pl.mg, pl.mgl, part, pl.unscale, pl.H, pl.W, pl.C, pl.nsplit, pl.xblk);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
@@ -920,10 +946,19 @@ int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H
   pl->f16 = f16;
   pl->unscale = ldexpf(1.f, -(x.exp + g.exp));
   const CUtensorMapSwizzle sw = f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-  N2F_TRY(map_act(&pl->mx, x.hi, f16, C, W, H, 32, kSegW, 1, sw));
-  N2F_TRY(map_act(&pl->mxl, x.lo, f16, C, W, H, 32, kSegW, 1, sw));
-  N2F_TRY(map_act(&pl->mg, g.hi, f16, N, W, H, 32, kSegW, 1, sw));
-  N2F_TRY(map_act(&pl->mgl, g.lo, f16, N, W, H, 32, kSegW, 1, sw));
+  // one TMA per operand part and stage: the 4 activation blocks of an M block
+  // share a tap when C % 128 == 0 (else one box per block), the gradient's
+  // N / 32 blocks always come as one box
+  pl->xblk = C % 128 == 0;
+  if (pl->xblk) {
+    N2F_TRY(map_act_blk(&pl->mx, x.hi, f16, C, W, H, kSegW, 4, sw));
+    N2F_TRY(map_act_blk(&pl->mxl, x.lo, f16, C, W, H, kSegW, 4, sw));
+  } else {
+    N2F_TRY(map_act(&pl->mx, x.hi, f16, C, W, H, 32, kSegW, 1, sw));
+    N2F_TRY(map_act(&pl->mxl, x.lo, f16, C, W, H, 32, kSegW, 1, sw));
+  }
+  N2F_TRY(map_act_blk(&pl->mg, g.hi, f16, N, W, H, kSegW, N / 32, sw));
+  N2F_TRY(map_act_blk(&pl->mgl, g.lo, f16, N, W, H, kSegW, N / 32, sw));
   return N2F_OK;
 }
 

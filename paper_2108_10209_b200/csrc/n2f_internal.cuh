@@ -102,6 +102,7 @@ struct WgradTcPlan {
   int H, W, C, N, mblocks, nsplit;
   bool f16;
   float unscale;
+  int xblk;  // activation blocks of an M block loaded as one 4-D box (C % 128 == 0)
 };
 int wgrad_tc_nsplit(int cin, int H, int W);
 int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H, int W, int C,
