@@ -306,6 +306,14 @@ def run_ours(args):
     shares = {name: round(float(pms[i].sum() / pms.sum()), 4) for i, name in enumerate(Engine.PROF_CLASSES)}
     epoch_ms_profiled = float(pms.sum())
     conv_tf = float(pfl[[1, 3, 4, 8]].sum() / (pms[[1, 3, 4, 8]].sum() * 1e-3) / 1e12)
+    # the split-precision kernels issue 3 MMAs per algorithmic MAC: FP16x3 at
+    # the fp16/bf16 dense rate (the default), 3xTF32 at half that rate
+    if args.conv_impl == 2:
+        mma_note, mma_cost = "3xTF32: 3 tf32 MMAs (half the bf16 rate) per algorithmic MAC", 2.0
+    elif args.conv_impl == 1:
+        mma_note, mma_cost = "SIMT fp32 (no tensor cores)", 0.0
+    else:
+        mma_note, mma_cost = "FP16x3: 3 fp16 MMAs (bf16 dense rate) per algorithmic MAC", 1.0
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")) as f:
@@ -343,8 +351,8 @@ def run_ours(args):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic,
                          "kernel": kname, "kernel_ms": kms, "kernel_algorithmic_flop": kflop,
-                         "peak_kind": f"{peak_kind} bf16 dense burst; kernels issue 3 tf32 MMAs "
-                                      "(3xTF32 split precision) per algorithmic MAC",
+                         "peak_kind": f"{peak_kind} bf16 dense burst; {mma_note}",
+                         "mma_frac": achieved * 3 * mma_cost / peak_tf,
                          "conv_kernels_tflops": conv_tf, "epoch_ms_profiled": epoch_ms_profiled,
                          "time_share": shares,
                          "path_tflops": path_tflops, "path_frac": path_tflops / peak_tf},

@@ -42,7 +42,7 @@ typedef struct n2f_config {
   int32_t patience_epochs;
   int32_t avg_window;
   int32_t max_epochs;
-  int32_t conv_impl;      /* 0 = auto, 1 = SIMT fp32, 2 = tcgen05 3xTF32 */
+  int32_t conv_impl;      /* 0 = auto (= 3), 1 = SIMT fp32, 2 = tcgen05 3xTF32, 3 = tcgen05 FP16x3 */
   uint64_t seed;
   int32_t use_graph;      /* 1 = whole loop in one CUDA graph (while node), 0 = host loop */
   int32_t reserved[7];

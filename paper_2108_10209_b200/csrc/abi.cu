@@ -206,7 +206,7 @@ int n2f_conv_bwd(const float* g, const float* x, const float* w, const float* ma
     if (db) N2F_TRY(reduce_partials(pb, db, ns, cout, S(stream)));
     const bool tcimpl = impl == kImplTc || impl == kImplTcF16, f16 = impl == kImplTcF16;
     if (dw && tcimpl && tc_supported(cin, cout)) {  // dW on the tensor cores
-      const int nst = wgrad_tc_nsplit(cin, h, wd);
+      const int nst = wgrad_tc_nsplit(cin, cout, h, wd);
       float* ptc;
       N2F_TRY(s.get(&ptc, (size_t)nst * cout * 9 * cin));
       TcOperand ox, og;

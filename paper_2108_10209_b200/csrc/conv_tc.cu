@@ -533,12 +533,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 // ---------------------------------------------------------------------------
 constexpr int kSegW = 32;  // pixels per stage (one image-row segment)
 
-template <int BN, bool F16>
+// CTA pairs (CS = 2, used when C % 128 == 0 and N >= 128): a cluster owns
+// two consecutive M blocks (cta_group::2 MMA, M = 256); each CTA stages its
+// own activation blocks and half of the gradient channels.
+template <int BN, bool F16, int CS>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_wgrad3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                   const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mgl,
                   float* __restrict__ part, float unscale, int H, int W, int C, int nsplit, int xblk) {
-  using Cfg = FwdCfg<BN, F16>;  // same stage bytes: A = 4 x 32 px rows, B = BN/32 x 32 px rows
+  using Cfg = FwdCfg<BN, F16, CS>;  // A = 4 blocks of 32 px rows, B = BN/CS/32 blocks
   using P = Prec<F16>;
   constexpr int kBlk = kSegW * P::kRow;  // bytes of one 32-channel MN block
   constexpr int S = Cfg::kStages;
@@ -549,15 +552,20 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __shared__ uint32_t tslot;
   uint8_t* base = align1024(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
   const int K9 = 9 * C;
-  const int m0 = blockIdx.x * 128;
+  const int m0 = blockIdx.x * 128;  // this CTA's M block ((tap, c) rows)
+  // the second CTA of the last pair may have no M block of its own: it loads
+  // block 0 (valid data for the pair MMA) and stores nothing
+  const bool ghost = m0 >= K9;
+  const int ml = ghost ? 0 : m0;
   const int split = blockIdx.y;
   const int segs_x = (W + kSegW - 1) / kSegW;
   const int nseg = segs_x * H;
   const int s0 = (int)((int64_t)nseg * split / nsplit), s1 = (int)((int64_t)nseg * (split + 1) / nsplit);
   const int KB = s1 - s0;
   const int NG = (KB + G - 1) / G;
-  int nblk_a = (K9 - m0 + 31) / 32;
+  int nblk_a = (K9 - ml + 31) / 32;
   if (nblk_a > 4) nblk_a = 4;
   const uint32_t stage_bytes = (uint32_t)nblk_a * kBlk * 2u + (uint32_t)Cfg::kStageB * 2u;
 
@@ -568,7 +576,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);
+      mbar_init(&tempty[b], 8 * CS);
     }
     fence_barrier_init();
     tma_prefetch(&mx);
@@ -577,14 +585,24 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     tma_prefetch(&mgl);
   }
   constexpr int kWCols = 2 * BN < 32 ? 32 : 2 * BN;  // two group buffers
-  if (warp == 1) tmem_alloc<kWCols>(&tslot);
+  if (warp == 1) {
+    if (CS == 2)
+      tmem_alloc_2sm<kWCols>(&tslot);
+    else
+      tmem_alloc<kWCols>(&tslot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CS == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t taddr = tslot;
 
   if (warp == 0) {
     // ---- TMA producer (whole warp walks the schedule, one elected lane issues)
+    const uint32_t full0 = CS == 2 ? mapa_shared(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
+    const int gblk0 = (int)rank * (BN / 32 / CS);  // this CTA's first gradient block
     for (int kb = 0; kb < KB; ++kb) {
       const int s = kb % S, round = kb / S;
       if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
@@ -592,75 +610,99 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const int y0 = seg / segs_x, x0 = (seg - y0 * segs_x) * kSegW;
       uint8_t* st = base + s * Cfg::kStageBytes;
       if (elect_one_sync()) {
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
-        if (xblk) {  // the 4 blocks share one tap: one 4-D box
-          const int tap = m0 / C, c = m0 - tap * C;
-          const int ky = tap / 3, kx = tap - 3 * ky;
-          tma_load_4d(st, &mx, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
-          tma_load_4d(st + Cfg::kStageA, &mxl, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
-        } else {
-          for (int j = 0; j < nblk_a; ++j) {
-            const int mm = m0 + 32 * j, tap = mm / C, c = mm - tap * C;
+        if (CS == 1) {
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          if (xblk) {  // the 4 blocks share one tap: one 4-D box
+            const int tap = ml / C, c = ml - tap * C;
             const int ky = tap / 3, kx = tap - 3 * ky;
-            tma_load_3d(st + j * kBlk, &mx, &full[s], c, x0 + kx - 1, y0 + ky - 1);
-            tma_load_3d(st + Cfg::kStageA + j * kBlk, &mxl, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+            tma_load_4d(st, &mx, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
+            tma_load_4d(st + Cfg::kStageA, &mxl, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
+          } else {
+            for (int j = 0; j < nblk_a; ++j) {
+              const int mm = ml + 32 * j, tap = mm / C, c = mm - tap * C;
+              const int ky = tap / 3, kx = tap - 3 * ky;
+              tma_load_3d(st + j * kBlk, &mx, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+              tma_load_3d(st + Cfg::kStageA + j * kBlk, &mxl, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+            }
           }
+          tma_load_4d(st + 2 * Cfg::kStageA, &mg, &full[s], 0, x0, 0, y0);
+          tma_load_4d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mgl, &full[s], 0, x0, 0, y0);
+        } else {  // pair: xblk always holds, bytes complete on the leader's barrier
+          const uint32_t fb = full0 + 8u * s;
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], CS * stage_bytes);
+          const int tap = ml / C, c = ml - tap * C;
+          const int ky = tap / 3, kx = tap - 3 * ky;
+          tma_load_4d_2sm(st, &mx, fb, 0, x0 + kx - 1, c / 32, y0 + ky - 1);
+          tma_load_4d_2sm(st + Cfg::kStageA, &mxl, fb, 0, x0 + kx - 1, c / 32, y0 + ky - 1);
+          tma_load_4d_2sm(st + 2 * Cfg::kStageA, &mg, fb, 0, x0, gblk0, y0);
+          tma_load_4d_2sm(st + 2 * Cfg::kStageA + Cfg::kStageB, &mgl, fb, 0, x0, gblk0, y0);
         }
-        tma_load_4d(st + 2 * Cfg::kStageA, &mg, &full[s], 0, x0, 0, y0);
-        tma_load_4d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mgl, &full[s], 0, x0, 0, y0);
       }
       __syncwarp();
     }
   } else if (warp == 1) {
-    // ---- MMA issuer (whole warp waits, one elected lane issues)
-    constexpr uint32_t idesc = P::idesc(128, BN, true, true);
-    constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
-                       kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
-    const uint64_t desc0 = P::mndesc(smem_u32(base));
-    int it = 0;
-    for (int g = 0; g < NG; ++g) {
-      const int b = g & 1;
-      if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
-      const int ng = (g + 1) * G <= KB ? G : KB - g * G;
-      for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
-      tc_fence_after();
-      if (elect_one_sync()) {
-        const uint32_t d = taddr + b * BN;
-        uint64_t ah[G];
+    // ---- MMA issuer (the pair's leader issues for both; whole warp waits,
+    // one elected lane issues)
+    if (rank == 0) {
+      constexpr uint32_t idesc = P::idesc(128 * CS, BN, true, true);
+      constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
+                         kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
+      const uint64_t desc0 = P::mndesc(smem_u32(base));
+      int it = 0;
+      for (int g = 0; g < NG; ++g) {
+        const int b = g & 1;
+        if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+        const int ng = (g + 1) * G <= KB ? G : KB - g * G;
+        for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
+        tc_fence_after();
+        if (elect_one_sync()) {
+          const uint32_t d = taddr + b * BN;
+          uint64_t ah[G];
 #pragma unroll
-        for (int j = 0; j < G; ++j) ah[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
-        // cross terms of the group first, then hi*hi; one K step = 1 KB = 64 units
+          for (int j = 0; j < G; ++j)
+            ah[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
+          // cross terms of the group first, then hi*hi; one K step = 1 KB = 64 units
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-          if (j < ng) {
+          for (int j = 0; j < G; ++j) {
+            if (j < ng) {
 #pragma unroll
-            for (int k = 0; k < P::kKSteps; ++k) {
-              const uint64_t a = ah[j] + 64 * k;
-              P::mma(d, a, a + kBl, idesc, (j | k) != 0);
-              P::mma(d, a + kAl, a + kBh, idesc, 1);
+              for (int k = 0; k < P::kKSteps; ++k) {
+                const uint64_t a = ah[j] + 64 * k;
+                P::template mma<CS>(d, a, a + kBl, idesc, (j | k) != 0);
+                P::template mma<CS>(d, a + kAl, a + kBh, idesc, 1);
+              }
             }
           }
-        }
 #pragma unroll
-        for (int j = 0; j < G; ++j) {
-          if (j < ng) {
+          for (int j = 0; j < G; ++j) {
+            if (j < ng) {
 #pragma unroll
-            for (int k = 0; k < P::kKSteps; ++k) {
-              const uint64_t a = ah[j] + 64 * k;
-              P::mma(d, a, a + kBh, idesc, 1);
+              for (int k = 0; k < P::kKSteps; ++k) {
+                const uint64_t a = ah[j] + 64 * k;
+                P::template mma<CS>(d, a, a + kBh, idesc, 1);
+              }
             }
           }
+          for (int j = 0; j < ng; ++j) {
+            if (CS == 2)
+              mma_commit_2sm(&empty[(it + j) % S]);
+            else
+              mma_commit(&empty[(it + j) % S]);
+          }
+          if (CS == 2)
+            mma_commit_2sm(&tfull[b]);
+          else
+            mma_commit(&tfull[b]);
         }
-        for (int j = 0; j < ng; ++j) mma_commit(&empty[(it + j) % S]);
-        mma_commit(&tfull[b]);
+        __syncwarp();
+        it += ng;
       }
-      __syncwarp();
-      it += ng;
     }
   } else {
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * HALF;
+    const uint32_t tempty0 = CS == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
     float acc[HALF];
 #pragma unroll
     for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
@@ -671,18 +713,31 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       drain_add<HALF>(lane_base + b * BN, acc);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
+      if (lane == 0) {
+        if (CS == 2)
+          mbar_arrive_cluster(tempty0 + 8u * b);
+        else
+          mbar_arrive(&tempty[b]);
+      }
     }
     const int m = m0 + q * 32 + lane;
-    if (m < K9) {
+    if (!ghost && m < K9) {
       float* dst = part + (int64_t)split * BN * K9 + m;
 #pragma unroll
       for (int j = 0; j < HALF; ++j) dst[(int64_t)(half * HALF + j) * K9] = acc[j] * unscale;
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<kWCols>(taddr);
+  if (CS == 2)
+    cluster_sync();
+  else
+    __syncthreads();
+  if (warp == 1) {
+    if (CS == 2)
+      tmem_dealloc_2sm<kWCols>(taddr);
+    else
+      tmem_dealloc<kWCols>(taddr);
+  }
 }
 
 __global__ void k_split_lo(const float* __restrict__ x, float* __restrict__ lo, int64_t n) {
@@ -782,8 +837,13 @@ int set_attr_one() {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   FwdCfg<BN, F16, 2>::kSmem));
   }
-  N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FwdCfg<BN, F16>::kSmem));
+  N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                FwdCfg<BN, F16, 1>::kSmem));
+  if (BN >= 128) {
+    N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  FwdCfg<BN, F16, 2>::kSmem));
+  }
   return N2F_OK;
 }
 
@@ -840,22 +900,38 @@ int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, 
   return fail(N2F_ERR_ARG, "conv_tc_launch: N=%d", pl.N);
 }
 
-template <int BN, bool F16>
+template <int BN, bool F16, int CS>
 int launch_wgrad_tc_bn(const WgradTcPlan& pl, float* part, cudaStream_t st) {
-  dim3 grid(pl.mblocks, pl.nsplit);
-  k_wgrad3x3_tc<BN, F16><<<grid, kThreadsTc, FwdCfg<BN, F16>::kSmem, st>>>(
-      pl.mx, pl.mxl, pl.mg, pl.mgl, part, pl.unscale, pl.H, pl.W, pl.C, pl.nsplit, pl.xblk);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.gridx, pl.nsplit);
+  cfg.blockDim = dim3(kThreadsTc);
+  cfg.dynamicSmemBytes = FwdCfg<BN, F16, CS>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_wgrad3x3_tc<BN, F16, CS>, pl.mx, pl.mxl, pl.mg, pl.mgl, part,
+                              pl.unscale, pl.H, pl.W, pl.C, pl.nsplit, pl.xblk));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
 
 template <bool F16>
 int launch_wgrad_tc_p(const WgradTcPlan& pl, float* part, cudaStream_t st) {
+  const bool two = pl.cs == 2;
   switch (pl.N) {
-    case 32: return launch_wgrad_tc_bn<32, F16>(pl, part, st);
-    case 64: return launch_wgrad_tc_bn<64, F16>(pl, part, st);
-    case 128: return launch_wgrad_tc_bn<128, F16>(pl, part, st);
-    case 256: return launch_wgrad_tc_bn<256, F16>(pl, part, st);
+    case 32: return launch_wgrad_tc_bn<32, F16, 1>(pl, part, st);
+    case 64: return launch_wgrad_tc_bn<64, F16, 1>(pl, part, st);
+    case 128:
+      return two ? launch_wgrad_tc_bn<128, F16, 2>(pl, part, st)
+                 : launch_wgrad_tc_bn<128, F16, 1>(pl, part, st);
+    case 256:
+      return two ? launch_wgrad_tc_bn<256, F16, 2>(pl, part, st)
+                 : launch_wgrad_tc_bn<256, F16, 1>(pl, part, st);
   }
   return fail(N2F_ERR_ARG, "wgrad_tc_launch: N=%d", pl.N);
 }
@@ -924,10 +1000,21 @@ int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, fl
                 : launch_conv_tc_p<false>(pl, bias, mask, o, colsum, epi, st);
 }
 
-int wgrad_tc_nsplit(int cin, int H, int W) {
+namespace {
+// CTA pairs for the wide wgrads (one 4-D activation box per stage and an even
+// split of the gradient channels); N2F_TC_CLUSTER=1 forces single CTAs
+int wgrad_cs(int cin, int cout) {
+  const char* cl = getenv("N2F_TC_CLUSTER");
+  return (cin % 128 == 0 && cout >= 128 && !(cl && atoi(cl) == 1)) ? 2 : 1;
+}
+}  // namespace
+
+int wgrad_tc_nsplit(int cin, int cout, int H, int W) {
+  const int cs = wgrad_cs(cin, cout);
   const int mblocks = (9 * cin + 127) / 128;
+  const int gridx = cs * ((mblocks + cs - 1) / cs);
   const int nseg = ((W + kSegW - 1) / kSegW) * H;
-  int n = 148 / mblocks;
+  int n = sm_count() / gridx;
   if (n < 1) n = 1;
   if (n > nseg) n = nseg;
   return n;
@@ -942,6 +1029,8 @@ int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H
   pl->C = C;
   pl->N = N;
   pl->mblocks = (9 * C + 127) / 128;
+  pl->cs = wgrad_cs(C, N);
+  pl->gridx = pl->cs * ((pl->mblocks + pl->cs - 1) / pl->cs);
   pl->nsplit = nsplit;
   pl->f16 = f16;
   pl->unscale = ldexpf(1.f, -(x.exp + g.exp));
@@ -957,8 +1046,8 @@ int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H
     N2F_TRY(map_act(&pl->mx, x.hi, f16, C, W, H, 32, kSegW, 1, sw));
     N2F_TRY(map_act(&pl->mxl, x.lo, f16, C, W, H, 32, kSegW, 1, sw));
   }
-  N2F_TRY(map_act_blk(&pl->mg, g.hi, f16, N, W, H, kSegW, N / 32, sw));
-  N2F_TRY(map_act_blk(&pl->mgl, g.lo, f16, N, W, H, kSegW, N / 32, sw));
+  N2F_TRY(map_act_blk(&pl->mg, g.hi, f16, N, W, H, kSegW, N / 32 / pl->cs, sw));
+  N2F_TRY(map_act_blk(&pl->mgl, g.lo, f16, N, W, H, kSegW, N / 32 / pl->cs, sw));
   return N2F_OK;
 }
 

@@ -457,7 +457,7 @@ int setup(n2f_ctx* c) {
   const int max_tiles = tiles[0] > tiles[1] ? tiles[0] : tiles[1];
   int wsplit[2][kLayers] = {};  // tcgen05 wgrad split-K per shape class
   for (int sc = 0; sc < 2; ++sc)
-    for (int li = 1; li < 8; ++li) wsplit[sc][li] = wgrad_tc_nsplit(kCin[li], c->ph[2 * sc], c->pw[2 * sc]);
+    for (int li = 1; li < 8; ++li) wsplit[sc][li] = wgrad_tc_nsplit(kCin[li], kCout[li], c->ph[2 * sc], c->pw[2 * sc]);
   for (int li = 0; li < kLayers; ++li) {
     int64_t nb = c->nsplit[li], nw = c->nsplit[li];
     if (c->tc && li >= 1 && li <= 6 && max_tiles > nb) nb = max_tiles;
@@ -746,8 +746,8 @@ int n2f_create(int device, int height, int width, const n2f_config* cfg, n2f_ctx
     return fail(N2F_ERR_ARG,
                 "conv_impl must be 0 (auto), 1 (SIMT), 2 (tcgen05 3xTF32) or 3 (tcgen05 FP16x3)");
   n2f_ctx* c = new n2f_ctx();
-  c->tc = cfg->conv_impl != kImplSimt;  // auto = tcgen05
-  c->f16 = cfg->conv_impl == kImplTcF16;
+  c->tc = cfg->conv_impl != kImplSimt;  // auto = tcgen05 FP16x3
+  c->f16 = cfg->conv_impl == kImplTcF16 || cfg->conv_impl == kImplAuto;
   c->device = device;
   c->H = height;
   c->W = width;

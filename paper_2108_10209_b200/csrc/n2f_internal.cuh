@@ -102,9 +102,11 @@ struct WgradTcPlan {
   int H, W, C, N, mblocks, nsplit;
   bool f16;
   float unscale;
-  int xblk;  // activation blocks of an M block loaded as one 4-D box (C % 128 == 0)
+  int xblk;   // activation blocks of an M block loaded as one 4-D box (C % 128 == 0)
+  int cs;     // CTAs per cluster (2: pairs of M blocks, cta_group::2)
+  int gridx;  // CTAs along M (mblocks rounded up to a multiple of cs)
 };
-int wgrad_tc_nsplit(int cin, int H, int W);
+int wgrad_tc_nsplit(int cin, int cout, int H, int W);
 int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H, int W, int C,
                   int N, int nsplit, bool f16);
 int wgrad_tc_launch(const WgradTcPlan& pl, float* part, cudaStream_t st);

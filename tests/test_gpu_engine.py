@@ -197,7 +197,7 @@ def test_short_fit_matches_oracle_protocol(oracle, use_graph, impl):
     np.testing.assert_allclose(hist, ref.val_history, rtol=5e-2)
     np.testing.assert_allclose(losses, ref.train_losses, rtol=5e-2)
     assert norm_rel(out, ref.denoised) < 2e-2
-    if use_graph and impl == 2:  # the public API (default impl): result types + telemetry schema
+    if use_graph and impl == 3:  # the public API (default impl): result types + telemetry schema
         sink = io.StringIO()
         res = train_single_channel(img, cfg, telemetry=sink, telemetry_tags={"slice": 0})
         assert res.epochs_run == 5 and res.stop_reason == "max_epochs"
