@@ -161,8 +161,8 @@ int n2f_conv_fwd(const float* x, const float* w, const float* b, float* y, int h
     N2F_TRY(make_operand(s, w, (int64_t)cout * 9 * cin, f16, kExpW, &ow, S(stream)));
     ConvTcPlan pl;
     N2F_TRY(conv_tc_plan(&pl, ox, ow, h, wd, cin, cout, f16));
-    N2F_TRY(conv_tc_launch(pl, b, nullptr, y, nullptr, nullptr, 1.f, nullptr,
-                           relu ? kEpiBiasRelu : kEpiBias, S(stream)));
+    N2F_TRY(conv_tc_plan_out(&pl, y, nullptr, nullptr, 1.f));
+    N2F_TRY(conv_tc_launch(pl, b, nullptr, nullptr, relu ? kEpiBiasRelu : kEpiBias, S(stream)));
   } else if (k == 3 && cin % 8 == 0 && cout % 32 == 0) {
     N2F_TRY(conv3x3_simt(x, w, b, nullptr, y, h, wd, cin, cout, relu ? kEpiBiasRelu : kEpiBias,
                          S(stream)));
@@ -235,8 +235,8 @@ int n2f_conv_bwd(const float* g, const float* x, const float* w, const float* ma
       }
       ConvTcPlan pl;
       N2F_TRY(conv_tc_plan(&pl, og, owt, h, wd, cout, cin, f16));
-      N2F_TRY(conv_tc_launch(pl, nullptr, mk, dx, nullptr, nullptr, 1.f, nullptr,
-                             mask ? kEpiMask : kEpiNone, S(stream)));
+      N2F_TRY(conv_tc_plan_out(&pl, dx, nullptr, nullptr, 1.f));
+      N2F_TRY(conv_tc_launch(pl, nullptr, mk, nullptr, mask ? kEpiMask : kEpiNone, S(stream)));
     } else {
       N2F_TRY(conv3x3_simt(g, wt, nullptr, mask, dx, h, wd, cout, cin, mask ? kEpiMask : kEpiNone,
                            S(stream)));

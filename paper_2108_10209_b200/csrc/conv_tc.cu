@@ -142,7 +142,17 @@ struct FwdCfg {
   static constexpr int kStageA = 128 * P::kRow;
   static constexpr int kStageB = (BN / CS) * P::kRow;  // this CTA's share of the weight rows
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
-  static constexpr int kMaxStages = (200 * 1024) / kStageBytes;
+  // epilogue staging (TMA-store source), per accumulate warp 32 pixels x kEpiCols
+  // channels: FP16 the fp32 output OR the fp16 (hi, lo) pair (never both);
+  // TF32 the fp32 output AND its tf32 residual
+  // (wide layers; the narrow ones keep direct transposed stores through a
+  // 32 x kEpiCols fp32 scratch: at 2 CTAs per SM their smem has no room for
+  // double-buffered staging and single-buffered TMA stores measured slower)
+  static constexpr bool kTmaEpi = BN >= 128;
+  static constexpr int kEpiCols = BN >= 128 ? 16 : 8;
+  static constexpr int kEpiWarpBytes = 32 * kEpiCols * ((F16 || !kTmaEpi) ? 4 : 8);
+  static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
+  static constexpr int kMaxStages = (220 * 1024 - kEpiBytes - 1024) / kStageBytes;
   // narrow layers run 2 CTAs per SM (their smem, registers and TMEM allow it)
   // with 2 groups' worth of stages; the others take as many stages as fit
   static constexpr bool kTwoPerSm = CS == 1 && BN <= 64;
@@ -150,9 +160,6 @@ struct FwdCfg {
   // stages per TMEM accumulation group (K = 64 FP16, 32 TF32; measured: a
   // 3-stage FP16 group for BN 256 was slower and doubled the truncation bias)
   static constexpr int kGroup = P::kGroup;
-  // epilogue transpose scratch: 8 warps x 32 pixels x kEpiCols fp32
-  static constexpr int kEpiCols = BN >= 128 ? 16 : 8;
-  static constexpr int kEpiBytes = 8 * 32 * kEpiCols * 4;
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
   // TMEM group buffers: as many as the CTA's column budget holds (<= 4)
   static constexpr int kTmemBudget = kTwoPerSm ? 256 : 512;
@@ -161,8 +168,8 @@ struct FwdCfg {
   static constexpr int kHalf = BN / 2;  // columns per epilogue warp
 };
 
-// Output of a conv epilogue.  y: fp32 values (may be null).  F16: yhi/ylo fp16
-// pair of y * oscale.  TF32: ylo fp32 residual (y itself is hi; requires y).
+// Raw output pointers for the direct-store epilogue.  y: fp32 values (may be
+// null).  F16: yhi/ylo fp16 pair of y * oscale.  TF32: ylo fp32 residual.
 struct ConvOut {
   float* y;
   void* yhi;
@@ -201,6 +208,18 @@ __device__ __forceinline__ void store_pair4(const ConvOut& o, int64_t idx, float
   }
 }
 
+// Row-swizzled 16-byte chunk position inside a TMA staging tile whose rows are
+// RB bytes (the SWIZZLE_32B / SWIZZLE_64B patterns; none for 16-byte rows).
+template <int RB>
+__device__ __forceinline__ int swz_chunk(int row, int k) {
+  if (RB == 64) return k ^ ((row >> 1) & 3);
+  if (RB == 32) return k ^ ((row >> 2) & 1);
+  return k;
+}
+
+// Epilogue output selection (bit mask of ConvTcPlan output maps).
+enum { kOutY = 1, kOutHi = 2, kOutLo = 4 };
+
 template <bool F16>
 __device__ __forceinline__ float4 load_mask4(const void* mask, int64_t idx) {
   if (F16) {
@@ -217,7 +236,9 @@ template <int BN, bool F16, int CS>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
-                 const float* __restrict__ bias, const void* __restrict__ mask, ConvOut out,
+                 const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
+                 const __grid_constant__ CUtensorMap myl, int omask, float oscale, ConvOut out,
+                 const float* __restrict__ bias, const void* __restrict__ mask,
                  float* __restrict__ colsum, float unscale, int H, int W, int C, int epi, int dbg) {
   using Cfg = FwdCfg<BN, F16, CS>;
   using P = Prec<F16>;
@@ -253,6 +274,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     tma_prefetch(&mxl);
     tma_prefetch(&mw);
     tma_prefetch(&mwl);
+    if (omask & kOutY) tma_prefetch(&my);
+    if (omask & kOutHi) tma_prefetch(&myh);
+    if (omask & kOutLo) tma_prefetch(&myl);
   }
   if (warp == 1) {
     if (CS == 2)
@@ -427,13 +451,134 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const long long ce = clock64();
 #endif
 
+      if constexpr (Cfg::kTmaEpi) {
+      // ---- epilogue: lane = pixel (row q of the tile, column x0 + lane),
+      // registers = channels.  Per EC-channel slice: scale removal, bias+ReLU
+      // or the ReLU mask, column sums, then the outputs are staged in smem in
+      // the TMA swizzle layout and written by TMA tensor stores (out-of-image
+      // pixels are clipped by the TMA unit), so the warp never waits on
+      // global stores.
+      constexpr int EC = Cfg::kEpiCols, CH = EC / 4;
+      constexpr int RBY = EC * 4;              // fp32 staging row bytes
+      constexpr int RBH = EC * (F16 ? 2 : 4);  // pair staging row bytes (fp16 / tf32 residual)
+      uint8_t* stg = base + S * Cfg::kStageBytes + (warp - 2) * Cfg::kEpiWarpBytes;
+      uint8_t* stg_h = stg;                                    // F16: hi (union with y)
+      uint8_t* stg_l = F16 ? stg + 32 * EC * 2 : stg + 32 * RBY;  // lo / tf32 residual
+      const int py = y0 + q, px = x0 + lane;
+      const bool valid = py < H && px < W;
+      const int n0 = half * HALF;
+#pragma unroll
+      for (int c0 = 0; c0 < HALF; c0 += EC) {
+        const int n = n0 + c0;
+        float v[EC];
+#pragma unroll
+        for (int i = 0; i < EC; ++i) v[i] = acc[c0 + i] * unscale;
+        if (epi == kEpiBiasRelu || epi == kEpiBias) {
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n) + k);
+            v[4 * k] += bb.x; v[4 * k + 1] += bb.y; v[4 * k + 2] += bb.z; v[4 * k + 3] += bb.w;
+          }
+          if (epi == kEpiBiasRelu) {
+#pragma unroll
+            for (int i = 0; i < EC; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+        } else if (epi == kEpiMask) {
+          const int64_t idx = ((int64_t)py * W + px) * BN + n;
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            float4 mk = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid) mk = load_mask4<F16>(mask, idx + 4 * k);
+            v[4 * k] = mk.x > 0.f ? v[4 * k] : 0.f;
+            v[4 * k + 1] = mk.y > 0.f ? v[4 * k + 1] : 0.f;
+            v[4 * k + 2] = mk.z > 0.f ? v[4 * k + 2] : 0.f;
+            v[4 * k + 3] = mk.w > 0.f ? v[4 * k + 3] : 0.f;
+          }
+        }
+        if (colsum) {  // deterministic per-tile column sums (bias gradient of this tensor)
+          // transpose-reduce: each level halves the channels a lane carries
+          float r[EC];
+#pragma unroll
+          for (int i = 0; i < EC; ++i) r[i] = valid ? v[i] : 0.f;
+          int ch = 0;
+#pragma unroll
+          for (int o = 16, cnt = EC; o >= 1; o >>= 1) {
+            if (cnt > 1) {
+              const int hcnt = cnt / 2;
+              const bool up = (lane & o) != 0;
+#pragma unroll
+              for (int i = 0; i < EC / 2; ++i) {
+                if (i < hcnt) {
+                  const float send = up ? r[i] : r[i + hcnt];
+                  const float keep = up ? r[i + hcnt] : r[i];
+                  r[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+              }
+              ch += up ? hcnt : 0;
+              cnt = hcnt;
+            } else {
+              r[0] += __shfl_xor_sync(0xffffffffu, r[0], o);
+            }
+          }
+          if ((lane & (32 / EC - 1)) == 0) csum[q][n + ch] = r[0];
+        }
+        // the previous slice's TMA stores must have finished reading the staging
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        if (omask & kOutY) {
+#pragma unroll
+          for (int k = 0; k < CH; ++k)
+            *reinterpret_cast<float4*>(stg + lane * RBY + 16 * swz_chunk<RBY>(lane, k)) =
+                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        }
+        if (F16 && (omask & (kOutHi | kOutLo))) {
+          uint32_t hw[EC / 2], lw[EC / 2];
+#pragma unroll
+          for (int i = 0; i < EC; i += 2) {
+            __half h0, l0, h1, l1;
+            split_f16(v[i] * oscale, h0, l0);
+            split_f16(v[i + 1] * oscale, h1, l1);
+            hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+            lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+          }
+#pragma unroll
+          for (int k = 0; k < EC / 8; ++k) {
+            const int off = lane * RBH + 16 * swz_chunk<RBH>(lane, k);
+            *reinterpret_cast<uint4*>(stg_h + off) =
+                make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
+            *reinterpret_cast<uint4*>(stg_l + off) =
+                make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
+          }
+        }
+        if (!F16 && (omask & kOutLo)) {  // tf32 residual of the fp32 output
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            float4 r4;
+            float hh;
+            split_tf32(v[4 * k], hh, r4.x);
+            split_tf32(v[4 * k + 1], hh, r4.y);
+            split_tf32(v[4 * k + 2], hh, r4.z);
+            split_tf32(v[4 * k + 3], hh, r4.w);
+            *reinterpret_cast<float4*>(stg_l + lane * RBH + 16 * swz_chunk<RBH>(lane, k)) = r4;
+          }
+        }
+        fence_proxy_async();  // generic-proxy staging writes -> TMA (async proxy)
+        __syncwarp();
+        if (lane == 0) {
+          if (omask & kOutY) tma_store_3d(&my, stg, n, x0, py);
+          if (F16 && (omask & kOutHi)) tma_store_3d(&myh, stg_h, n, x0, py);
+          if (omask & kOutLo) tma_store_3d(&myl, stg_l, n, x0, py);
+          bulk_commit_group();
+        }
+      }
+      } else {
       // ---- epilogue.  The drain leaves lane = pixel, registers = channels;
       // global rows are pixel-major, so EC-column slices are transposed
       // through a per-warp smem scratch (16-byte chunks XOR-swizzled:
       // conflict-free both ways) and re-read as (pixel, 4-channel chunk)
       // pairs: CPR lanes cover EC contiguous channels of one pixel.
       constexpr int EC = Cfg::kEpiCols, CPR = EC / 4, RPL = 32 / EC;  // rows per 128 B bank line
-      float* scr = reinterpret_cast<float*>(base + S * Cfg::kStageBytes) + (warp - 2) * 32 * EC;
+      float* scr = reinterpret_cast<float*>(base + S * Cfg::kStageBytes + (warp - 2) * Cfg::kEpiWarpBytes);
       const int n0 = half * HALF;
       const int kk = lane % CPR;  // this lane's 4-channel chunk after the transpose
 #pragma unroll
@@ -489,6 +634,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         __syncwarp();  // scratch reused by the next slice
       }
+      }
       if (colsum) {  // the 8 accumulate warps only (named barrier 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
         for (int n = tid - 64; n < BN; n += 256)
@@ -505,6 +651,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
              "drain %lld epilogue %lld\n",
              blockIdx.x, warp, C, BN, CS, H, W, gg, clock64() - t_0, tw, td, te);
 #endif
+    if (lane == 0) bulk_wait0();  // all output stores complete before the CTA retires
   }
   tc_fence_before();
   if (CS == 2)
@@ -863,8 +1010,8 @@ int set_attrs_once() {
 }
 
 template <int BN, bool F16, int CS>
-int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask, const ConvOut& o,
-                      float* colsum, int epi, cudaStream_t st) {
+int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum,
+                      int epi, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(kThreadsTc);
@@ -877,25 +1024,27 @@ int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_tc<BN, F16, CS>, pl.mx, pl.mxl, pl.mw, pl.mwl, bias,
-                              mask, o, colsum, pl.unscale, pl.H, pl.W, pl.C, epi, pl.dbg));
+  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_tc<BN, F16, CS>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
+                              pl.myh, pl.myl, pl.omask, pl.oscale,
+                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, bias, mask, colsum, pl.unscale,
+                              pl.H, pl.W, pl.C, epi, pl.dbg));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
 
 template <bool F16>
-int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, const ConvOut& o,
-                     float* colsum, int epi, cudaStream_t st) {
+int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum,
+                     int epi, cudaStream_t st) {
   const bool two = pl.cs == 2;
   switch (pl.N) {
-    case 32: return launch_conv_tc_bn<32, F16, 1>(pl, bias, mask, o, colsum, epi, st);
-    case 64: return launch_conv_tc_bn<64, F16, 1>(pl, bias, mask, o, colsum, epi, st);
+    case 32: return launch_conv_tc_bn<32, F16, 1>(pl, bias, mask, colsum, epi, st);
+    case 64: return launch_conv_tc_bn<64, F16, 1>(pl, bias, mask, colsum, epi, st);
     case 128:
-      return two ? launch_conv_tc_bn<128, F16, 2>(pl, bias, mask, o, colsum, epi, st)
-                 : launch_conv_tc_bn<128, F16, 1>(pl, bias, mask, o, colsum, epi, st);
+      return two ? launch_conv_tc_bn<128, F16, 2>(pl, bias, mask, colsum, epi, st)
+                 : launch_conv_tc_bn<128, F16, 1>(pl, bias, mask, colsum, epi, st);
     case 256:
-      return two ? launch_conv_tc_bn<256, F16, 2>(pl, bias, mask, o, colsum, epi, st)
-                 : launch_conv_tc_bn<256, F16, 1>(pl, bias, mask, o, colsum, epi, st);
+      return two ? launch_conv_tc_bn<256, F16, 2>(pl, bias, mask, colsum, epi, st)
+                 : launch_conv_tc_bn<256, F16, 1>(pl, bias, mask, colsum, epi, st);
   }
   return fail(N2F_ERR_ARG, "conv_tc_launch: N=%d", pl.N);
 }
@@ -992,12 +1141,44 @@ int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any c
   return ((W + kTW - 1) / kTW) * 2 * ((H + 2 * kTH - 1) / (2 * kTH));
 }
 
-int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* y, void* yhi,
-                   void* ylo, float oscale, float* colsum, int epi, cudaStream_t st) {
-  const ConvOut o{y, yhi, ylo, oscale};
-  if (!pl.f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
-  return pl.f16 ? launch_conv_tc_p<true>(pl, bias, mask, o, colsum, epi, st)
-                : launch_conv_tc_p<false>(pl, bias, mask, o, colsum, epi, st);
+// Output tensor maps of a conv plan: NHWC [H][W][N] viewed as (N, W, H), box
+// {EC channels, 32 pixels, 1 row} = one accumulate warp's staging slice.
+int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale) {
+  if (!pl->f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
+  const int ec = pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4);
+  auto sw_for = [](int row_bytes) {
+    return row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                           : (row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
+  };
+  pl->omask = 0;
+  pl->oscale = oscale;
+  pl->y = y;
+  pl->yhi = yhi;
+  pl->ylo = ylo;
+  if (y) {
+    N2F_TRY(map_act(&pl->my, y, false, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 4)));
+    pl->omask |= kOutY;
+  }
+  if (pl->f16) {
+    if (yhi) {
+      N2F_TRY(map_act(&pl->myh, yhi, true, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 2)));
+      pl->omask |= kOutHi;
+    }
+    if (ylo) {
+      N2F_TRY(map_act(&pl->myl, ylo, true, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 2)));
+      pl->omask |= kOutLo;
+    }
+  } else if (ylo) {
+    N2F_TRY(map_act(&pl->myl, ylo, false, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 4)));
+    pl->omask |= kOutLo;
+  }
+  return N2F_OK;
+}
+
+int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
+                   cudaStream_t st) {
+  return pl.f16 ? launch_conv_tc_p<true>(pl, bias, mask, colsum, epi, st)
+                : launch_conv_tc_p<false>(pl, bias, mask, colsum, epi, st);
 }
 
 namespace {

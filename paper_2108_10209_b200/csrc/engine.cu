@@ -205,7 +205,7 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
   const float* x0 = c->pin + k * c->plane;
   const float* tgt = c->ptgt + k * c->plane;
   const bool f16 = c->f16;
-  const float sa = ldexpf(1.f, kExpAct), sg = ldexpf(1.f, c->exp_g);
+  const float sg = ldexpf(1.f, c->exp_g);
   if (f16) {
     PROF(kPFirst, 0, conv_flop(P, 0),
          conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1));
@@ -215,14 +215,9 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
     PROF(kPFirst, 0, conv_flop(P, 0),
          conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1, c->act_lo[0]));
   }
-  for (int li = 1; li < 8; ++li) {
-    float* y = (!f16 || li == 7) ? c->act[li] : nullptr;
-    void* yhi = (f16 && li < 7) ? c->act16[0][li] : nullptr;
-    void* ylo = li < 7 ? (f16 ? (void*)c->act16[1][li] : (void*)c->act_lo[li]) : nullptr;
+  for (int li = 1; li < 8; ++li)
     PROF(kPFwd, li, conv_flop(P, li),
-         conv_tc_launch(c->fwd_plan[sc][li], B_(c, li), nullptr, y, yhi, ylo, sa, nullptr,
-                        kEpiBiasRelu, st));
-  }
+         conv_tc_launch(c->fwd_plan[sc][li], B_(c, li), nullptr, nullptr, kEpiBiasRelu, st));
   PROF(kPHead, 8, 6.0 * P * kMaxC,
        launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, f16 ? nullptr : c->gA, c->part_w[8],
                          c->part_b[8], c->part_loss + (int64_t)k * c->nblk_head, c->z, P,
@@ -233,17 +228,10 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
   float* gn = c->gB;
   for (int li = 7; li >= 1; --li) {
     PROF(kPWgrad, li, conv_flop(P, li), wgrad_tc_launch(c->wgrad_plan[sc][li], c->part_w[li], st));
-    // output pair goes to the buffer this layer does not read: gB when li is odd
-    const int nb = (li & 1) ? 1 : 0;
-    void *yhi = nullptr, *ylo = nullptr;
-    if (li > 1) {
-      yhi = f16 ? c->g16[nb][0] : nullptr;
-      ylo = f16 ? (void*)c->g16[nb][1] : (void*)(nb ? c->gB_lo : c->gA_lo);
-    }
     const void* mask = f16 ? (const void*)c->act16[0][li - 1] : (const void*)c->act[li - 1];
     PROF(kPDgrad, li, conv_flop(P, li),
-         conv_tc_launch(c->dgrad_plan[sc][li], nullptr, mask, (!f16 || li == 1) ? gn : nullptr, yhi,
-                        ylo, sg, li > 1 ? c->part_b[li - 1] : nullptr, kEpiMask, st));
+         conv_tc_launch(c->dgrad_plan[sc][li], nullptr, mask, li > 1 ? c->part_b[li - 1] : nullptr,
+                        kEpiMask, st));
     float* t = g;
     g = gn;
     gn = t;
@@ -268,15 +256,9 @@ int enqueue_validate_tc(n2f_ctx* c) {
          conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1,
                          c->vA_lo));
   }
-  for (int li = 1; li < 8; ++li) {
-    const int ob = (li & 1) ? 1 : 0;  // layer li writes vB when odd
-    float* out = (!f16 || li == 7) ? (ob ? c->vB : c->vA) : nullptr;
-    void* yhi = (f16 && li < 7) ? c->v16[ob][0] : nullptr;
-    void* ylo = li < 7 ? (f16 ? (void*)c->v16[ob][1] : (void*)(ob ? c->vB_lo : c->vA_lo)) : nullptr;
+  for (int li = 1; li < 8; ++li)
     PROF(kPValConv, li, conv_flop(c->Pv, li),
-         conv_tc_launch(c->val_plan[li], B_(c, li), nullptr, out, yhi, ylo, ldexpf(1.f, kExpAct),
-                        nullptr, kEpiBiasRelu, st));
-  }
+         conv_tc_launch(c->val_plan[li], B_(c, li), nullptr, nullptr, kEpiBiasRelu, st));
   // layer 7 (odd) wrote vB
   PROF(kPHeadVal, 8, 2.0 * c->Pv * kMaxC,
        launch_head_val(c->vB, W_(c, 8), B_(c, 8), c->norm, c->ring, c->Pv, c->nblk_val, c->dstate,
@@ -520,14 +502,32 @@ int setup(n2f_ctx* c) {
       if (f16) return TcOperand{c->v16[ab][0], c->v16[ab][1], kExpAct};
       return ab ? TcOperand{c->vB, c->vB_lo, 0} : TcOperand{c->vA, c->vA_lo, 0};
     };
+    const float sa = ldexpf(1.f, kExpAct), sg = ldexpf(1.f, c->exp_g);
     for (int sc = 0; sc < 2; ++sc) {
       const int h = c->ph[2 * sc], w = c->pw[2 * sc];
       for (int li = 1; li < 8; ++li) {
-        N2F_TRY(conv_tc_plan(&c->fwd_plan[sc][li], act_op(li - 1), w_op(li), h, w, kCin[li],
-                             kCout[li], f16));
+        ConvTcPlan& fp = c->fwd_plan[sc][li];
+        N2F_TRY(conv_tc_plan(&fp, act_op(li - 1), w_op(li), h, w, kCin[li], kCout[li], f16));
+        // forward outputs: the operand pair of the next layer (L8: fp32 for the head)
+        if (li == 7)
+          N2F_TRY(conv_tc_plan_out(&fp, c->act[7], nullptr, nullptr, sa));
+        else if (f16)
+          N2F_TRY(conv_tc_plan_out(&fp, nullptr, c->act16[0][li], c->act16[1][li], sa));
+        else
+          N2F_TRY(conv_tc_plan_out(&fp, c->act[li], nullptr, c->act_lo[li], sa));
         const int ab = (li & 1) ? 0 : 1;  // L8 (li 7) reads gA (head output), then alternate
         N2F_TRY(conv_tc_plan(&c->dgrad_plan[sc][li], g_op(ab), wt_op(li), h, w, kCout[li],
                              kCin[li], f16));
+        // dgrad output: the buffer this layer does not read (B when li is odd);
+        // L1's feeds the SIMT first-layer wgrad in fp32
+        const int nb = 1 - ab;
+        float* gf = nb ? c->gB : c->gA;
+        if (li == 1)
+          N2F_TRY(conv_tc_plan_out(&c->dgrad_plan[sc][li], gf, nullptr, nullptr, sg));
+        else if (f16)
+          N2F_TRY(conv_tc_plan_out(&c->dgrad_plan[sc][li], nullptr, c->g16[nb][0], c->g16[nb][1], sg));
+        else
+          N2F_TRY(conv_tc_plan_out(&c->dgrad_plan[sc][li], gf, nullptr, nb ? c->gB_lo : c->gA_lo, sg));
         N2F_TRY(wgrad_tc_plan(&c->wgrad_plan[sc][li], act_op(li - 1), g_op(ab), h, w, kCin[li],
                               kCout[li], wsplit[sc][li], f16));
       }
@@ -538,6 +538,14 @@ int setup(n2f_ctx* c) {
       const int ab = (li & 1) ? 0 : 1;  // L1 writes vA; layer li reads vA when li is odd
       N2F_TRY(conv_tc_plan(&c->val_plan[li], v_op(ab), w_op(li), c->H, c->W, kCin[li], kCout[li],
                            f16));
+      const int ob = 1 - ab;  // layer li writes vB when odd
+      float* vf = ob ? c->vB : c->vA;
+      if (li == 7)
+        N2F_TRY(conv_tc_plan_out(&c->val_plan[li], vf, nullptr, nullptr, sa));
+      else if (f16)
+        N2F_TRY(conv_tc_plan_out(&c->val_plan[li], nullptr, c->v16[ob][0], c->v16[ob][1], sa));
+      else
+        N2F_TRY(conv_tc_plan_out(&c->val_plan[li], vf, nullptr, ob ? c->vB_lo : c->vA_lo, sa));
     }
     c->bias_tiles[0] = tiles[0];
     c->bias_tiles[1] = tiles[1];

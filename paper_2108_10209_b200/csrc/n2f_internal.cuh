@@ -80,6 +80,12 @@ struct TcOperand {
 };
 struct ConvTcPlan {
   CUtensorMap mx, mxl, mw, mwl;
+  CUtensorMap my, myh, myl;  // outputs (conv_tc_plan_out): fp32, fp16 hi / tf32-or-fp16 lo
+  int omask;                 // which outputs exist (1 y, 2 hi, 4 lo)
+  float oscale;              // FP16 pair = fp16 split of y * oscale
+  float* y;                  // the same outputs as raw pointers (narrow-layer epilogue)
+  void* yhi;
+  void* ylo;
   int H, W, C, N, grid;
   bool f16;
   float unscale;  // 2^-(exp_x + exp_w)
@@ -90,12 +96,13 @@ struct ConvTcPlan {
 bool tc_supported(int cin, int cout);
 int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, int W, int C, int N,
                  bool f16);
-// Outputs: y fp32 (may be null); FP16 plans write the fp16 pair of y * oscale
-// into yhi/ylo (either may be null); TF32 plans write the fp32 residual into
-// ylo (y required).  mask: layer-input tensor for the ReLU mask (fp32 in TF32
-// mode, fp16 hi in FP16 mode).
-int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* y, void* yhi,
-                   void* ylo, float oscale, float* colsum, int epi, cudaStream_t st);
+// Outputs (bound once per plan): y fp32 (may be null); FP16 plans write the
+// fp16 pair of y * oscale into yhi/ylo (either may be null); TF32 plans write
+// the fp32 residual into ylo (y required).  mask at launch: layer-input tensor
+// for the ReLU mask (fp32 in TF32 mode, fp16 hi in FP16 mode).
+int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale);
+int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
+                   cudaStream_t st);
 int conv_tc_tiles(int H, int W);  // upper bound of ConvTcPlan::tiles
 struct WgradTcPlan {
   CUtensorMap mx, mxl, mg, mgl;
