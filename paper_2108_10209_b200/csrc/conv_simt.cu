@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     k_conv_first(const float* __restrict__ x, const float* __restrict__ w,
                  const float* __restrict__ b, float* __restrict__ y, float* __restrict__ ylo, int H,
-                 int W, int N, int relu) {
+                 int W, int N, int relu, __half* __restrict__ yh16, __half* __restrict__ yl16,
+                 float oscale) {
   __shared__ float ws[kMaxC * 9];
   __shared__ float bs[kMaxC];
   for (int i = threadIdx.x; i < N * 9; i += blockDim.x) ws[i] = w[i];
@@ -169,7 +170,20 @@ __global__ void __launch_bounds__(kThreads)
     for (int t = 0; t < 9; ++t) a = fmaf(xv[t], ws[n * 9 + t], a);
     o[j] = relu ? fmaxf(a + bs[n], 0.f) : a + bs[n];
   }
-  *reinterpret_cast<float4*>(y + (size_t)p * N + 4 * q) = make_float4(o[0], o[1], o[2], o[3]);
+  if (y) *reinterpret_cast<float4*>(y + (size_t)p * N + 4 * q) = make_float4(o[0], o[1], o[2], o[3]);
+  if (yh16) {  // fp16 pair of y * oscale for the FP16 tcgen05 consumers
+    uint32_t hw[2], lw[2];
+#pragma unroll
+    for (int j = 0; j < 4; j += 2) {
+      __half h0, l0, h1, l1;
+      tc::split_f16(o[j] * oscale, h0, l0);
+      tc::split_f16(o[j + 1] * oscale, h1, l1);
+      hw[j / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+      lw[j / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+    }
+    *reinterpret_cast<uint2*>(yh16 + (size_t)p * N + 4 * q) = make_uint2(hw[0], hw[1]);
+    *reinterpret_cast<uint2*>(yl16 + (size_t)p * N + 4 * q) = make_uint2(lw[0], lw[1]);
+  }
   if (ylo) {  // tf32 residuals for a tcgen05 consumer
     float l[4], hh;
 #pragma unroll
@@ -313,6 +327,7 @@ __global__ void __launch_bounds__(kThreads)
   float acc[10];
 #pragma unroll
   for (int t = 0; t < 10; ++t) acc[t] = 0.f;
+#pragma unroll 4
   for (int p = pbeg + lane; p < pend; p += nl) {
     const float gv = __ldg(g + (size_t)p * NO + o);
     const int py = p / W, px = p - py * W;
@@ -362,11 +377,14 @@ int conv3x3_simt(const float* x, const float* wk, const float* bias, const float
 }
 
 int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
-                    int cout, cudaStream_t st, int relu, float* ylo) {
+                    int cout, cudaStream_t st, int relu, float* ylo, void* yh16, void* yl16,
+                    float oscale) {
   if (cout % 4 || cout > kMaxC) return fail(N2F_ERR_ARG, "conv_first: cout %d", cout);
+  if (ylo && !y) return fail(N2F_ERR_ARG, "conv_first: tf32 residual needs y");
   const int64_t total = (int64_t)h * w_ * (cout / 4);
   k_conv_first<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, st>>>(
-      x, w, b, y, ylo, h, w_, cout, relu);
+      x, w, b, y, ylo, h, w_, cout, relu, reinterpret_cast<__half*>(yh16),
+      reinterpret_cast<__half*>(yl16), oscale);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
@@ -385,7 +403,9 @@ int wgrad_nsplit(int64_t pixels, int cin, int cout) {
   const int64_t tiles =
       (cin == 1) ? 1 : (int64_t)((cout + bm - 1) / bm) * ((9 * cin + bn - 1) / bn);
   int64_t want = (4 * 148 + tiles - 1) / tiles;
-  int64_t maxs = (pixels + 511) / 512;
+  // the first layer's wgrad (one tile) is latency-bound: more, smaller splits
+  int64_t maxs = (pixels + (cin == 1 ? 127 : 511)) / (cin == 1 ? 128 : 512);
+  if (cin == 1) want = 8 * 148;
   int64_t n = want < maxs ? want : maxs;
   if (n < 1) n = 1;
   if (n > 1024) n = 1024;

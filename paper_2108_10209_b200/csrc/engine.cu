@@ -208,9 +208,8 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
   const float sg = ldexpf(1.f, c->exp_g);
   if (f16) {
     PROF(kPFirst, 0, conv_flop(P, 0),
-         conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1));
-    PROF(kPFirst, 0, 0.0,
-         split_f16(c->act[0], c->act16[0][0], c->act16[1][0], kExpAct, P * kCout[0], st));
+         conv_first_simt(x0, W_(c, 0), B_(c, 0), nullptr, h, w, kCout[0], st, 1, nullptr,
+                         c->act16[0][0], c->act16[1][0], ldexpf(1.f, kExpAct)));
   } else {
     PROF(kPFirst, 0, conv_flop(P, 0),
          conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1, c->act_lo[0]));
@@ -248,9 +247,8 @@ int enqueue_validate_tc(n2f_ctx* c) {
   const bool f16 = c->f16;
   if (f16) {
     PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
-         conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1));
-    PROF(kPValFirst, 0, 0.0,
-         split_f16(c->vA, c->v16[0][0], c->v16[0][1], kExpAct, c->Pv * kCout[0], st));
+         conv_first_simt(c->norm, W_(c, 0), B_(c, 0), nullptr, c->H, c->W, kCout[0], st, 1, nullptr,
+                         c->v16[0][0], c->v16[0][1], ldexpf(1.f, kExpAct)));
   } else {
     PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
          conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1,

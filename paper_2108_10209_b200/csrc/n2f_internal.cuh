@@ -61,7 +61,8 @@ enum Epi { kEpiBiasRelu = 0, kEpiMask = 1, kEpiBias = 2, kEpiNone = 3 };
 int conv3x3_simt(const float* x, const float* wk, const float* bias, const float* mask, float* y,
                  int h, int w, int cin, int cout, int epi, cudaStream_t st);
 int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
-                    int cout, cudaStream_t st, int relu = 1, float* ylo = nullptr);
+                    int cout, cudaStream_t st, int relu = 1, float* ylo = nullptr,
+                    void* yh16 = nullptr, void* yl16 = nullptr, float oscale = 1.f);
 int wgrad3x3_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
                   int cin, int cout, int nsplit, cudaStream_t st);
 int wgrad_first_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
