@@ -317,7 +317,10 @@ def run_ours(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        # only when the capture is of the kernel this run found dominant
+        if kname.startswith(tj.get("kernel", "?")):
+            traffic = tj.get("dram_bytes_per_launch")
     except Exception:
         pass
 
