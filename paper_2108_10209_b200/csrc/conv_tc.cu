@@ -694,8 +694,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
   constexpr int G = P::kGroup;
+  constexpr int NB = Cfg::kBufs;  // TMEM group buffers (4 for N <= 128: the short
+                                  // narrow-layer groups need a deep hand-off queue)
   extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t full[S], empty[S], tfull[2], tempty[2];
+  __shared__ uint64_t full[S], empty[S], tfull[NB], tempty[NB];
   __shared__ uint32_t tslot;
   uint8_t* base = align1024(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -721,7 +723,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NB; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 8 * CS);
     }
@@ -731,7 +733,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     tma_prefetch(&mg);
     tma_prefetch(&mgl);
   }
-  constexpr int kWCols = 2 * BN < 32 ? 32 : 2 * BN;  // two group buffers
+  constexpr int kWCols = Cfg::kTmemCols;
   if (warp == 1) {
     if (CS == 2)
       tmem_alloc_2sm<kWCols>(&tslot);
@@ -750,9 +752,19 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     // ---- TMA producer (whole warp walks the schedule, one elected lane issues)
     const uint32_t full0 = CS == 2 ? mapa_shared(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
     const int gblk0 = (int)rank * (BN / 32 / CS);  // this CTA's first gradient block
+#if N2F_TC_TRACE
+    long long pw = 0, pi = 0, p0 = clock64();
+#endif
     for (int kb = 0; kb < KB; ++kb) {
       const int s = kb % S, round = kb / S;
+#if N2F_TC_TRACE
+      const long long c0 = clock64();
+#endif
       if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+#if N2F_TC_TRACE
+      const long long c1 = clock64();
+      pw += c1 - c0;
+#endif
       const int seg = s0 + kb;
       const int y0 = seg / segs_x, x0 = (seg - y0 * segs_x) * kSegW;
       uint8_t* st = base + s * Cfg::kStageBytes;
@@ -786,7 +798,15 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
       }
       __syncwarp();
+#if N2F_TC_TRACE
+      pi += clock64() - c1;
+#endif
     }
+#if N2F_TC_TRACE
+    if (lane == 0 && (blockIdx.x == 0 && blockIdx.y == 0))
+      printf("[wg prod] C %d BN %d CS %d stages %d total %lld wait_empty %lld issue %lld\n", C, BN, CS,
+             KB, clock64() - p0, pw, pi);
+#endif
   } else if (warp == 1) {
     // ---- MMA issuer (the pair's leader issues for both; whole warp waits,
     // one elected lane issues)
@@ -796,11 +816,25 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                          kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
       const uint64_t desc0 = P::mndesc(smem_u32(base));
       int it = 0;
+#if N2F_TC_TRACE
+      long long we_ = 0, wf_ = 0, is_ = 0, t0_ = clock64();
+#endif
       for (int g = 0; g < NG; ++g) {
-        const int b = g & 1;
-        if (g >= 2) mbar_wait(&tempty[b], ((g >> 1) - 1) & 1);
+        const int b = g % NB;
+#if N2F_TC_TRACE
+        const long long c0 = clock64();
+#endif
+        if (g >= NB) mbar_wait(&tempty[b], ((g / NB) - 1) & 1);
+#if N2F_TC_TRACE
+        const long long c1 = clock64();
+        we_ += c1 - c0;
+#endif
         const int ng = (g + 1) * G <= KB ? G : KB - g * G;
         for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
+#if N2F_TC_TRACE
+        const long long c2 = clock64();
+        wf_ += c2 - c1;
+#endif
         tc_fence_after();
         if (elect_one_sync()) {
           const uint32_t d = taddr + b * BN;
@@ -842,8 +876,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             mma_commit(&tfull[b]);
         }
         __syncwarp();
+#if N2F_TC_TRACE
+        is_ += clock64() - c2;
+#endif
         it += ng;
       }
+#if N2F_TC_TRACE
+      if (lane == 0 && (blockIdx.x == 0 && blockIdx.y == 0))
+        printf("[wg mma] C %d BN %d CS %d groups %d total %lld wait_tempty %lld wait_full %lld issue %lld\n",
+               C, BN, CS, NG, clock64() - t0_, we_, wf_, is_);
+#endif
     }
   } else {
     const int q = warp & 3;
@@ -854,8 +896,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
     for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
     for (int g = 0; g < NG; ++g) {
-      const int b = g & 1;
-      mbar_wait(&tfull[b], (g >> 1) & 1);
+      const int b = g % NB;
+      mbar_wait(&tfull[b], (g / NB) & 1);
       tc_fence_after();
       drain_add<HALF>(lane_base + b * BN, acc);
       tc_fence_before();
@@ -1195,7 +1237,11 @@ int wgrad_tc_nsplit(int cin, int cout, int H, int W) {
   const int mblocks = (9 * cin + 127) / 128;
   const int gridx = cs * ((mblocks + cs - 1) / cs);
   const int nseg = ((W + kSegW - 1) / kSegW) * H;
-  int n = sm_count() / gridx;
+  // narrow layers (N <= 64) fit two CTAs per SM: twice the splits keeps two
+  // TMA pipelines in flight per SM (their short MMA stages are latency-bound)
+  const char* ws = getenv("N2F_WGRAD_PER_SM");
+  const int per_sm = ws ? atoi(ws) : (cout <= 64 ? 2 : 1);
+  int n = per_sm * sm_count() / gridx;
   if (n < 1) n = 1;
   if (n > nseg) n = nseg;
   return n;

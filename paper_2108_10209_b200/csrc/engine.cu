@@ -419,11 +419,16 @@ int setup(n2f_ctx* c) {
   N2F_TRY(dalloc(c, &c->m, off));
   N2F_TRY(dalloc(c, &c->v, off));
   for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt[li], c->pnum[2 * li]));
-  for (int li = 0; li < 8; ++li) N2F_TRY(dalloc(c, &c->act[li], c->Pt * kCout[li]));
+  // FP16x3 keeps layer outputs as fp16 operand pairs (allocated below); fp32
+  // copies only where an fp32 consumer exists: L8's output (the head), the L1
+  // dgrad output (the SIMT first-layer wgrad) and the validation L8 output
+  const bool f16 = c->f16;
+  for (int li = 0; li < 8; ++li)
+    if (!f16 || li == 7) N2F_TRY(dalloc(c, &c->act[li], c->Pt * kCout[li]));
   N2F_TRY(dalloc(c, &c->z, c->Pt));
-  N2F_TRY(dalloc(c, &c->gA, c->Pt * kMaxC));
-  N2F_TRY(dalloc(c, &c->gB, c->Pt * kMaxC));
-  N2F_TRY(dalloc(c, &c->vA, c->Pv * kMaxC));
+  if (!f16) N2F_TRY(dalloc(c, &c->gA, c->Pt * kMaxC));
+  N2F_TRY(dalloc(c, &c->gB, c->Pt * (f16 ? kCout[0] : kMaxC)));
+  if (!f16) N2F_TRY(dalloc(c, &c->vA, c->Pv * kMaxC));
   N2F_TRY(dalloc(c, &c->vB, c->Pv * kMaxC));
   N2F_TRY(dalloc(c, &c->ring, (int64_t)c->cfg.avg_window * c->Pv));
 

@@ -27,6 +27,7 @@ def main():
     eng = Engine(args.size, args.size, TrainConfig(seed=0, max_epochs=3, patience_epochs=10**6),
                  conv_impl=args.impl)
     eng.fit_host(np.ascontiguousarray(noisy))  # warm up + leaves a prepared context
+    print(f"context device bytes: {eng.device_bytes / 2**30:.2f} GiB")
     ms, fl, ln = eng.profile_epoch()
     total = ms.sum()
     rows = []
