@@ -238,8 +238,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
                  const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
                  const __grid_constant__ CUtensorMap myl, int omask, float oscale, ConvOut out,
-                 const float* __restrict__ bias, const void* __restrict__ mask,
-                 float* __restrict__ colsum, float unscale, int H, int W, int C, int epi, int dbg) {
+                 const float* __restrict__ bias, const void* __restrict__ mask, int mask_bits,
+                 uint32_t* __restrict__ mbits_out, float* __restrict__ colsum, float unscale, int H,
+                 int W, int C, int epi, int dbg) {
   using Cfg = FwdCfg<BN, F16, CS>;
   using P = Prec<F16>;
   constexpr int S = Cfg::kStages;
@@ -467,6 +468,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       const int py = y0 + q, px = x0 + lane;
       const bool valid = py < H && px < W;
       const int n0 = half * HALF;
+      // ReLU masks as bits: [pixel][BN / 32] words, bit = channel > 0 (the
+      // forward writes them, the dgrad of the next layer reads them: 1/16 of
+      // the fp16 mask bytes, one load per thread per tile)
+      constexpr int WPP = BN / 32, MW = HALF / 32 > 0 ? HALF / 32 : 1;
+      const int64_t pix = (int64_t)py * W + px;
+      uint32_t mw[MW];
+      if (epi == kEpiMask && mask_bits) {
+#pragma unroll
+        for (int k = 0; k < MW; ++k)
+          mw[k] = valid ? __ldg(reinterpret_cast<const uint32_t*>(mask) + pix * WPP + n0 / 32 + k) : 0u;
+      }
+      uint32_t ob = 0;
 #pragma unroll
       for (int c0 = 0; c0 < HALF; c0 += EC) {
         const int n = n0 + c0;
@@ -483,8 +496,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 #pragma unroll
             for (int i = 0; i < EC; ++i) v[i] = fmaxf(v[i], 0.f);
           }
+        } else if (epi == kEpiMask && mask_bits) {
+          const uint32_t bits = mw[c0 / 32] >> (c0 % 32);
+#pragma unroll
+          for (int i = 0; i < EC; ++i) v[i] = ((bits >> i) & 1u) ? v[i] : 0.f;
         } else if (epi == kEpiMask) {
-          const int64_t idx = ((int64_t)py * W + px) * BN + n;
+          const int64_t idx = pix * BN + n;
 #pragma unroll
           for (int k = 0; k < CH; ++k) {
             float4 mk = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -493,6 +510,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             v[4 * k + 1] = mk.y > 0.f ? v[4 * k + 1] : 0.f;
             v[4 * k + 2] = mk.z > 0.f ? v[4 * k + 2] : 0.f;
             v[4 * k + 3] = mk.w > 0.f ? v[4 * k + 3] : 0.f;
+          }
+        }
+        if (mbits_out) {  // this layer's ReLU mask for the next layer's dgrad
+          uint32_t sb = 0;
+#pragma unroll
+          for (int i = 0; i < EC; ++i) sb |= (v[i] > 0.f ? 1u : 0u) << i;
+          ob |= sb << (c0 % 32);
+          if ((c0 + EC) % 32 == 0) {
+            if (valid) mbits_out[pix * WPP + n / 32] = ob;
+            ob = 0;
           }
         }
         if (colsum) {  // deterministic per-tile column sums (bias gradient of this tensor)
@@ -1068,7 +1095,8 @@ int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask,
   cfg.numAttrs = 1;
   N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_tc<BN, F16, CS>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
                               pl.myh, pl.myl, pl.omask, pl.oscale,
-                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, bias, mask, colsum, pl.unscale,
+                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, bias, mask, pl.mask_bits,
+                              pl.mbits_out, colsum, pl.unscale,
                               pl.H, pl.W, pl.C, epi, pl.dbg));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
@@ -1194,6 +1222,8 @@ int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscal
   };
   pl->omask = 0;
   pl->oscale = oscale;
+  pl->mbits_out = nullptr;
+  pl->mask_bits = 0;
   pl->y = y;
   pl->yhi = yhi;
   pl->ylo = ylo;
@@ -1214,6 +1244,14 @@ int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscal
     N2F_TRY(map_act(&pl->myl, ylo, false, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 4)));
     pl->omask |= kOutLo;
   }
+  return N2F_OK;
+}
+
+int conv_tc_plan_maskbits(ConvTcPlan* pl, uint32_t* mbits_out, int mask_bits_in) {
+  if ((mbits_out || mask_bits_in) && pl->N < 128)
+    return fail(N2F_ERR_ARG, "bit-packed ReLU masks need N >= 128 (TMA epilogue), N=%d", pl->N);
+  pl->mbits_out = mbits_out;
+  pl->mask_bits = mask_bits_in;
   return N2F_OK;
 }
 

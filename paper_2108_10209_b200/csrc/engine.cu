@@ -104,6 +104,7 @@ struct n2f_ctx {
   __half* act16[2][kLayers] = {}; // layer outputs 0..6
   __half* g16[2][2] = {};         // [A/B][hi/lo] gradient ping-pong
   __half* v16[2][2] = {};         // [A/B][hi/lo] validation ping-pong
+  uint32_t* mbits[kLayers] = {};  // bit-packed ReLU masks of the wide forward outputs (L5..L7)
   ConvTcPlan fwd_plan[2][kLayers]{};
   ConvTcPlan dgrad_plan[2][kLayers]{};
   ConvTcPlan val_plan[kLayers]{};
@@ -227,7 +228,8 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
   float* gn = c->gB;
   for (int li = 7; li >= 1; --li) {
     PROF(kPWgrad, li, conv_flop(P, li), wgrad_tc_launch(c->wgrad_plan[sc][li], c->part_w[li], st));
-    const void* mask = f16 ? (const void*)c->act16[0][li - 1] : (const void*)c->act[li - 1];
+    const void* mask = c->mbits[li - 1] ? (const void*)c->mbits[li - 1]
+                       : f16 ? (const void*)c->act16[0][li - 1] : (const void*)c->act[li - 1];
     PROF(kPDgrad, li, conv_flop(P, li),
          conv_tc_launch(c->dgrad_plan[sc][li], nullptr, mask, li > 1 ? c->part_b[li - 1] : nullptr,
                         kEpiMask, st));
@@ -506,6 +508,9 @@ int setup(n2f_ctx* c) {
       return ab ? TcOperand{c->vB, c->vB_lo, 0} : TcOperand{c->vA, c->vA_lo, 0};
     };
     const float sa = ldexpf(1.f, kExpAct), sg = ldexpf(1.f, c->exp_g);
+    // wide forward outputs feeding a wide dgrad also emit bit-packed ReLU masks
+    for (int li = 1; li < 7; ++li)
+      if (kCout[li] >= 128) N2F_TRY(dalloc(c, &c->mbits[li], c->Pt * (kCout[li] / 32)));
     for (int sc = 0; sc < 2; ++sc) {
       const int h = c->ph[2 * sc], w = c->pw[2 * sc];
       for (int li = 1; li < 8; ++li) {
@@ -518,6 +523,7 @@ int setup(n2f_ctx* c) {
           N2F_TRY(conv_tc_plan_out(&fp, nullptr, c->act16[0][li], c->act16[1][li], sa));
         else
           N2F_TRY(conv_tc_plan_out(&fp, c->act[li], nullptr, c->act_lo[li], sa));
+        if (c->mbits[li]) N2F_TRY(conv_tc_plan_maskbits(&fp, c->mbits[li], 0));
         const int ab = (li & 1) ? 0 : 1;  // L8 (li 7) reads gA (head output), then alternate
         N2F_TRY(conv_tc_plan(&c->dgrad_plan[sc][li], g_op(ab), wt_op(li), h, w, kCout[li],
                              kCin[li], f16));
@@ -531,6 +537,7 @@ int setup(n2f_ctx* c) {
           N2F_TRY(conv_tc_plan_out(&c->dgrad_plan[sc][li], nullptr, c->g16[nb][0], c->g16[nb][1], sg));
         else
           N2F_TRY(conv_tc_plan_out(&c->dgrad_plan[sc][li], gf, nullptr, nb ? c->gB_lo : c->gA_lo, sg));
+        if (c->mbits[li - 1]) N2F_TRY(conv_tc_plan_maskbits(&c->dgrad_plan[sc][li], nullptr, 1));
         N2F_TRY(wgrad_tc_plan(&c->wgrad_plan[sc][li], act_op(li - 1), g_op(ab), h, w, kCin[li],
                               kCout[li], wsplit[sc][li], f16));
       }

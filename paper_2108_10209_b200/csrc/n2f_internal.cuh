@@ -84,6 +84,8 @@ struct ConvTcPlan {
   CUtensorMap my, myh, myl;  // outputs (conv_tc_plan_out): fp32, fp16 hi / tf32-or-fp16 lo
   int omask;                 // which outputs exist (1 y, 2 hi, 4 lo)
   float oscale;              // FP16 pair = fp16 split of y * oscale
+  uint32_t* mbits_out;       // bit-packed ReLU mask of the output ([px][N/32]), or null
+  int mask_bits;             // the launch's `mask` is such a bit mask (else fp16/fp32 values)
   float* y;                  // the same outputs as raw pointers (narrow-layer epilogue)
   void* yhi;
   void* ylo;
@@ -102,6 +104,9 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
 // the fp32 residual into ylo (y required).  mask at launch: layer-input tensor
 // for the ReLU mask (fp32 in TF32 mode, fp16 hi in FP16 mode).
 int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale);
+// Wide layers (N >= 128): the forward can emit its ReLU mask bit-packed, the
+// dgrad can consume one (call after conv_tc_plan_out).
+int conv_tc_plan_maskbits(ConvTcPlan* pl, uint32_t* mbits_out, int mask_bits_in);
 int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
                    cudaStream_t st);
 int conv_tc_tiles(int H, int W);  // upper bound of ConvTcPlan::tiles
