@@ -694,6 +694,319 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 }
 
 // ---------------------------------------------------------------------------
+// FP16x3 3x3 conv forward / dgrad with halo reuse ("dy stages"), CTA pairs.
+//   Each CTA owns a 16 (x) x 8 (y) pixel tile whose 128 GEMM rows are ordered
+//   y-fastest (m = 8 * x + y); the pair covers 32 x 8 pixels (M = 256,
+//   tcgen05.mma.cta_group::2, each CTA staging half of the weight rows).
+//   A K stage is (32-channel chunk, dy): ONE activation box of 18 x-columns x
+//   8 rows (tile + x halo, shifted by dy) serves the three dx taps, because a
+//   dx shift of the tile is exactly 8 GEMM rows = one swizzle atom (descriptor
+//   offset); one 4-D weight box holds the three taps' weight rows.  Relative
+//   to one box per tap this cuts the activation bytes per MAC by 2.7x and the
+//   TMA instruction count by 3x.  A stage is one TMEM accumulation group
+//   (K = 96: 18 MMAs, 6 of them hi*hi).  Epilogue: TMA tensor stores.
+// ---------------------------------------------------------------------------
+template <int BN>
+struct DyCfg {
+  static constexpr int kRowsA = 18 * 8;              // halo columns x rows
+  static constexpr int kStageA = kRowsA * 64;        // one fp16 part (hi or lo), 32 channels
+  static constexpr int kTapB = (BN / 2) * 64;        // this CTA's weight rows of one tap
+  static constexpr int kStageB = 3 * kTapB;          // the three dx taps
+  static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
+  static constexpr int kEpiCols = BN == 256 ? 8 : 16;
+  static constexpr int kEpiBuf = 32 * kEpiCols * 4;  // one staging buffer (fp32 y, or the fp16 pair)
+  static constexpr int kEpiWarpBytes = 2 * kEpiBuf;  // double-buffered
+  static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
+  static constexpr int kMaxStages = (218 * 1024 - kEpiBytes - 1024) / kStageBytes;
+  static constexpr int kStages = kMaxStages > 8 ? 8 : kMaxStages;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
+  static constexpr int kBufs = 512 / BN > 4 ? 4 : 512 / BN;  // TMEM group buffers
+  static constexpr int kTmemCols = kBufs * BN;
+  static constexpr int kHalf = BN / 2;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreadsTc, 1)
+    k_conv3x3_dy(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
+                 const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
+                 const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
+                 const __grid_constant__ CUtensorMap myl, int omask, float oscale,
+                 const float* __restrict__ bias, const void* __restrict__ mask, int mask_bits,
+                 uint32_t* __restrict__ mbits_out, float* __restrict__ colsum, float unscale, int H,
+                 int W, int C, int epi) {
+  using Cfg = DyCfg<BN>;
+  using P = Prec<true>;
+  constexpr int S = Cfg::kStages;
+  constexpr int HALF = Cfg::kHalf;
+  constexpr int NB = Cfg::kBufs;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ uint64_t full[S], empty[S], tfull[NB], tempty[NB];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(16) float csum[4][BN];
+  uint8_t* base = align1024(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  const int tiles_x = (W + 31) / 32;
+  const int nunits = tiles_x * ((H + 7) / 8);
+  const int KB = 3 * (C / 32);  // stages (= groups) per tile
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 16);  // every accumulate warp of the pair
+    }
+    fence_barrier_init();
+    tma_prefetch(&mx);
+    tma_prefetch(&mxl);
+    tma_prefetch(&mw);
+    tma_prefetch(&mwl);
+    if (omask & kOutY) tma_prefetch(&my);
+    if (omask & kOutHi) tma_prefetch(&myh);
+    if (omask & kOutLo) tma_prefetch(&myl);
+  }
+  if (warp == 1) tmem_alloc_2sm<Cfg::kTmemCols>(&tslot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t taddr = tslot;
+
+  if (warp == 0) {
+    // ---- TMA producer: per stage one activation box (hi, lo) and one
+    // three-tap weight box (hi, lo); bytes complete on the leader's barrier
+    const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);
+    const int n0 = (int)rank * (BN / 2);
+    int it = 0;
+    for (int ut = cid; ut < nunits; ut += ncl) {
+      const int x0 = (ut % tiles_x) * 32 + 16 * (int)rank, y0 = (ut / tiles_x) * 8;
+      for (int kb = 0; kb < KB; ++kb, ++it) {
+        const int s = it % S, round = it / S;
+        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
+        const int c0 = (kb / 3) * 32, dy = kb % 3;
+        uint8_t* st = base + s * Cfg::kStageBytes;
+        if (elect_one_sync()) {
+          const uint32_t fb = full0 + 8u * s;
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+          tma_load_3d_2sm(st, &mx, fb, c0, y0 + dy - 1, x0 - 1);
+          tma_load_3d_2sm(st + Cfg::kStageA, &mxl, fb, c0, y0 + dy - 1, x0 - 1);
+          tma_load_4d_2sm(st + 2 * Cfg::kStageA, &mw, fb, c0, n0, 0, dy);
+          tma_load_4d_2sm(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, fb, c0, n0, 0, dy);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer (the leader issues for the pair): one stage = one group
+    if (rank == 0) {
+      constexpr uint32_t idesc = P::idesc(256, BN, false, false);
+      constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
+                         kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4, kTap = Cfg::kTapB >> 4;
+      const uint64_t desc0 = P::kdesc(smem_u32(base));
+      int gg = 0;
+      for (int ut = cid; ut < nunits; ut += ncl) {
+        for (int kb = 0; kb < KB; ++kb, ++gg) {
+          const int s = gg % S, b = gg % NB;
+          if (gg >= NB) mbar_wait(&tempty[b], ((gg / NB) - 1) & 1);
+          mbar_wait(&full[s], (gg / S) & 1);
+          tc_fence_after();
+          if (elect_one_sync()) {
+            const uint32_t d = taddr + b * BN;
+            const uint64_t a0 = desc0 + (uint64_t)(s * (Cfg::kStageBytes >> 4));
+            // cross terms of the three taps first, then hi*hi; a dx shift is
+            // 8 rows = 512 B = 32 descriptor units, a K step 32 B = 2 units
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                const uint64_t a = a0 + 32 * dx + 2 * k, bh = a0 + kBh + kTap * dx + 2 * k;
+                mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, (dx | k) != 0);
+                mma_f16_2sm(d, a + kAl, bh, idesc, 1);
+              }
+            }
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+              for (int k = 0; k < 2; ++k)
+                mma_f16_2sm(d, a0 + 32 * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k, idesc, 1);
+            }
+            mma_commit_2sm(&empty[s]);
+            mma_commit_2sm(&tfull[b]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ---- group accumulation in registers (round-to-nearest fp32 adds)
+    const int q = warp & 3;            // TMEM lane quarter
+    const int half = (warp - 2) >> 2;  // column half
+    const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * HALF;
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    // this lane's pixel: GEMM row m = 32 q + lane = 8 * xl + yl
+    const int xl = 4 * q + (lane >> 3), yl = lane & 7;
+    constexpr int EC = DyCfg<BN>::kEpiCols, CH = EC / 4;
+    constexpr int RBY = EC * 4, RBH = EC * 2;  // staging row bytes: fp32 / fp16
+    const int srow = yl * 4 + (lane >> 3);      // staging row: box {EC ch, 4 x, 8 y}
+    uint8_t* stg0 = base + S * Cfg::kStageBytes + (warp - 2) * Cfg::kEpiWarpBytes;
+    int gg = 0, sb = 0;
+    for (int ut = cid; ut < nunits; ut += ncl) {
+      const int x0 = (ut % tiles_x) * 32 + 16 * (int)rank, y0 = (ut / tiles_x) * 8;
+      const int tile = ut * 2 + (int)rank;  // colsum row
+      float acc[HALF];
+#pragma unroll
+      for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
+      for (int kb = 0; kb < KB; ++kb, ++gg) {
+        const int b = gg % NB;
+        mbar_wait(&tfull[b], (gg / NB) & 1);
+        tc_fence_after();
+        drain_add<HALF>(lane_base + b * BN, acc);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty0 + 8u * b);
+      }
+
+      // ---- epilogue (see k_conv3x3_tc): scale removal, bias+ReLU or the ReLU
+      // mask, column sums, bit masks, staging in the TMA swizzle layout and
+      // TMA tensor stores of {EC channels, 4 x, 8 y} boxes
+      const int px = x0 + xl, py = y0 + yl;
+      const bool valid = py < H && px < W;
+      const int n0 = half * HALF;
+      constexpr int WPP = BN / 32, MW = HALF / 32 > 0 ? HALF / 32 : 1;
+      const int64_t pix = (int64_t)py * W + px;
+      uint32_t mw[MW];
+      if (epi == kEpiMask && mask_bits) {
+#pragma unroll
+        for (int k = 0; k < MW; ++k)
+          mw[k] = valid ? __ldg(reinterpret_cast<const uint32_t*>(mask) + pix * WPP + n0 / 32 + k) : 0u;
+      }
+      uint32_t ob = 0;
+#pragma unroll
+      for (int c0 = 0; c0 < HALF; c0 += EC) {
+        const int n = n0 + c0;
+        float v[EC];
+#pragma unroll
+        for (int i = 0; i < EC; ++i) v[i] = acc[c0 + i] * unscale;
+        if (epi == kEpiBiasRelu || epi == kEpiBias) {
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n) + k);
+            v[4 * k] += bb.x; v[4 * k + 1] += bb.y; v[4 * k + 2] += bb.z; v[4 * k + 3] += bb.w;
+          }
+          if (epi == kEpiBiasRelu) {
+#pragma unroll
+            for (int i = 0; i < EC; ++i) v[i] = fmaxf(v[i], 0.f);
+          }
+        } else if (epi == kEpiMask && mask_bits) {
+          const uint32_t bits = mw[(c0 / 32) % MW] >> (n % 32);
+#pragma unroll
+          for (int i = 0; i < EC; ++i) v[i] = ((bits >> i) & 1u) ? v[i] : 0.f;
+        } else if (epi == kEpiMask) {
+          const int64_t idx = pix * BN + n;
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            float4 mk = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (valid) mk = load_mask4<true>(mask, idx + 4 * k);
+            v[4 * k] = mk.x > 0.f ? v[4 * k] : 0.f;
+            v[4 * k + 1] = mk.y > 0.f ? v[4 * k + 1] : 0.f;
+            v[4 * k + 2] = mk.z > 0.f ? v[4 * k + 2] : 0.f;
+            v[4 * k + 3] = mk.w > 0.f ? v[4 * k + 3] : 0.f;
+          }
+        }
+        if (mbits_out) {  // this layer's ReLU mask for the next layer's dgrad
+          uint32_t sbits = 0;
+#pragma unroll
+          for (int i = 0; i < EC; ++i) sbits |= (v[i] > 0.f ? 1u : 0u) << i;
+          ob |= sbits << (n % 32);
+          if ((n + EC) % 32 == 0) {
+            if (valid) mbits_out[pix * WPP + n / 32] = ob;
+            ob = 0;
+          }
+        }
+        if (colsum) {  // transpose-reduce column sums over the warp's 32 pixels
+          float r[EC];
+#pragma unroll
+          for (int i = 0; i < EC; ++i) r[i] = valid ? v[i] : 0.f;
+          int ch = 0;
+#pragma unroll
+          for (int o = 16, cnt = EC; o >= 1; o >>= 1) {
+            if (cnt > 1) {
+              const int hcnt = cnt / 2;
+              const bool up = (lane & o) != 0;
+#pragma unroll
+              for (int i = 0; i < EC / 2; ++i) {
+                if (i < hcnt) {
+                  const float send = up ? r[i] : r[i + hcnt];
+                  const float keep = up ? r[i + hcnt] : r[i];
+                  r[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+              }
+              ch += up ? hcnt : 0;
+              cnt = hcnt;
+            } else {
+              r[0] += __shfl_xor_sync(0xffffffffu, r[0], o);
+            }
+          }
+          if ((lane & (32 / EC - 1)) == 0) csum[q][n + ch] = r[0];
+        }
+        // staging buffer sb: its previous TMA stores (two slices ago) must be done reading
+        uint8_t* stg = stg0 + sb * Cfg::kEpiBuf;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        if (omask & kOutY) {
+#pragma unroll
+          for (int k = 0; k < CH; ++k)
+            *reinterpret_cast<float4*>(stg + srow * RBY + 16 * swz_chunk<RBY>(srow, k)) =
+                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        }
+        if (omask & (kOutHi | kOutLo)) {
+          uint32_t hw[EC / 2], lw[EC / 2];
+#pragma unroll
+          for (int i = 0; i < EC; i += 2) {
+            __half h0, l0, h1, l1;
+            split_f16(v[i] * oscale, h0, l0);
+            split_f16(v[i + 1] * oscale, h1, l1);
+            hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+            lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+          }
+#pragma unroll
+          for (int k = 0; k < EC / 8; ++k) {
+            const int off = srow * RBH + 16 * swz_chunk<RBH>(srow, k);
+            *reinterpret_cast<uint4*>(stg + off) =
+                make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
+            *reinterpret_cast<uint4*>(stg + 32 * RBH + off) =
+                make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
+          }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          const int bx = x0 + 4 * q;
+          if (omask & kOutY) tma_store_3d(&my, stg, n, bx, y0);
+          if (omask & kOutHi) tma_store_3d(&myh, stg, n, bx, y0);
+          if (omask & kOutLo) tma_store_3d(&myl, stg + 32 * RBH, n, bx, y0);
+          bulk_commit_group();
+        }
+        sb ^= 1;
+      }
+      if (colsum) {  // the 8 accumulate warps only (named barrier 1)
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        for (int n = tid - 64; n < BN; n += 256)
+          colsum[(int64_t)tile * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) tmem_dealloc_2sm<Cfg::kTmemCols>(taddr);
+}
+
+// ---------------------------------------------------------------------------
 // 3x3 conv wgrad as a tcgen05 GEMM with both operands MN-major:
 //   D[m = (tap, c)][n = o] = sum_p X[p + d(tap)][c] * G[p][o]
 //   M = 128 (tap, c) rows (4 blocks of 32 channels, each within one tap),
@@ -1027,6 +1340,36 @@ int map_act_blk(CUtensorMap* m, const void* p, bool f16, int C, int W, int H, in
   return N2F_OK;
 }
 
+// NHWC activation viewed as 3-D (C, H, W): a box {32, bh, bw} lands as
+// [x][y][32 channels], i.e. GEMM rows ordered y-fastest (the dy-stage conv).
+int map_act_yx(CUtensorMap* m, const void* p, int C, int W, int H, int bh, int bw) {
+  N2F_TRY(encoder());
+  const cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)H, (cuuint64_t)W};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * C * 2, (cuuint64_t)C * 2};
+  const cuuint32_t box[3] = {32, (cuuint32_t)bh, (cuuint32_t)bw};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(p), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(act yx) failed: %d", (int)r);
+  return N2F_OK;
+}
+
+// K-major weights [N][9 taps][C] (fp16) viewed as 4-D (C, N, dx, dy): a box
+// {32, rows, 3, 1} holds the three dx taps of one dy as [dx][row][32 ch].
+int map_w_taps(CUtensorMap* m, const void* p, int C, int N, int rows) {
+  N2F_TRY(encoder());
+  const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)N, 3, 3};
+  const cuuint64_t strides[3] = {(cuuint64_t)9 * C * 2, (cuuint64_t)C * 2, (cuuint64_t)3 * C * 2};
+  const cuuint32_t box[4] = {32, (cuuint32_t)rows, 3, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(p), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(w taps) failed: %d", (int)r);
+  return N2F_OK;
+}
+
 // Row-major matrix [rows][cols] viewed as 2-D (cols, rows).
 int map_mat(CUtensorMap* m, const void* p, bool f16, int cols, int rows, int bc, int br,
             CUtensorMapSwizzle sw) {
@@ -1052,6 +1395,10 @@ int set_attr_one() {
     N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, F16, 2>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   FwdCfg<BN, F16, 2>::kSmem));
+  }
+  if (F16) {
+    N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  DyCfg<BN>::kSmem));
   }
   N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 FwdCfg<BN, F16, 1>::kSmem));
@@ -1102,9 +1449,39 @@ int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask,
   return N2F_OK;
 }
 
+template <int BN>
+int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
+                   cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kThreadsTc);
+  cfg.dynamicSmemBytes = DyCfg<BN>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my, pl.myh,
+                              pl.myl, pl.omask, pl.oscale, bias, mask, pl.mask_bits, pl.mbits_out,
+                              colsum, pl.unscale, pl.H, pl.W, pl.C, epi));
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
 template <bool F16>
 int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum,
                      int epi, cudaStream_t st) {
+  if (F16 && pl.dy) {
+    switch (pl.N) {
+      case 32: return launch_conv_dy<32>(pl, bias, mask, colsum, epi, st);
+      case 64: return launch_conv_dy<64>(pl, bias, mask, colsum, epi, st);
+      case 128: return launch_conv_dy<128>(pl, bias, mask, colsum, epi, st);
+      case 256: return launch_conv_dy<256>(pl, bias, mask, colsum, epi, st);
+    }
+  }
   const bool two = pl.cs == 2;
   switch (pl.N) {
     case 32: return launch_conv_tc_bn<32, F16, 1>(pl, bias, mask, colsum, epi, st);
@@ -1186,6 +1563,24 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
   // are wrong when set): 1 skip the TMEM drain, 2 skip the MMAs, 4 skip TMA
   const char* dbg = getenv("N2F_TC_DEBUG");
   pl->dbg = dbg ? atoi(dbg) : 0;
+  // FP16, N <= 128: the dy-stage CTA-pair kernel (for N = 256 the per-tap
+  // kernel below measured faster: its 3 x 66 KB dy stages leave no room for
+  // the 16-channel epilogue staging).  N2F_CONV_DY=0/2: never/always.
+  const char* dyenv = getenv("N2F_CONV_DY");
+  const int dymode = dyenv ? atoi(dyenv) : 1;
+  pl->dy = f16 && (dymode == 2 || (dymode == 1 && N <= 128));
+  if (pl->dy) {
+    pl->cs = 2;
+    const int units = ((W + 31) / 32) * ((H + 7) / 8);
+    const int max_units = sm_count() / 2;
+    pl->grid = 2 * (units < max_units ? units : max_units);
+    pl->tiles = 2 * units;
+    N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, 8, 18));
+    N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, 8, 18));
+    N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, N / 2));
+    N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, N / 2));
+    return N2F_OK;
+  }
   // wide layers (N >= 128) run as CTA pairs (cta_group::2, M = 256: each CTA
   // stages its own 128 pixels and half of the weight rows); N2F_TC_CLUSTER=1
   // forces single CTAs
@@ -1215,7 +1610,9 @@ int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any c
 // {EC channels, 32 pixels, 1 row} = one accumulate warp's staging slice.
 int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale) {
   if (!pl->f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
-  const int ec = pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4);
+  // staging slice geometry: dy kernel {EC channels, 4 x, 8 y}, else {EC, 32 x, 1 y}
+  const int ec = pl->dy ? (pl->N == 256 ? 8 : 16) : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
+  const int bw = pl->dy ? 4 : kTW, bh = pl->dy ? 8 : 1;
   auto sw_for = [](int row_bytes) {
     return row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                            : (row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -1228,27 +1625,27 @@ int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscal
   pl->yhi = yhi;
   pl->ylo = ylo;
   if (y) {
-    N2F_TRY(map_act(&pl->my, y, false, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 4)));
+    N2F_TRY(map_act(&pl->my, y, false, pl->N, pl->W, pl->H, ec, bw, bh, sw_for(ec * 4)));
     pl->omask |= kOutY;
   }
   if (pl->f16) {
     if (yhi) {
-      N2F_TRY(map_act(&pl->myh, yhi, true, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 2)));
+      N2F_TRY(map_act(&pl->myh, yhi, true, pl->N, pl->W, pl->H, ec, bw, bh, sw_for(ec * 2)));
       pl->omask |= kOutHi;
     }
     if (ylo) {
-      N2F_TRY(map_act(&pl->myl, ylo, true, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 2)));
+      N2F_TRY(map_act(&pl->myl, ylo, true, pl->N, pl->W, pl->H, ec, bw, bh, sw_for(ec * 2)));
       pl->omask |= kOutLo;
     }
   } else if (ylo) {
-    N2F_TRY(map_act(&pl->myl, ylo, false, pl->N, pl->W, pl->H, ec, kTW, 1, sw_for(ec * 4)));
+    N2F_TRY(map_act(&pl->myl, ylo, false, pl->N, pl->W, pl->H, ec, bw, bh, sw_for(ec * 4)));
     pl->omask |= kOutLo;
   }
   return N2F_OK;
 }
 
 int conv_tc_plan_maskbits(ConvTcPlan* pl, uint32_t* mbits_out, int mask_bits_in) {
-  if ((mbits_out || mask_bits_in) && pl->N < 128)
+  if ((mbits_out || mask_bits_in) && pl->N < (pl->dy ? 64 : 128))
     return fail(N2F_ERR_ARG, "bit-packed ReLU masks need N >= 128 (TMA epilogue), N=%d", pl->N);
   pl->mbits_out = mbits_out;
   pl->mask_bits = mask_bits_in;

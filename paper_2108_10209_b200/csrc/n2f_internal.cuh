@@ -94,6 +94,7 @@ struct ConvTcPlan {
   float unscale;  // 2^-(exp_x + exp_w)
   int dbg;        // profiling experiments only (N2F_TC_DEBUG)
   int cs;         // CTAs per cluster (2: cta_group::2 pair, M = 256)
+  int dy;         // FP16 dy-stage halo kernel (16 x 8 pixel tiles per CTA)
   int tiles;      // 128-pixel tiles = rows of the colsum output
 };
 bool tc_supported(int cin, int cout);
