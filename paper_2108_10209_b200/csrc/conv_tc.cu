@@ -713,9 +713,10 @@ struct DyCfg {
   static constexpr int kTapB = (BN / 2) * 64;        // this CTA's weight rows of one tap
   static constexpr int kStageB = 3 * kTapB;          // the three dx taps
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
-  static constexpr int kEpiCols = BN == 256 ? 8 : 16;
+  static constexpr int kEpiCols = 16;
   static constexpr int kEpiBuf = 32 * kEpiCols * 4;  // one staging buffer (fp32 y, or the fp16 pair)
-  static constexpr int kEpiWarpBytes = 2 * kEpiBuf;  // double-buffered
+  static constexpr int kEpiNBuf = BN == 256 ? 1 : 2;  // double-buffered where smem allows
+  static constexpr int kEpiWarpBytes = kEpiNBuf * kEpiBuf;
   static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
   static constexpr int kMaxStages = (218 * 1024 - kEpiBytes - 1024) / kStageBytes;
   static constexpr int kStages = kMaxStages > 8 ? 8 : kMaxStages;
@@ -954,7 +955,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         // staging buffer sb: its previous TMA stores (two slices ago) must be done reading
         uint8_t* stg = stg0 + sb * Cfg::kEpiBuf;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (lane == 0) {
+          if (Cfg::kEpiNBuf == 2)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         __syncwarp();
         if (omask & kOutY) {
 #pragma unroll
@@ -990,7 +996,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           if (omask & kOutLo) tma_store_3d(&myl, stg + 32 * RBH, n, bx, y0);
           bulk_commit_group();
         }
-        sb ^= 1;
+        if (Cfg::kEpiNBuf == 2) sb ^= 1;
       }
       if (colsum) {  // the 8 accumulate warps only (named barrier 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -1563,11 +1569,10 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
   // are wrong when set): 1 skip the TMEM drain, 2 skip the MMAs, 4 skip TMA
   const char* dbg = getenv("N2F_TC_DEBUG");
   pl->dbg = dbg ? atoi(dbg) : 0;
-  // FP16, N <= 128: the dy-stage CTA-pair kernel (for N = 256 the per-tap
-  // kernel below measured faster: its 3 x 66 KB dy stages leave no room for
-  // the 16-channel epilogue staging).  N2F_CONV_DY=0/2: never/always.
+  // FP16: the dy-stage CTA-pair kernel (N2F_CONV_DY=0 selects the per-tap
+  // kernel below, 1 uses dy only for N <= 128)
   const char* dyenv = getenv("N2F_CONV_DY");
-  const int dymode = dyenv ? atoi(dyenv) : 1;
+  const int dymode = dyenv ? atoi(dyenv) : 2;
   pl->dy = f16 && (dymode == 2 || (dymode == 1 && N <= 128));
   if (pl->dy) {
     pl->cs = 2;
@@ -1611,7 +1616,7 @@ int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any c
 int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale) {
   if (!pl->f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
   // staging slice geometry: dy kernel {EC channels, 4 x, 8 y}, else {EC, 32 x, 1 y}
-  const int ec = pl->dy ? (pl->N == 256 ? 8 : 16) : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
+  const int ec = pl->dy ? 16 : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
   const int bw = pl->dy ? 4 : kTW, bh = pl->dy ? 8 : 1;
   auto sw_for = [](int row_bytes) {
     return row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
