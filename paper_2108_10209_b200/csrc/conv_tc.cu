@@ -1024,22 +1024,45 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 // dW[o][tap][c] (scale removed) and the partials are reduced in fixed order
 // before Adam.  Accumulation is grouped exactly like the forward kernel.
 // ---------------------------------------------------------------------------
-constexpr int kSegW = 32;  // pixels per stage (one image-row segment)
+constexpr int kSegW = 32;  // default pixels per stage (one image-row segment)
+
+// wgrad stage geometry: SEG pixels (K) per stage; A = 4 MN blocks of 32
+// (tap, channel) rows, B = BN / CS / 32 blocks of gradient channels.  Narrow
+// layers take 64-pixel stages (twice the MMA work per TMA instruction) with
+// one stage per accumulation group (K = 64, as the 2 x 32 grouping).
+template <int BN, bool F16, int CS, int SEG>
+struct WgCfg {
+  using P = Prec<F16>;
+  static constexpr int kBlk = SEG * P::kRow;  // bytes of one 32-channel MN block
+  static constexpr int kStageA = 4 * kBlk;
+  static constexpr int kStageB = (BN / CS / 32) * kBlk;
+  static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
+  static constexpr bool kTwoPerSm = CS == 1 && BN <= 64 && SEG == 32;
+  static constexpr int kGroup = SEG == 64 ? 1 : P::kGroup;
+  static constexpr int kMaxStages = (200 * 1024) / kStageBytes;
+  static constexpr int kStages = kTwoPerSm ? 2 * P::kGroup : (kMaxStages > 8 ? 8 : kMaxStages);
+  static constexpr int kSmem = kStages * kStageBytes + 1024;
+  static constexpr int kTmemBudget = kTwoPerSm ? 256 : 512;
+  static constexpr int kBufs = kTmemBudget / BN > 4 ? 4 : kTmemBudget / BN;
+  static constexpr int kTmemCols = kBufs * BN;
+  static constexpr int kHalf = BN / 2;
+  static constexpr int kKSteps = SEG / (F16 ? 16 : 8);  // MMA K steps per stage
+};
 
 // CTA pairs (CS = 2, used when C % 128 == 0 and N >= 128): a cluster owns
 // two consecutive M blocks (cta_group::2 MMA, M = 256); each CTA stages its
 // own activation blocks and half of the gradient channels.
-template <int BN, bool F16, int CS>
+template <int BN, bool F16, int CS, int SEG>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_wgrad3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                   const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mgl,
                   float* __restrict__ part, float unscale, int H, int W, int C, int nsplit, int xblk) {
-  using Cfg = FwdCfg<BN, F16, CS>;  // A = 4 blocks of 32 px rows, B = BN/CS/32 blocks
+  using Cfg = WgCfg<BN, F16, CS, SEG>;
   using P = Prec<F16>;
-  constexpr int kBlk = kSegW * P::kRow;  // bytes of one 32-channel MN block
+  constexpr int kBlk = Cfg::kBlk;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
-  constexpr int G = P::kGroup;
+  constexpr int G = Cfg::kGroup;
   constexpr int NB = Cfg::kBufs;  // TMEM group buffers (4 for N <= 128: the short
                                   // narrow-layer groups need a deep hand-off queue)
   extern __shared__ uint8_t smem_raw[];
@@ -1055,7 +1078,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const bool ghost = m0 >= K9;
   const int ml = ghost ? 0 : m0;
   const int split = blockIdx.y;
-  const int segs_x = (W + kSegW - 1) / kSegW;
+  const int segs_x = (W + SEG - 1) / SEG;
   const int nseg = segs_x * H;
   const int s0 = (int)((int64_t)nseg * split / nsplit), s1 = (int)((int64_t)nseg * (split + 1) / nsplit);
   const int KB = s1 - s0;
@@ -1112,7 +1135,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       pw += c1 - c0;
 #endif
       const int seg = s0 + kb;
-      const int y0 = seg / segs_x, x0 = (seg - y0 * segs_x) * kSegW;
+      const int y0 = seg / segs_x, x0 = (seg - y0 * segs_x) * SEG;
       uint8_t* st = base + s * Cfg::kStageBytes;
       if (elect_one_sync()) {
         if (CS == 1) {
@@ -1122,12 +1145,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             const int ky = tap / 3, kx = tap - 3 * ky;
             tma_load_4d(st, &mx, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
             tma_load_4d(st + Cfg::kStageA, &mxl, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
-          } else {
-            for (int j = 0; j < nblk_a; ++j) {
+          } else {  // one 4-D box per tap (C / 32 blocks of it)
+            const int bpt = C / 32;
+            for (int j = 0; j < nblk_a; j += bpt) {
               const int mm = ml + 32 * j, tap = mm / C, c = mm - tap * C;
               const int ky = tap / 3, kx = tap - 3 * ky;
-              tma_load_3d(st + j * kBlk, &mx, &full[s], c, x0 + kx - 1, y0 + ky - 1);
-              tma_load_3d(st + Cfg::kStageA + j * kBlk, &mxl, &full[s], c, x0 + kx - 1, y0 + ky - 1);
+              tma_load_4d(st + j * kBlk, &mx, &full[s], 0, x0 + kx - 1, c / 32, y0 + ky - 1);
+              tma_load_4d(st + Cfg::kStageA + j * kBlk, &mxl, &full[s], 0, x0 + kx - 1, c / 32,
+                          y0 + ky - 1);
             }
           }
           tma_load_4d(st + 2 * Cfg::kStageA, &mg, &full[s], 0, x0, 0, y0);
@@ -1160,7 +1185,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       constexpr uint32_t idesc = P::idesc(128 * CS, BN, true, true);
       constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
                          kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
-      const uint64_t desc0 = P::mndesc(smem_u32(base));
+      // MN-major: LBO = the stride of the 32-element MN blocks (SEG pixel rows)
+      const uint64_t desc0 = sw128_desc(smem_u32(base), kBlk, 512, P::kLayMN);
       int it = 0;
 #if N2F_TC_TRACE
       long long we_ = 0, wf_ = 0, is_ = 0, t0_ = clock64();
@@ -1193,7 +1219,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           for (int j = 0; j < G; ++j) {
             if (j < ng) {
 #pragma unroll
-              for (int k = 0; k < P::kKSteps; ++k) {
+              for (int k = 0; k < Cfg::kKSteps; ++k) {
                 const uint64_t a = ah[j] + 64 * k;
                 P::template mma<CS>(d, a, a + kBl, idesc, (j | k) != 0);
                 P::template mma<CS>(d, a + kAl, a + kBh, idesc, 1);
@@ -1204,7 +1230,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           for (int j = 0; j < G; ++j) {
             if (j < ng) {
 #pragma unroll
-              for (int k = 0; k < P::kKSteps; ++k) {
+              for (int k = 0; k < Cfg::kKSteps; ++k) {
                 const uint64_t a = ah[j] + 64 * k;
                 P::template mma<CS>(d, a, a + kBh, idesc, 1);
               }
@@ -1406,12 +1432,18 @@ int set_attr_one() {
     N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   DyCfg<BN>::kSmem));
   }
-  N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FwdCfg<BN, F16, 1>::kSmem));
-  if (BN >= 128) {
-    N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 2>,
+  N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1, 32>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                WgCfg<BN, F16, 1, 32>::kSmem));
+  if (F16) {
+    N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1, 64>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  FwdCfg<BN, F16, 2>::kSmem));
+                                  WgCfg<BN, F16, 1, 64>::kSmem));
+  }
+  if (BN >= 128) {
+    N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 2, 32>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  WgCfg<BN, F16, 2, 32>::kSmem));
   }
   return N2F_OK;
 }
@@ -1502,12 +1534,12 @@ int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, 
   return fail(N2F_ERR_ARG, "conv_tc_launch: N=%d", pl.N);
 }
 
-template <int BN, bool F16, int CS>
+template <int BN, bool F16, int CS, int SEG>
 int launch_wgrad_tc_bn(const WgradTcPlan& pl, float* part, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.gridx, pl.nsplit);
   cfg.blockDim = dim3(kThreadsTc);
-  cfg.dynamicSmemBytes = FwdCfg<BN, F16, CS>::kSmem;
+  cfg.dynamicSmemBytes = WgCfg<BN, F16, CS, SEG>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1516,24 +1548,29 @@ int launch_wgrad_tc_bn(const WgradTcPlan& pl, float* part, cudaStream_t st) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_wgrad3x3_tc<BN, F16, CS>, pl.mx, pl.mxl, pl.mg, pl.mgl, part,
-                              pl.unscale, pl.H, pl.W, pl.C, pl.nsplit, pl.xblk));
+  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_wgrad3x3_tc<BN, F16, CS, SEG>, pl.mx, pl.mxl, pl.mg, pl.mgl,
+                              part, pl.unscale, pl.H, pl.W, pl.C, pl.nsplit, pl.xblk));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
 
+template <int BN, bool F16>
+int launch_wgrad_tc_n(const WgradTcPlan& pl, float* part, cudaStream_t st) {
+  if (pl.cs == 2) {
+    if constexpr (BN >= 128) return launch_wgrad_tc_bn<BN, F16, 2, 32>(pl, part, st);
+    return fail(N2F_ERR_ARG, "wgrad pair with N=%d", BN);
+  }
+  if (F16 && pl.seg == 64) return launch_wgrad_tc_bn<BN, F16, 1, F16 ? 64 : 32>(pl, part, st);
+  return launch_wgrad_tc_bn<BN, F16, 1, 32>(pl, part, st);
+}
+
 template <bool F16>
 int launch_wgrad_tc_p(const WgradTcPlan& pl, float* part, cudaStream_t st) {
-  const bool two = pl.cs == 2;
   switch (pl.N) {
-    case 32: return launch_wgrad_tc_bn<32, F16, 1>(pl, part, st);
-    case 64: return launch_wgrad_tc_bn<64, F16, 1>(pl, part, st);
-    case 128:
-      return two ? launch_wgrad_tc_bn<128, F16, 2>(pl, part, st)
-                 : launch_wgrad_tc_bn<128, F16, 1>(pl, part, st);
-    case 256:
-      return two ? launch_wgrad_tc_bn<256, F16, 2>(pl, part, st)
-                 : launch_wgrad_tc_bn<256, F16, 1>(pl, part, st);
+    case 32: return launch_wgrad_tc_n<32, F16>(pl, part, st);
+    case 64: return launch_wgrad_tc_n<64, F16>(pl, part, st);
+    case 128: return launch_wgrad_tc_n<128, F16>(pl, part, st);
+    case 256: return launch_wgrad_tc_n<256, F16>(pl, part, st);
   }
   return fail(N2F_ERR_ARG, "wgrad_tc_launch: N=%d", pl.N);
 }
@@ -1706,15 +1743,15 @@ int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H
   // share a tap when C % 128 == 0 (else one box per block), the gradient's
   // N / 32 blocks always come as one box
   pl->xblk = C % 128 == 0;
-  if (pl->xblk) {
-    N2F_TRY(map_act_blk(&pl->mx, x.hi, f16, C, W, H, kSegW, 4, sw));
-    N2F_TRY(map_act_blk(&pl->mxl, x.lo, f16, C, W, H, kSegW, 4, sw));
-  } else {
-    N2F_TRY(map_act(&pl->mx, x.hi, f16, C, W, H, 32, kSegW, 1, sw));
-    N2F_TRY(map_act(&pl->mxl, x.lo, f16, C, W, H, 32, kSegW, 1, sw));
-  }
-  N2F_TRY(map_act_blk(&pl->mg, g.hi, f16, N, W, H, kSegW, N / 32 / pl->cs, sw));
-  N2F_TRY(map_act_blk(&pl->mgl, g.lo, f16, N, W, H, kSegW, N / 32 / pl->cs, sw));
+  // FP16 single-CTA wgrads take 64-pixel stages (N2F_WGRAD_SEG overrides)
+  const char* segenv = getenv("N2F_WGRAD_SEG");
+  pl->seg = (f16 && pl->cs == 1) ? (segenv ? atoi(segenv) : 64) : kSegW;
+  if (pl->seg != 32 && pl->seg != 64) pl->seg = kSegW;
+  const int bpt = pl->xblk ? 4 : C / 32;  // activation blocks per box (one tap)
+  N2F_TRY(map_act_blk(&pl->mx, x.hi, f16, C, W, H, pl->seg, bpt, sw));
+  N2F_TRY(map_act_blk(&pl->mxl, x.lo, f16, C, W, H, pl->seg, bpt, sw));
+  N2F_TRY(map_act_blk(&pl->mg, g.hi, f16, N, W, H, pl->seg, N / 32 / pl->cs, sw));
+  N2F_TRY(map_act_blk(&pl->mgl, g.lo, f16, N, W, H, pl->seg, N / 32 / pl->cs, sw));
   return N2F_OK;
 }
 

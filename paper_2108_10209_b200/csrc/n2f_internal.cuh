@@ -119,6 +119,7 @@ struct WgradTcPlan {
   int xblk;   // activation blocks of an M block loaded as one 4-D box (C % 128 == 0)
   int cs;     // CTAs per cluster (2: pairs of M blocks, cta_group::2)
   int gridx;  // CTAs along M (mblocks rounded up to a multiple of cs)
+  int seg;    // pixels per K stage (32, or 64 for the FP16 single-CTA kernels)
 };
 int wgrad_tc_nsplit(int cin, int cout, int H, int W);
 int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H, int W, int C,
