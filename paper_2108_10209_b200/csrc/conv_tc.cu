@@ -212,6 +212,7 @@ __device__ __forceinline__ void store_pair4(const ConvOut& o, int64_t idx, float
 // RB bytes (the SWIZZLE_32B / SWIZZLE_64B patterns; none for 16-byte rows).
 template <int RB>
 __device__ __forceinline__ int swz_chunk(int row, int k) {
+  if (RB == 128) return k ^ (row & 7);
   if (RB == 64) return k ^ ((row >> 1) & 3);
   if (RB == 32) return k ^ ((row >> 2) & 1);
   return k;
@@ -713,9 +714,11 @@ struct DyCfg {
   static constexpr int kTapB = (BN / 2) * 64;        // this CTA's weight rows of one tap
   static constexpr int kStageB = 3 * kTapB;          // the three dx taps
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
-  static constexpr int kEpiCols = 16;
+  // staging slices: 32 channels (one fence + TMA issue per 32) where smem
+  // allows, 16 for BN = 256 (whose three 66 KB dy stages fill the rest)
+  static constexpr int kEpiCols = BN == 256 ? 16 : (BN / 2 < 32 ? BN / 2 : 32);
   static constexpr int kEpiBuf = 32 * kEpiCols * 4;  // one staging buffer (fp32 y, or the fp16 pair)
-  static constexpr int kEpiNBuf = BN == 256 ? 1 : 2;  // double-buffered where smem allows
+  static constexpr int kEpiNBuf = 1;
   static constexpr int kEpiWarpBytes = kEpiNBuf * kEpiBuf;
   static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
   static constexpr int kMaxStages = (218 * 1024 - kEpiBytes - 1024) / kStageBytes;
@@ -731,10 +734,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv3x3_dy(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
                  const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
-                 const __grid_constant__ CUtensorMap myl, int omask, float oscale,
-                 const float* __restrict__ bias, const void* __restrict__ mask, int mask_bits,
-                 uint32_t* __restrict__ mbits_out, float* __restrict__ colsum, float unscale, int H,
-                 int W, int C, int epi) {
+                 const __grid_constant__ CUtensorMap myl, int omask, float oscale, ConvOut out,
+                 int direct, const float* __restrict__ bias, const void* __restrict__ mask,
+                 int mask_bits, uint32_t* __restrict__ mbits_out, float* __restrict__ colsum,
+                 float unscale, int H, int W, int C, int epi) {
   using Cfg = DyCfg<BN>;
   using P = Prec<true>;
   constexpr int S = Cfg::kStages;
@@ -744,6 +747,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __shared__ uint64_t full[S], empty[S], tfull[NB], tempty[NB];
   __shared__ uint32_t tslot;
   __shared__ __align__(16) float csum[4][BN];
+  __shared__ __align__(16) float sbias[BN];  // the bias, staged once (L1 is mostly smem here)
   uint8_t* base = align1024(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_ctarank();
@@ -808,11 +812,24 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                          kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4, kTap = Cfg::kTapB >> 4;
       const uint64_t desc0 = P::kdesc(smem_u32(base));
       int gg = 0;
+#if N2F_TC_TRACE
+      long long we_ = 0, wf_ = 0, t0_ = clock64();
+#endif
       for (int ut = cid; ut < nunits; ut += ncl) {
         for (int kb = 0; kb < KB; ++kb, ++gg) {
           const int s = gg % S, b = gg % NB;
+#if N2F_TC_TRACE
+          const long long c0 = clock64();
+#endif
           if (gg >= NB) mbar_wait(&tempty[b], ((gg / NB) - 1) & 1);
+#if N2F_TC_TRACE
+          const long long c1 = clock64();
+#endif
           mbar_wait(&full[s], (gg / S) & 1);
+#if N2F_TC_TRACE
+          we_ += c1 - c0;
+          wf_ += clock64() - c1;
+#endif
           tc_fence_after();
           if (elect_one_sync()) {
             const uint32_t d = taddr + b * BN;
@@ -840,6 +857,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           __syncwarp();
         }
       }
+#if N2F_TC_TRACE
+      if (lane == 0 && blockIdx.x == 0)
+        printf("[dy mma] C %d BN %d units/cta %d groups %d total %lld wait_tempty %lld wait_full %lld\n",
+               C, BN, (nunits + ncl - 1) / ncl, gg, clock64() - t0_, we_, wf_);
+#endif
     }
   } else {
     // ---- group accumulation in registers (round-to-nearest fp32 adds)
@@ -847,6 +869,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     const int half = (warp - 2) >> 2;  // column half
     const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * HALF;
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+#if N2F_TC_TRACE
+    long long tw = 0, td = 0, te = 0, twr = 0, tcomp = 0, tstg = 0, tiss = 0, t_0 = clock64();
+#endif
+    if (epi == kEpiBiasRelu || epi == kEpiBias) {
+      for (int n = tid - 64; n < BN; n += 256) sbias[n] = bias[n];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
     // this lane's pixel: GEMM row m = 32 q + lane = 8 * xl + yl
     const int xl = 4 * q + (lane >> 3), yl = lane & 7;
     constexpr int EC = DyCfg<BN>::kEpiCols, CH = EC / 4;
@@ -862,13 +891,26 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
       for (int kb = 0; kb < KB; ++kb, ++gg) {
         const int b = gg % NB;
+#if N2F_TC_TRACE
+        const long long c0 = clock64();
+#endif
         mbar_wait(&tfull[b], (gg / NB) & 1);
+#if N2F_TC_TRACE
+        const long long c1 = clock64();
+        tw += c1 - c0;
+#endif
         tc_fence_after();
         drain_add<HALF>(lane_base + b * BN, acc);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty0 + 8u * b);
+#if N2F_TC_TRACE
+        td += clock64() - c1;
+#endif
       }
+#if N2F_TC_TRACE
+      const long long ce = clock64();
+#endif
 
       // ---- epilogue (see k_conv3x3_tc): scale removal, bias+ReLU or the ReLU
       // mask, column sums, bit masks, staging in the TMA swizzle layout and
@@ -887,6 +929,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
       uint32_t ob = 0;
 #pragma unroll
       for (int c0 = 0; c0 < HALF; c0 += EC) {
+#if N2F_TC_TRACE
+        const long long cs0 = clock64();
+#endif
         const int n = n0 + c0;
         float v[EC];
 #pragma unroll
@@ -894,7 +939,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         if (epi == kEpiBiasRelu || epi == kEpiBias) {
 #pragma unroll
           for (int k = 0; k < CH; ++k) {
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n) + k);
+            const float4 bb = *reinterpret_cast<const float4*>(sbias + n + 4 * k);
             v[4 * k] += bb.x; v[4 * k + 1] += bb.y; v[4 * k + 2] += bb.z; v[4 * k + 3] += bb.w;
           }
           if (epi == kEpiBiasRelu) {
@@ -953,8 +998,42 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           }
           if ((lane & (32 / EC - 1)) == 0) csum[q][n + ch] = r[0];
         }
+        if (direct) {  // direct stores from registers: 16 channels of this lane's pixel
+          if (valid) {
+            const int64_t idx = pix * BN + n;
+            if (out.y) {
+#pragma unroll
+              for (int k = 0; k < CH; ++k)
+                *reinterpret_cast<float4*>(out.y + idx + 4 * k) =
+                    make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            }
+            if (out.yhi) {
+              uint32_t hw[EC / 2], lw[EC / 2];
+#pragma unroll
+              for (int i = 0; i < EC; i += 2) {
+                __half h0, l0, h1, l1;
+                split_f16(v[i] * oscale, h0, l0);
+                split_f16(v[i + 1] * oscale, h1, l1);
+                hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+                lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+              }
+#pragma unroll
+              for (int k = 0; k < EC / 8; ++k) {
+                *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out.yhi) + idx + 8 * k) =
+                    make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
+                *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out.ylo) + idx + 8 * k) =
+                    make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
+              }
+            }
+          }
+          continue;
+        }
         // staging buffer sb: its previous TMA stores (two slices ago) must be done reading
         uint8_t* stg = stg0 + sb * Cfg::kEpiBuf;
+#if N2F_TC_TRACE
+        const long long cw = clock64();
+        tcomp += cw - cs0;
+#endif
         if (lane == 0) {
           if (Cfg::kEpiNBuf == 2)
             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -962,6 +1041,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
         __syncwarp();
+#if N2F_TC_TRACE
+        twr += clock64() - cw;
+#endif
         if (omask & kOutY) {
 #pragma unroll
           for (int k = 0; k < CH; ++k)
@@ -989,7 +1071,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         }
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) {
+#if N2F_TC_TRACE
+        const long long cf = clock64();
+        tstg += cf - cw;
+#endif
+        if (elect_one_sync()) {
           const int bx = x0 + 4 * q;
           if (omask & kOutY) tma_store_3d(&my, stg, n, bx, y0);
           if (omask & kOutHi) tma_store_3d(&myh, stg, n, bx, y0);
@@ -997,6 +1083,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           bulk_commit_group();
         }
         if (Cfg::kEpiNBuf == 2) sb ^= 1;
+#if N2F_TC_TRACE
+        __syncwarp();
+        tiss += clock64() - cf;
+#endif
       }
       if (colsum) {  // the 8 accumulate warps only (named barrier 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -1004,7 +1094,16 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           colsum[(int64_t)tile * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
         asm volatile("bar.sync 1, 256;" ::: "memory");
       }
+#if N2F_TC_TRACE
+      te += clock64() - ce;
+#endif
     }
+#if N2F_TC_TRACE
+    if (lane == 0 && blockIdx.x == 0 && (warp == 2 || warp == 9))
+      printf("[dy acc w%d] C %d BN %d total %lld wait_tfull %lld drain %lld epilogue %lld (compute %lld "
+             "wait_read %lld stage+fence %lld issue %lld)\n",
+             warp, C, BN, clock64() - t_0, tw, td, te, tcomp, twr, tstg - twr, tiss);
+#endif
     if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
@@ -1502,9 +1601,14 @@ int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, fl
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static const int direct = [] {
+    const char* e = getenv("N2F_DY_DIRECT");
+    return e ? atoi(e) : 0;
+  }();
   N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my, pl.myh,
-                              pl.myl, pl.omask, pl.oscale, bias, mask, pl.mask_bits, pl.mbits_out,
-                              colsum, pl.unscale, pl.H, pl.W, pl.C, epi));
+                              pl.myl, pl.omask, pl.oscale, ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale},
+                              direct, bias, mask, pl.mask_bits, pl.mbits_out, colsum, pl.unscale,
+                              pl.H, pl.W, pl.C, epi));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
@@ -1653,11 +1757,13 @@ int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any c
 int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale) {
   if (!pl->f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
   // staging slice geometry: dy kernel {EC channels, 4 x, 8 y}, else {EC, 32 x, 1 y}
-  const int ec = pl->dy ? 16 : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
+  const int ec = pl->dy ? (pl->N == 256 ? 16 : (pl->N / 2 < 32 ? pl->N / 2 : 32))
+                        : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
   const int bw = pl->dy ? 4 : kTW, bh = pl->dy ? 8 : 1;
   auto sw_for = [](int row_bytes) {
-    return row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                           : (row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
+    return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+           : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+           : (row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
   };
   pl->omask = 0;
   pl->oscale = oscale;
