@@ -25,8 +25,10 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include "loss_dev.cuh"
 #include "n2f_internal.cuh"
 #include "tc_common.cuh"
+#include "train.cuh"
 
 // Build with -DN2F_TC_TRACE=1 for per-warp cycle accounting (N2F_TC_DEBUG=64).
 #ifndef N2F_TC_TRACE
@@ -729,7 +731,9 @@ struct DyCfg {
   static constexpr int kHalf = BN / 2;
 };
 
-template <int BN>
+// HEAD: 0 plain conv; 1 / 2 (BN = 256 only) = the L9 training / validation
+// head fused into the epilogue (see HeadTrainArgs / HeadValArgs).
+template <int BN, int HEAD>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_conv3x3_dy(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
@@ -737,7 +741,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
                  const __grid_constant__ CUtensorMap myl, int omask, float oscale, ConvOut out,
                  int direct, const float* __restrict__ bias, const void* __restrict__ mask,
                  int mask_bits, uint32_t* __restrict__ mbits_out, float* __restrict__ colsum,
-                 float unscale, int H, int W, int C, int epi) {
+                 float unscale, int H, int W, int C, int epi, HeadTrainArgs ht, HeadValArgs hv) {
   using Cfg = DyCfg<BN>;
   using P = Prec<true>;
   constexpr int S = Cfg::kStages;
@@ -748,6 +752,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __shared__ uint32_t tslot;
   __shared__ __align__(16) float csum[4][BN];
   __shared__ __align__(16) float sbias[BN];  // the bias, staged once (L1 is mostly smem here)
+  __shared__ float zp[HEAD ? 2 : 1][HEAD ? 128 : 1];  // fused head: per-half partial dots
+  __shared__ float sw9[HEAD ? BN : 1];                 // fused head: the 1x1 weights
+  __shared__ double hred_d[4];
+  __shared__ float hred_f[4];
   uint8_t* base = align1024(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_ctarank();
@@ -757,6 +765,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   const int KB = 3 * (C / 32);  // stages (= groups) per tile
 
   if (tid == 0) {
+    if (HEAD == 1 && blockIdx.x == 0 && ht.step_counter) *ht.step_counter += 1;  // Adam t
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -873,7 +882,10 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     long long tw = 0, td = 0, te = 0, twr = 0, tcomp = 0, tstg = 0, tiss = 0, t_0 = clock64();
 #endif
     if (epi == kEpiBiasRelu || epi == kEpiBias) {
-      for (int n = tid - 64; n < BN; n += 256) sbias[n] = bias[n];
+      for (int n = tid - 64; n < BN; n += 256) {
+        sbias[n] = bias[n];
+        if (HEAD) sw9[n] = (HEAD == 1 ? ht.w9 : hv.w9)[n];
+      }
       asm volatile("bar.sync 1, 256;" ::: "memory");
     }
     // this lane's pixel: GEMM row m = 32 q + lane = 8 * xl + yl
@@ -927,6 +939,130 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
           mw[k] = valid ? __ldg(reinterpret_cast<const uint32_t*>(mask) + pix * WPP + n0 / 32 + k) : 0u;
       }
       uint32_t ob = 0;
+      if constexpr (HEAD != 0) {
+        // ---- fused L9 head.  The L8 activation (fp32, the regular epilogue's
+        // rounding: scale, bias add, ReLU) replaces acc in place; the two
+        // column halves exchange their partial dots with w9 through smem.
+        const float* w9 = sw9;
+        float pd = 0.f;
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) {
+          const float a = fmaxf(__fadd_rn(__fmul_rn(acc[j], unscale), sbias[n0 + j]), 0.f);
+          acc[j] = a;
+          pd = fmaf(a, w9[n0 + j], pd);
+        }
+        const int m = 32 * q + lane;
+        zp[half][m] = pd;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const float z = __fadd_rn(__fadd_rn(zp[0][m], zp[1][m]), __ldg(HEAD == 1 ? ht.b9 : hv.b9));
+        if constexpr (HEAD == 2) {
+          double se = 0.0;
+          if (half == 0 && valid) {
+            const float o = clip_unit(sigmoid_ref(z));
+            hv.ring[(int64_t)(hv.st->epoch % hv.window) * ((int64_t)H * W) + pix] = o;
+            const double d = (double)o - (double)__ldg(hv.norm + pix);
+            se = d * d;
+          }
+          if (half == 0) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+            if (lane == 0) hred_d[q] = se;
+          }
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (tid == 64) hv.part_se[tile] = (hred_d[0] + hred_d[1]) + (hred_d[2] + hred_d[3]);
+        } else {
+          float elem = 0.f, dz = 0.f;
+          if (valid) dz = loss_grad(z, __ldg(ht.tgt + pix), ht.loss, ht.nf, ht.two_over_n, &elem);
+          if (half == 0 && valid) ht.zout[pix] = z;
+#pragma unroll
+          for (int c0 = 0; c0 < HALF; c0 += EC) {
+            const int n = n0 + c0;
+            float g[EC], wa[EC], gk[EC];
+#pragma unroll
+            for (int i = 0; i < EC; ++i) {
+              const float a = acc[c0 + i];
+              g[i] = (valid && a > 0.f) ? __fmul_rn(w9[n + i], dz) : 0.f;  // head backward
+              gk[i] = g[i];
+              wa[i] = valid ? __fmul_rn(dz, a) : 0.f;  // dW9 terms
+            }
+            // transpose-reduce both column sums (bias grad of L8, dW9 partial)
+            int ch = 0;
+#pragma unroll
+            for (int o = 16, cnt = EC; o >= 1; o >>= 1) {
+              if (cnt > 1) {
+                const int hcnt = cnt / 2;
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < EC / 2; ++i) {
+                  if (i < hcnt) {
+                    const float s1 = up ? g[i] : g[i + hcnt], k1 = up ? g[i + hcnt] : g[i];
+                    const float s2 = up ? wa[i] : wa[i + hcnt], k2 = up ? wa[i + hcnt] : wa[i];
+                    g[i] = k1 + __shfl_xor_sync(0xffffffffu, s1, o);
+                    wa[i] = k2 + __shfl_xor_sync(0xffffffffu, s2, o);
+                  }
+                }
+                ch += up ? hcnt : 0;
+                cnt = hcnt;
+              } else {
+                g[0] += __shfl_xor_sync(0xffffffffu, g[0], o);
+                wa[0] += __shfl_xor_sync(0xffffffffu, wa[0], o);
+              }
+            }
+            if ((lane & (32 / EC - 1)) == 0) {
+              if (colsum) csum[q][n + ch] = g[0];
+              ht.part_w9[((int64_t)tile * 4 + q) * BN + n + ch] = wa[0];
+            }
+            // stage this lane's g pair (gk: the values before the reduction)
+            uint32_t hw[EC / 2], lw[EC / 2];
+#pragma unroll
+            for (int i = 0; i < EC; i += 2) {
+              __half h0, l0, h1, l1;
+              split_f16(__fmul_rn(gk[i], oscale), h0, l0);
+              split_f16(__fmul_rn(gk[i + 1], oscale), h1, l1);
+              hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+              lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+            }
+            uint8_t* stg = stg0;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < EC / 8; ++k) {
+              const int off = srow * RBH + 16 * swz_chunk<RBH>(srow, k);
+              *reinterpret_cast<uint4*>(stg + off) =
+                  make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
+              *reinterpret_cast<uint4*>(stg + 32 * RBH + off) =
+                  make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (elect_one_sync()) {
+              const int bx = x0 + 4 * q;
+              tma_store_3d(&myh, stg, n, bx, y0);
+              tma_store_3d(&myl, stg + 32 * RBH, n, bx, y0);
+              bulk_commit_group();
+            }
+          }
+          // per-tile db9 / loss partials over the tile's valid pixels (half 0)
+          if (half == 0) {
+            float sdz = dz;
+            double sl = (double)elem;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              sdz += __shfl_xor_sync(0xffffffffu, sdz, o);
+              sl += __shfl_xor_sync(0xffffffffu, sl, o);
+            }
+            if (lane == 0) {
+              hred_f[q] = sdz;
+              hred_d[q] = sl;
+            }
+          }
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (tid == 64) {
+            ht.part_b9[tile] = (hred_f[0] + hred_f[1]) + (hred_f[2] + hred_f[3]);
+            ht.part_loss[tile] = (hred_d[0] + hred_d[1]) + (hred_d[2] + hred_d[3]);
+          }
+        }
+      } else {
 #pragma unroll
       for (int c0 = 0; c0 < HALF; c0 += EC) {
 #if N2F_TC_TRACE
@@ -1088,6 +1224,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         tiss += clock64() - cf;
 #endif
       }
+      }  // HEAD
       if (colsum) {  // the 8 accumulate warps only (named barrier 1)
         asm volatile("bar.sync 1, 256;" ::: "memory");
         for (int n = tid - 64; n < BN; n += 256)
@@ -1528,8 +1665,14 @@ int set_attr_one() {
                                   FwdCfg<BN, F16, 2>::kSmem));
   }
   if (F16) {
-    N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<BN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   DyCfg<BN>::kSmem));
+    if (BN == 256) {
+      N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<256, 1>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, DyCfg<256>::kSmem));
+      N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<256, 2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, DyCfg<256>::kSmem));
+    }
   }
   N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1, 32>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1586,9 +1729,9 @@ int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask,
   return N2F_OK;
 }
 
-template <int BN>
+template <int BN, int HEAD>
 int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
-                   cudaStream_t st) {
+                   const HeadTrainArgs& ht, const HeadValArgs& hv, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(kThreadsTc);
@@ -1605,10 +1748,11 @@ int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, fl
     const char* e = getenv("N2F_DY_DIRECT");
     return e ? atoi(e) : 0;
   }();
-  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my, pl.myh,
-                              pl.myl, pl.omask, pl.oscale, ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale},
-                              direct, bias, mask, pl.mask_bits, pl.mbits_out, colsum, pl.unscale,
-                              pl.H, pl.W, pl.C, epi));
+  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN, HEAD>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
+                              pl.myh, pl.myl, pl.omask, pl.oscale,
+                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, HEAD ? 0 : direct, bias, mask,
+                              pl.mask_bits, pl.mbits_out, colsum, pl.unscale, pl.H, pl.W, pl.C, epi,
+                              ht, hv));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
@@ -1617,11 +1761,13 @@ template <bool F16>
 int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum,
                      int epi, cudaStream_t st) {
   if (F16 && pl.dy) {
+    const HeadTrainArgs ht{};
+    const HeadValArgs hv{};
     switch (pl.N) {
-      case 32: return launch_conv_dy<32>(pl, bias, mask, colsum, epi, st);
-      case 64: return launch_conv_dy<64>(pl, bias, mask, colsum, epi, st);
-      case 128: return launch_conv_dy<128>(pl, bias, mask, colsum, epi, st);
-      case 256: return launch_conv_dy<256>(pl, bias, mask, colsum, epi, st);
+      case 32: return launch_conv_dy<32, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
+      case 64: return launch_conv_dy<64, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
+      case 128: return launch_conv_dy<128, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
+      case 256: return launch_conv_dy<256, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
     }
   }
   const bool two = pl.cs == 2;
@@ -1798,6 +1944,19 @@ int conv_tc_plan_maskbits(ConvTcPlan* pl, uint32_t* mbits_out, int mask_bits_in)
   pl->mbits_out = mbits_out;
   pl->mask_bits = mask_bits_in;
   return N2F_OK;
+}
+
+int conv_tc_launch_head_train(const ConvTcPlan& pl, const float* bias, float* colsum,
+                              const HeadTrainArgs& ht, cudaStream_t st) {
+  if (!pl.dy || pl.N != 256 || !(pl.omask & kOutHi) || !(pl.omask & kOutLo))
+    return fail(N2F_ERR_ARG, "fused training head needs the FP16 dy plan of L8 with a pair output");
+  return launch_conv_dy<256, 1>(pl, bias, nullptr, colsum, kEpiBiasRelu, ht, HeadValArgs{}, st);
+}
+
+int conv_tc_launch_head_val(const ConvTcPlan& pl, const float* bias, const HeadValArgs& hv,
+                            cudaStream_t st) {
+  if (!pl.dy || pl.N != 256) return fail(N2F_ERR_ARG, "fused validation head needs the FP16 dy plan of L8");
+  return launch_conv_dy<256, 2>(pl, bias, nullptr, nullptr, kEpiBiasRelu, HeadTrainArgs{}, hv, st);
 }
 
 int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,

@@ -215,15 +215,21 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
     PROF(kPFirst, 0, conv_flop(P, 0),
          conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1, c->act_lo[0]));
   }
-  for (int li = 1; li < 8; ++li)
+  for (int li = 1; li < (f16 ? 7 : 8); ++li)
     PROF(kPFwd, li, conv_flop(P, li),
          conv_tc_launch(c->fwd_plan[sc][li], B_(c, li), nullptr, nullptr, kEpiBiasRelu, st));
-  PROF(kPHead, 8, 6.0 * P * kMaxC,
-       launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, f16 ? nullptr : c->gA, c->part_w[8],
-                         c->part_b[8], c->part_loss + (int64_t)k * c->nblk_head, c->z, P,
-                         c->nblk_head, c->cfg.loss, c->step_counter, st,
-                         f16 ? nullptr : c->gA_lo, c->part_b[7], f16 ? c->g16[0][0] : nullptr,
-                         f16 ? c->g16[0][1] : nullptr, sg));
+  if (f16) {  // L8 forward with the L9 head, loss and head backward fused
+    HeadTrainArgs ht{W_(c, 8), B_(c, 8), tgt, c->z, c->part_w[8], c->part_b[8],
+                     c->part_loss + (int64_t)k * c->nblk_head, c->step_counter, c->cfg.loss,
+                     (float)P, (float)(2.0 / (double)P)};
+    PROF(kPFwd, 7, conv_flop(P, 7) + 6.0 * P * kMaxC,
+         conv_tc_launch_head_train(c->fwd_plan[sc][7], B_(c, 7), c->part_b[7], ht, st));
+  } else {
+    PROF(kPHead, 8, 6.0 * P * kMaxC,
+         launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, c->gA, c->part_w[8], c->part_b[8],
+                           c->part_loss + (int64_t)k * c->nblk_head, c->z, P, c->nblk_head,
+                           c->cfg.loss, c->step_counter, st, c->gA_lo, c->part_b[7]));
+  }
   float* g = c->gA;
   float* gn = c->gB;
   for (int li = 7; li >= 1; --li) {
@@ -256,13 +262,19 @@ int enqueue_validate_tc(n2f_ctx* c) {
          conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1,
                          c->vA_lo));
   }
-  for (int li = 1; li < 8; ++li)
+  for (int li = 1; li < (f16 ? 7 : 8); ++li)
     PROF(kPValConv, li, conv_flop(c->Pv, li),
          conv_tc_launch(c->val_plan[li], B_(c, li), nullptr, nullptr, kEpiBiasRelu, st));
-  // layer 7 (odd) wrote vB
-  PROF(kPHeadVal, 8, 2.0 * c->Pv * kMaxC,
-       launch_head_val(c->vB, W_(c, 8), B_(c, 8), c->norm, c->ring, c->Pv, c->nblk_val, c->dstate,
-                       c->cfg.avg_window, c->part_se, st));
+  if (f16) {  // L8 with the validation head fused
+    HeadValArgs hv{W_(c, 8), B_(c, 8), c->norm, c->ring, c->dstate, c->cfg.avg_window, c->part_se};
+    PROF(kPValConv, 7, conv_flop(c->Pv, 7) + 2.0 * c->Pv * kMaxC,
+         conv_tc_launch_head_val(c->val_plan[7], B_(c, 7), hv, st));
+  } else {
+    // layer 7 (odd) wrote vB
+    PROF(kPHeadVal, 8, 2.0 * c->Pv * kMaxC,
+         launch_head_val(c->vB, W_(c, 8), B_(c, 8), c->norm, c->ring, c->Pv, c->nblk_val, c->dstate,
+                         c->cfg.avg_window, c->part_se, st));
+  }
   return N2F_OK;
 }
 
@@ -421,17 +433,17 @@ int setup(n2f_ctx* c) {
   N2F_TRY(dalloc(c, &c->m, off));
   N2F_TRY(dalloc(c, &c->v, off));
   for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt[li], c->pnum[2 * li]));
-  // FP16x3 keeps layer outputs as fp16 operand pairs (allocated below); fp32
-  // copies only where an fp32 consumer exists: L8's output (the head), the L1
-  // dgrad output (the SIMT first-layer wgrad) and the validation L8 output
+  // FP16x3 keeps layer outputs as fp16 operand pairs (allocated below) and
+  // fuses the L9 head into L8's epilogue; the only fp32 layer buffer left is
+  // the L1 dgrad output (the SIMT first-layer wgrad)
   const bool f16 = c->f16;
-  for (int li = 0; li < 8; ++li)
-    if (!f16 || li == 7) N2F_TRY(dalloc(c, &c->act[li], c->Pt * kCout[li]));
+  if (!f16)
+    for (int li = 0; li < 8; ++li) N2F_TRY(dalloc(c, &c->act[li], c->Pt * kCout[li]));
   N2F_TRY(dalloc(c, &c->z, c->Pt));
   if (!f16) N2F_TRY(dalloc(c, &c->gA, c->Pt * kMaxC));
   N2F_TRY(dalloc(c, &c->gB, c->Pt * (f16 ? kCout[0] : kMaxC)));
   if (!f16) N2F_TRY(dalloc(c, &c->vA, c->Pv * kMaxC));
-  N2F_TRY(dalloc(c, &c->vB, c->Pv * kMaxC));
+  if (!f16) N2F_TRY(dalloc(c, &c->vB, c->Pv * kMaxC));
   N2F_TRY(dalloc(c, &c->ring, (int64_t)c->cfg.avg_window * c->Pv));
 
   c->nblk_head = nblocks_for(c->Pt, 64);
@@ -447,8 +459,12 @@ int setup(n2f_ctx* c) {
     for (int li = 1; li < 8; ++li) wsplit[sc][li] = wgrad_tc_nsplit(kCin[li], kCout[li], c->ph[2 * sc], c->pw[2 * sc]);
   for (int li = 0; li < kLayers; ++li) {
     int64_t nb = c->nsplit[li], nw = c->nsplit[li];
-    if (c->tc && li >= 1 && li <= 6 && max_tiles > nb) nb = max_tiles;
+    if (c->tc && li >= 1 && li <= 7 && max_tiles > nb) nb = max_tiles;
     if (c->tc && li == 7 && c->nblk_head > nb) nb = c->nblk_head;
+    if (f16 && li == 8) {  // fused head: per-tile db9, per-(tile, warp group) dW9
+      nb = max_tiles;
+      nw = 4 * (int64_t)max_tiles;
+    }
     if (c->tc && li >= 1 && li <= 7) {
       nw = wsplit[0][li] > wsplit[1][li] ? wsplit[0][li] : wsplit[1][li];
       if (c->nsplit[li] > nw) nw = c->nsplit[li];
@@ -516,8 +532,11 @@ int setup(n2f_ctx* c) {
       for (int li = 1; li < 8; ++li) {
         ConvTcPlan& fp = c->fwd_plan[sc][li];
         N2F_TRY(conv_tc_plan(&fp, act_op(li - 1), w_op(li), h, w, kCin[li], kCout[li], f16));
-        // forward outputs: the operand pair of the next layer (L8: fp32 for the head)
-        if (li == 7)
+        // forward outputs: the operand pair of the next layer; L8: fp32 for the
+        // head (TF32) or, with the head fused (FP16), the L8 gradient pair
+        if (li == 7 && f16)
+          N2F_TRY(conv_tc_plan_out(&fp, nullptr, c->g16[0][0], c->g16[0][1], sg));
+        else if (li == 7)
           N2F_TRY(conv_tc_plan_out(&fp, c->act[7], nullptr, nullptr, sa));
         else if (f16)
           N2F_TRY(conv_tc_plan_out(&fp, nullptr, c->act16[0][li], c->act16[1][li], sa));
@@ -550,7 +569,9 @@ int setup(n2f_ctx* c) {
                            f16));
       const int ob = 1 - ab;  // layer li writes vB when odd
       float* vf = ob ? c->vB : c->vA;
-      if (li == 7)
+      if (li == 7 && f16)
+        N2F_TRY(conv_tc_plan_out(&c->val_plan[li], nullptr, nullptr, nullptr, sa));  // fused head
+      else if (li == 7)
         N2F_TRY(conv_tc_plan_out(&c->val_plan[li], vf, nullptr, nullptr, sa));
       else if (f16)
         N2F_TRY(conv_tc_plan_out(&c->val_plan[li], nullptr, c->v16[ob][0], c->v16[ob][1], sa));
@@ -560,8 +581,14 @@ int setup(n2f_ctx* c) {
     c->bias_tiles[0] = tiles[0];
     c->bias_tiles[1] = tiles[1];
   }
+  if (f16) {  // fused heads write one loss / squared-error partial per tile
+    c->nblk_head = max_tiles;
+    c->nblk_val = c->val_plan[7].tiles;
+  }
   N2F_TRY(dalloc(c, &c->part_loss, 4 * (int64_t)c->nblk_head));
   N2F_TRY(dalloc(c, &c->part_se, c->nblk_val));
+  // a shape class with fewer tiles leaves its tail of the loss partials at 0
+  N2F_CUDA(cudaMemset(c->part_loss, 0, 4 * (size_t)c->nblk_head * sizeof(double)));
   N2F_TRY(dalloc(c, &c->dstate, 1));
   N2F_TRY(dalloc(c, &c->step_counter, 1));
   N2F_TRY(dalloc(c, &c->val_hist, c->cfg.max_epochs));
@@ -634,8 +661,13 @@ int setup(n2f_ctx* c) {
     for (int sc = 0; sc < 2; ++sc) {
       c->adam_sc[sc] = a;
       for (int li = 1; li <= 7; ++li) {
-        c->adam_sc[sc].t[2 * li + 1].nsplit = li == 7 ? c->nblk_head : c->dgrad_plan[sc][li + 1].tiles;
+        c->adam_sc[sc].t[2 * li + 1].nsplit =
+            li == 7 ? (f16 ? c->fwd_plan[sc][7].tiles : c->nblk_head) : c->dgrad_plan[sc][li + 1].tiles;
         c->adam_sc[sc].t[2 * li].nsplit = c->wsplit[sc][li];
+      }
+      if (f16) {  // the head's partials come from the fused L8 epilogue
+        c->adam_sc[sc].t[16].nsplit = 4 * c->fwd_plan[sc][7].tiles;
+        c->adam_sc[sc].t[17].nsplit = c->fwd_plan[sc][7].tiles;
       }
     }
   }

@@ -3,6 +3,7 @@
 // device-side early-stopping state machine and the output window mean.
 #include "n2f_internal.cuh"
 #include "tc_common.cuh"
+#include "loss_dev.cuh"
 #include "train.cuh"
 
 namespace n2f {
@@ -15,28 +16,6 @@ __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-// Two-branch logistic (tensor.py:153-161), IEEE division.
-__device__ __forceinline__ float sigmoid_ref(float z) {
-  if (z >= 0.f) return __fdiv_rn(1.f, __fadd_rn(1.f, expf(-z)));
-  const float e = expf(z);
-  return __fdiv_rn(e, __fadd_rn(1.f, e));
-}
-
-// dloss/dz and the per-element loss for the two training losses
-// (tensor.py:164-193, trainer.py:112-117).
-__device__ __forceinline__ float loss_grad(float z, float t, int loss, float inv_n_num,
-                                           float two_over_n, float* elem) {
-  const float s = sigmoid_ref(z);
-  if (loss == 0) {
-    *elem = __fadd_rn(__fsub_rn(fmaxf(z, 0.f), __fmul_rn(z, t)), log1pf(expf(-fabsf(z))));
-    return __fdiv_rn(__fsub_rn(s, t), inv_n_num);  // (sigmoid(z) - t) / N
-  }
-  const float d = __fsub_rn(s, t);
-  *elem = __fmul_rn(d, d);
-  const float gs = __fmul_rn(two_over_n, d);                   // (2/N) * diff
-  return __fmul_rn(__fmul_rn(gs, s), __fsub_rn(1.f, s));       // grad_s * s * (1 - s)
 }
 
 // ---------------------------------------------------------------------------

@@ -18,6 +18,40 @@ struct DevState {
   unsigned long long t0;  // %globaltimer at the start of the fit
 };
 
+// The 1x1 head (L9) fused into the epilogue of the last 3x3 convolution
+// (FP16x3 path): training = logits, loss, dloss/dz, the L8 gradient pair and
+// per-tile partials of dW9 / db9 / loss; validation = sigmoid, clip, ring slot
+// and per-tile squared-error partials.
+struct HeadTrainArgs {
+  const float* w9;
+  const float* b9;
+  const float* tgt;
+  float* zout;
+  float* part_w9;      // [tiles * 4][256] (one row per 32-pixel warp group)
+  float* part_b9;      // [tiles]
+  double* part_loss;   // [tiles]
+  int* step_counter;   // Adam t, incremented once per step
+  int loss;
+  float nf, two_over_n;
+};
+struct HeadValArgs {
+  const float* w9;
+  const float* b9;
+  const float* norm;
+  float* ring;
+  const DevState* st;
+  int window;
+  double* part_se;  // [tiles]
+};
+
+// L8 forward with the head fused (FP16 dy plan, N = 256; conv_tc.cu).  The
+// training variant writes the L8 gradient pair through the plan's outputs and
+// the bias gradient of L8 into colsum ([tiles][256]).
+int conv_tc_launch_head_train(const ConvTcPlan& pl, const float* bias, float* colsum,
+                              const HeadTrainArgs& ht, cudaStream_t st);
+int conv_tc_launch_head_val(const ConvTcPlan& pl, const float* bias, const HeadValArgs& hv,
+                            cudaStream_t st);
+
 struct Pt4 {
   double v[4];
 };
