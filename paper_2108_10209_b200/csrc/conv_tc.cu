@@ -31,6 +31,10 @@
 #include "train.cuh"
 
 // Build with -DN2F_TC_TRACE=1 for per-warp cycle accounting (N2F_TC_DEBUG=64).
+// -DN2F_DY256_EC32=1: experiment, 32-channel staging for N = 256 (2 dy stages)
+#ifndef N2F_DY256_EC32
+#define N2F_DY256_EC32 1
+#endif
 #ifndef N2F_TC_TRACE
 #define N2F_TC_TRACE 0
 #endif
@@ -718,7 +722,7 @@ struct DyCfg {
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
   // staging slices: 32 channels (one fence + TMA issue per 32) where smem
   // allows, 16 for BN = 256 (whose three 66 KB dy stages fill the rest)
-  static constexpr int kEpiCols = BN == 256 ? 16 : (BN / 2 < 32 ? BN / 2 : 32);
+  static constexpr int kEpiCols = (BN == 256 && !N2F_DY256_EC32) ? 16 : (BN / 2 < 32 ? BN / 2 : 32);
   static constexpr int kEpiBuf = 32 * kEpiCols * 4;  // one staging buffer (fp32 y, or the fp16 pair)
   static constexpr int kEpiNBuf = 1;
   static constexpr int kEpiWarpBytes = kEpiNBuf * kEpiBuf;
@@ -734,7 +738,7 @@ struct DyCfg {
 // HEAD: 0 plain conv; 1 / 2 (BN = 256 only) = the L9 training / validation
 // head fused into the epilogue (see HeadTrainArgs / HeadValArgs).
 template <int BN, int HEAD>
-__global__ void __launch_bounds__(kThreadsTc, 1)
+__global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 warps share an SMSP
     k_conv3x3_dy(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
                  const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
@@ -1903,7 +1907,7 @@ int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any c
 int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale) {
   if (!pl->f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
   // staging slice geometry: dy kernel {EC channels, 4 x, 8 y}, else {EC, 32 x, 1 y}
-  const int ec = pl->dy ? (pl->N == 256 ? 16 : (pl->N / 2 < 32 ? pl->N / 2 : 32))
+  const int ec = pl->dy ? ((pl->N == 256 && !N2F_DY256_EC32) ? 16 : (pl->N / 2 < 32 ? pl->N / 2 : 32))
                         : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
   const int bw = pl->dy ? 4 : kTW, bh = pl->dy ? 8 : 1;
   auto sw_for = [](int row_bytes) {
