@@ -1,5 +1,5 @@
-"""Full-fit PSNR parity across seeds: CPU oracle vs the GPU engine (SIMT and
-tcgen05 convs).  Prints one JSON line per (seed) and a summary.
+"""Full-fit PSNR parity across seeds: CPU oracle vs the GPU engine (SIMT,
+tcgen05 3xTF32 and FP16x3 convs).  Prints one JSON line per (seed) and a summary.
 
     python tools/psnr_parity.py --size 64 --seeds 4
 """
@@ -37,7 +37,7 @@ def main():
         noisy = synthetic.gaussian_noisy(clean, args.sigma / 255, 200 + s).astype(np.float64)
         row = {"seed": s, "psnr_noisy": psnr(noisy, clean)}
         cfg = TrainConfig(seed=s)
-        for impl, name in (() if args.cpu_only else ((1, "simt"), (2, "tc"))):
+        for impl, name in (() if args.cpu_only else ((1, "simt"), (2, "tf32x3"), (3, "f16x3"))):
             eng = Engine(args.size, args.size, cfg, conv_impl=impl)
             out, r, hist, _, _ = eng.fit_host(np.ascontiguousarray(noisy))
             eng.close()
@@ -51,7 +51,7 @@ def main():
             row["cpu_s"] = time.time() - t
         rows.append(row)
         print(json.dumps(row), flush=True)
-    keys = ([] if args.cpu_only else ["simt", "tc"]) + ([] if args.no_cpu else ["cpu"])
+    keys = ([] if args.cpu_only else ["simt", "tf32x3", "f16x3"]) + ([] if args.no_cpu else ["cpu"])
     print(json.dumps({"mean": {k: float(np.mean([r[k] for r in rows])) for k in keys}}))
 
 
