@@ -370,15 +370,17 @@ int build_graph(n2f_ctx* c) {
   return N2F_OK;
 }
 
-// Move every Adam tensor with more than kMaxInlineSplits partials onto a
-// k_col_reduce pass (output slot = the tensor's arena offset in grad_red).
-constexpr int kMaxInlineSplits = 32;
+// Move the tall partial matrices (many split-K rows over few columns: per-tile
+// bias sums, the head, the first layer) onto a k_col_reduce pass (output slot =
+// the tensor's arena offset in grad_red); wide ones (the wgrad partials of the
+// 3x3 layers) are summed inline by Adam, one coalesced column per thread.
+constexpr int kMaxInlineSplits = 32, kMaxInlineSplitsWide = 256;
 int route_reductions(n2f_ctx* c, AdamArgs& a, ColReduceArgs& r) {
   r.n = 0;
   r.prefix[0] = 0;
   for (int q = 0; q < a.ntensors; ++q) {
     AdamTensor& T = a.t[q];
-    if (T.nsplit <= kMaxInlineSplits) continue;
+    if (T.nsplit <= kMaxInlineSplits || (T.n >= 4096 && T.nsplit <= kMaxInlineSplitsWide)) continue;
     if (r.n == kMaxColReduce) return fail(N2F_ERR_ARG, "too many reductions");
     ColReduce& t = r.t[r.n];
     t.part = T.part;

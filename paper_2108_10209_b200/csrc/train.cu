@@ -202,12 +202,29 @@ __global__ void __launch_bounds__(kThreads)
     k_adam(AdamArgs args, const int* __restrict__ step_counter, int fixed_t) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= args.total) return;
-  int k = 0;
-  while (k + 1 < args.ntensors && i >= args.t[k + 1].off) ++k;
-  const AdamTensor& T = args.t[k];
+  int tl = 0, th = args.ntensors - 1;  // the tensor holding parameter i (binary search)
+  while (tl < th) {
+    const int mid = (tl + th + 1) >> 1;
+    if (i >= args.t[mid].off)
+      tl = mid;
+    else
+      th = mid - 1;
+  }
+  const AdamTensor& T = args.t[tl];
   const int64_t j = i - T.off;
-  float g = T.part[j];
-  for (int s = 1; s < T.nsplit; ++s) g += T.part[(int64_t)s * T.n + j];
+  // fixed-order sum of the split-K partials; four independent loads in flight
+  const float* __restrict__ part = T.part + j;
+  float g = __ldg(part);
+  int s = 1;
+  for (; s + 3 < T.nsplit; s += 4) {
+    const float a0 = __ldg(part + (int64_t)s * T.n), a1 = __ldg(part + (int64_t)(s + 1) * T.n);
+    const float a2 = __ldg(part + (int64_t)(s + 2) * T.n), a3 = __ldg(part + (int64_t)(s + 3) * T.n);
+    g += a0;
+    g += a1;
+    g += a2;
+    g += a3;
+  }
+  for (; s < T.nsplit; ++s) g += __ldg(part + (int64_t)s * T.n);
   const int t = step_counter ? *step_counter : fixed_t;
   const int ti = (t < args.table_len ? t : args.table_len) - 1;
   const float bc1 = args.bc1[ti], bc2 = args.bc2[ti];
@@ -259,8 +276,19 @@ __global__ void __launch_bounds__(1024) k_col_reduce(ColReduceArgs a) {
   const int col = (b - a.prefix[k]) * 32 + (threadIdx.x & 31);
   const int r0 = threadIdx.x >> 5;
   float s = 0.f;
-  if (col < T.cols)
-    for (int r = r0; r < T.rows; r += 32) s += T.part[(int64_t)r * T.cols + col];
+  if (col < T.cols) {  // fixed order; four independent loads in flight
+    const float* __restrict__ pc = T.part + col;
+    int r = r0;
+    for (; r + 96 < T.rows; r += 128) {
+      const float a0 = __ldg(pc + (int64_t)r * T.cols), a1 = __ldg(pc + (int64_t)(r + 32) * T.cols);
+      const float a2 = __ldg(pc + (int64_t)(r + 64) * T.cols), a3 = __ldg(pc + (int64_t)(r + 96) * T.cols);
+      s += a0;
+      s += a1;
+      s += a2;
+      s += a3;
+    }
+    for (; r < T.rows; r += 32) s += __ldg(pc + (int64_t)r * T.cols);
+  }
   sm[r0][threadIdx.x & 31] = s;
   __syncthreads();
   if (r0 == 0 && col < T.cols) {
