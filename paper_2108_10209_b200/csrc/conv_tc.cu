@@ -31,9 +31,13 @@
 #include "train.cuh"
 
 // Build with -DN2F_TC_TRACE=1 for per-warp cycle accounting (N2F_TC_DEBUG=64).
-// -DN2F_DY256_EC32=1: experiment, 32-channel staging for N = 256 (2 dy stages)
+// -DN2F_DY256_EC32=0: 16-channel staging for N = 256 (3 dy stages instead of 2)
 #ifndef N2F_DY256_EC32
 #define N2F_DY256_EC32 1
+#endif
+// -DN2F_DY_KC16=1: 16-channel K chunks for N = 256 (experiment)
+#ifndef N2F_DY_KC16
+#define N2F_DY_KC16 0
 #endif
 #ifndef N2F_TC_TRACE
 #define N2F_TC_TRACE 0
@@ -715,10 +719,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 // ---------------------------------------------------------------------------
 template <int BN>
 struct DyCfg {
-  static constexpr int kRowsA = 18 * 8;              // halo columns x rows
-  static constexpr int kStageA = kRowsA * 64;        // one fp16 part (hi or lo), 32 channels
-  static constexpr int kTapB = (BN / 2) * 64;        // this CTA's weight rows of one tap
-  static constexpr int kStageB = 3 * kTapB;          // the three dx taps
+  // K chunk of a stage: 32 channels (SWIZZLE_64B rows); 16 (SWIZZLE_32B, five
+  // stages for N = 256) measured no faster.  A group spans K = 96 either way.
+  static constexpr int kKC = N2F_DY_KC16 && BN == 256 ? 16 : 32;
+  static constexpr int kRow = kKC * 2;                // bytes per GEMM row (fp16)
+  static constexpr int kGroup = 32 / kKC;             // stages per group
+  static constexpr int kKSteps = kKC / 16;            // MMA K steps per tap and stage
+  static constexpr uint32_t kLayout = kKC == 32 ? 4 : 6;  // UMMA SWIZZLE_64B / _32B
+  static constexpr int kDxUnits = (8 * kRow) >> 4;    // a dx shift: 8 rows, descriptor units
+  static constexpr int kRowsA = 18 * 8;               // halo columns x rows
+  static constexpr int kStageA = kRowsA * kRow;       // one fp16 part (hi or lo)
+  static constexpr int kTapB = (BN / 2) * kRow;       // this CTA's weight rows of one tap
+  static constexpr int kStageB = 3 * kTapB;           // the three dx taps
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
   // staging slices: 32 channels (one fence + TMA issue per 32) where smem
   // allows, 16 for BN = 256 (whose three 66 KB dy stages fill the rest)
@@ -766,7 +778,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
   const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
   const int tiles_x = (W + 31) / 32;
   const int nunits = tiles_x * ((H + 7) / 8);
-  const int KB = 3 * (C / 32);  // stages (= groups) per tile
+  constexpr int G = Cfg::kGroup;
+  const int KB = 3 * (C / Cfg::kKC);  // stages per tile
+  const int NG = KB / G;              // accumulation groups per tile
 
   if (tid == 0) {
     if (HEAD == 1 && blockIdx.x == 0 && ht.step_counter) *ht.step_counter += 1;  // Adam t
@@ -804,7 +818,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
       for (int kb = 0; kb < KB; ++kb, ++it) {
         const int s = it % S, round = it / S;
         if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-        const int c0 = (kb / 3) * 32, dy = kb % 3;
+        const int c0 = (kb / 3) * Cfg::kKC, dy = kb % 3;
         uint8_t* st = base + s * Cfg::kStageBytes;
         if (elect_one_sync()) {
           const uint32_t fb = full0 + 8u * s;
@@ -823,14 +837,14 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
       constexpr uint32_t idesc = P::idesc(256, BN, false, false);
       constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
                          kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4, kTap = Cfg::kTapB >> 4;
-      const uint64_t desc0 = P::kdesc(smem_u32(base));
-      int gg = 0;
+      const uint64_t desc0 = sw128_desc(smem_u32(base), 16, 8 * Cfg::kRow, Cfg::kLayout);
+      int gg = 0, it = 0;
 #if N2F_TC_TRACE
       long long we_ = 0, wf_ = 0, t0_ = clock64();
 #endif
       for (int ut = cid; ut < nunits; ut += ncl) {
-        for (int kb = 0; kb < KB; ++kb, ++gg) {
-          const int s = gg % S, b = gg % NB;
+        for (int g = 0; g < NG; ++g, ++gg) {
+          const int b = gg % NB;
 #if N2F_TC_TRACE
           const long long c0 = clock64();
 #endif
@@ -838,7 +852,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
 #if N2F_TC_TRACE
           const long long c1 = clock64();
 #endif
-          mbar_wait(&full[s], (gg / S) & 1);
+          for (int j = 0; j < G; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
 #if N2F_TC_TRACE
           we_ += c1 - c0;
           wf_ += clock64() - c1;
@@ -846,28 +860,41 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
           tc_fence_after();
           if (elect_one_sync()) {
             const uint32_t d = taddr + b * BN;
-            const uint64_t a0 = desc0 + (uint64_t)(s * (Cfg::kStageBytes >> 4));
-            // cross terms of the three taps first, then hi*hi; a dx shift is
-            // 8 rows = 512 B = 32 descriptor units, a K step 32 B = 2 units
+            uint64_t a0[G];
 #pragma unroll
-            for (int dx = 0; dx < 3; ++dx) {
+            for (int j = 0; j < G; ++j)
+              a0[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
+            // cross terms of the whole group first, then hi*hi; a dx shift is
+            // 8 rows (one swizzle atom), a K step 32 B = 2 descriptor units
 #pragma unroll
-              for (int k = 0; k < 2; ++k) {
-                const uint64_t a = a0 + 32 * dx + 2 * k, bh = a0 + kBh + kTap * dx + 2 * k;
-                mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, (dx | k) != 0);
-                mma_f16_2sm(d, a + kAl, bh, idesc, 1);
+            for (int j = 0; j < G; ++j) {
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+                for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  const uint64_t a = a0[j] + Cfg::kDxUnits * dx + 2 * k;
+                  const uint64_t bh = a0[j] + kBh + kTap * dx + 2 * k;
+                  mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, (j | dx | k) != 0);
+                  mma_f16_2sm(d, a + kAl, bh, idesc, 1);
+                }
               }
             }
 #pragma unroll
-            for (int dx = 0; dx < 3; ++dx) {
+            for (int j = 0; j < G; ++j) {
 #pragma unroll
-              for (int k = 0; k < 2; ++k)
-                mma_f16_2sm(d, a0 + 32 * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k, idesc, 1);
+              for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+                for (int k = 0; k < Cfg::kKSteps; ++k)
+                  mma_f16_2sm(d, a0[j] + Cfg::kDxUnits * dx + 2 * k,
+                              a0[j] + kBh + kTap * dx + 2 * k, idesc, 1);
+              }
             }
-            mma_commit_2sm(&empty[s]);
+#pragma unroll
+            for (int j = 0; j < G; ++j) mma_commit_2sm(&empty[(it + j) % S]);
             mma_commit_2sm(&tfull[b]);
           }
           __syncwarp();
+          it += G;
         }
       }
 #if N2F_TC_TRACE
@@ -905,7 +932,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
       float acc[HALF];
 #pragma unroll
       for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
-      for (int kb = 0; kb < KB; ++kb, ++gg) {
+      for (int g = 0; g < NG; ++g, ++gg) {
         const int b = gg % NB;
 #if N2F_TC_TRACE
         const long long c0 = clock64();
@@ -1614,14 +1641,15 @@ int map_act_blk(CUtensorMap* m, const void* p, bool f16, int C, int W, int H, in
 
 // NHWC activation viewed as 3-D (C, H, W): a box {32, bh, bw} lands as
 // [x][y][32 channels], i.e. GEMM rows ordered y-fastest (the dy-stage conv).
-int map_act_yx(CUtensorMap* m, const void* p, int C, int W, int H, int bh, int bw) {
+int map_act_yx(CUtensorMap* m, const void* p, int C, int W, int H, int bc, int bh, int bw) {
   N2F_TRY(encoder());
   const cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)H, (cuuint64_t)W};
   const cuuint64_t strides[2] = {(cuuint64_t)W * C * 2, (cuuint64_t)C * 2};
-  const cuuint32_t box[3] = {32, (cuuint32_t)bh, (cuuint32_t)bw};
+  const cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)bh, (cuuint32_t)bw};
+  const CUtensorMapSwizzle sw = bc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(p), dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(act yx) failed: %d", (int)r);
   return N2F_OK;
@@ -1629,14 +1657,15 @@ int map_act_yx(CUtensorMap* m, const void* p, int C, int W, int H, int bh, int b
 
 // K-major weights [N][9 taps][C] (fp16) viewed as 4-D (C, N, dx, dy): a box
 // {32, rows, 3, 1} holds the three dx taps of one dy as [dx][row][32 ch].
-int map_w_taps(CUtensorMap* m, const void* p, int C, int N, int rows) {
+int map_w_taps(CUtensorMap* m, const void* p, int C, int N, int bc, int rows) {
   N2F_TRY(encoder());
   const cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)N, 3, 3};
   const cuuint64_t strides[3] = {(cuuint64_t)9 * C * 2, (cuuint64_t)C * 2, (cuuint64_t)3 * C * 2};
-  const cuuint32_t box[4] = {32, (cuuint32_t)rows, 3, 1};
+  const cuuint32_t box[4] = {(cuuint32_t)bc, (cuuint32_t)rows, 3, 1};
+  const CUtensorMapSwizzle sw = bc == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(p), dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(w taps) failed: %d", (int)r);
   return N2F_OK;
@@ -1871,10 +1900,11 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
     const int max_units = sm_count() / 2;
     pl->grid = 2 * (units < max_units ? units : max_units);
     pl->tiles = 2 * units;
-    N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, 8, 18));
-    N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, 8, 18));
-    N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, N / 2));
-    N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, N / 2));
+    const int kc = N2F_DY_KC16 && N == 256 ? 16 : 32;  // DyCfg<N>::kKC
+    N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, kc, 8, 18));
+    N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, kc, 8, 18));
+    N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, kc, N / 2));
+    N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, kc, N / 2));
     return N2F_OK;
   }
   // wide layers (N >= 128) run as CTA pairs (cta_group::2, M = 256: each CTA
