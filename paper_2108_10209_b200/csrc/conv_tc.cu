@@ -218,6 +218,14 @@ __device__ __forceinline__ void store_pair4(const ConvOut& o, int64_t idx, float
   }
 }
 
+// Programmatic dependent launch: let the next kernel of the stream launch (its
+// prologue overlaps this kernel's tail), and wait for the previous one's
+// results only after this kernel's own prologue.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Row-swizzled 16-byte chunk position inside a TMA staging tile whose rows are
 // RB bytes (the SWIZZLE_32B / SWIZZLE_64B patterns; none for 16-byte rows).
 template <int RB>
@@ -264,6 +272,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __shared__ uint32_t tslot;
   __shared__ __align__(16) float csum[4][BN];
   uint8_t* base = align1024(smem_raw);
+  pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
   const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
@@ -303,6 +312,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t taddr = tslot;
+  pdl_wait();  // everything above overlaps the previous kernel's tail (PDL)
 
   if (warp == 0) {
     // ---- TMA producer (stage index `it` runs across tiles).  The whole warp
@@ -773,6 +783,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
   __shared__ double hred_d[4];
   __shared__ float hred_f[4];
   uint8_t* base = align1024(smem_raw);
+  pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
@@ -806,6 +817,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
   cluster_sync();
   tc_fence_after();
   const uint32_t taddr = tslot;
+  pdl_wait();  // everything above overlaps the previous kernel's tail (PDL)
 
   if (warp == 0) {
     // ---- TMA producer: per stage one activation box (hi, lo) and one
@@ -1336,6 +1348,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   __shared__ uint64_t full[S], empty[S], tfull[NB], tempty[NB];
   __shared__ uint32_t tslot;
   uint8_t* base = align1024(smem_raw);
+  pdl_trigger();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
   const int K9 = 9 * C;
@@ -1383,6 +1396,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t taddr = tslot;
+  pdl_wait();  // everything above overlaps the previous kernel's tail (PDL)
 
   if (warp == 0) {
     // ---- TMA producer (whole warp walks the schedule, one elected lane issues)
@@ -1688,6 +1702,15 @@ int map_mat(CUtensorMap* m, const void* p, bool f16, int cols, int rows, int bc,
   return N2F_OK;
 }
 
+// N2F_PDL=0 disables programmatic dependent launch (A/B experiments)
+int pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("N2F_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return on;
+}
+
 template <int BN, bool F16>
 int set_attr_one() {
   N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, F16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1746,13 +1769,15 @@ int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask,
   cfg.blockDim = dim3(kThreadsTc);
   cfg.dynamicSmemBytes = FwdCfg<BN, F16, CS>::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_tc<BN, F16, CS>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
                               pl.myh, pl.myl, pl.omask, pl.oscale,
                               ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, bias, mask, pl.mask_bits,
@@ -1770,13 +1795,15 @@ int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, fl
   cfg.blockDim = dim3(kThreadsTc);
   cfg.dynamicSmemBytes = DyCfg<BN>::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   static const int direct = [] {
     const char* e = getenv("N2F_DY_DIRECT");
     return e ? atoi(e) : 0;
@@ -1824,13 +1851,15 @@ int launch_wgrad_tc_bn(const WgradTcPlan& pl, float* part, cudaStream_t st) {
   cfg.blockDim = dim3(kThreadsTc);
   cfg.dynamicSmemBytes = WgCfg<BN, F16, CS, SEG>::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   N2F_CUDA(cudaLaunchKernelEx(&cfg, k_wgrad3x3_tc<BN, F16, CS, SEG>, pl.mx, pl.mxl, pl.mg, pl.mgl,
                               part, pl.unscale, pl.H, pl.W, pl.C, pl.nsplit, pl.xblk));
   N2F_LAUNCH_CHECK();
