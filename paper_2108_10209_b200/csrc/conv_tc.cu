@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
     const int xl = 4 * q + (lane >> 3), yl = lane & 7;
     constexpr int EC = DyCfg<BN>::kEpiCols, CH = EC / 4;
     constexpr int RBY = EC * 4, RBH = EC * 2;  // staging row bytes: fp32 / fp16
-    const int srow = yl * 4 + (lane >> 3);      // staging row: box {EC ch, 4 x, 8 y}
+    const int srow = lane;  // staging row: box {EC ch, 8 y, 4 x} staged [x][y][ch]
     uint8_t* stg0 = base + S * Cfg::kStageBytes + (warp - 2) * Cfg::kEpiWarpBytes;
     int gg = 0, sb = 0;
     for (int ut = cid; ut < nunits; ut += ncl) {
@@ -1080,8 +1080,8 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
             __syncwarp();
             if (elect_one_sync()) {
               const int bx = x0 + 4 * q;
-              tma_store_3d(&myh, stg, n, bx, y0);
-              tma_store_3d(&myl, stg + 32 * RBH, n, bx, y0);
+              tma_store_3d(&myh, stg, n, y0, bx);
+              tma_store_3d(&myl, stg + 32 * RBH, n, y0, bx);
               bulk_commit_group();
             }
           }
@@ -1256,9 +1256,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
 #endif
         if (elect_one_sync()) {
           const int bx = x0 + 4 * q;
-          if (omask & kOutY) tma_store_3d(&my, stg, n, bx, y0);
-          if (omask & kOutHi) tma_store_3d(&myh, stg, n, bx, y0);
-          if (omask & kOutLo) tma_store_3d(&myl, stg + 32 * RBH, n, bx, y0);
+          if (omask & kOutY) tma_store_3d(&my, stg, n, y0, bx);
+          if (omask & kOutHi) tma_store_3d(&myh, stg, n, y0, bx);
+          if (omask & kOutLo) tma_store_3d(&myl, stg + 32 * RBH, n, y0, bx);
           bulk_commit_group();
         }
         if (Cfg::kEpiNBuf == 2) sb ^= 1;
@@ -1669,6 +1669,23 @@ int map_act_yx(CUtensorMap* m, const void* p, int C, int W, int H, int bc, int b
   return N2F_OK;
 }
 
+// Output tensor [H][W][C] viewed as 3-D (C, H, W) for the dy kernel's TMA
+// stores: a box {bc, 8 y, 4 x} is staged as [x][y][channels], i.e. row = lane.
+int map_out_yx(CUtensorMap* m, void* p, bool f16, int C, int W, int H, int bc,
+               CUtensorMapSwizzle sw) {
+  N2F_TRY(encoder());
+  const cuuint64_t es = f16 ? 2 : 4;
+  const cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)H, (cuuint64_t)W};
+  const cuuint64_t strides[2] = {(cuuint64_t)W * C * es, (cuuint64_t)C * es};
+  const cuuint32_t box[3] = {(cuuint32_t)bc, 8, 4};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        3, p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(out yx) failed: %d", (int)r);
+  return N2F_OK;
+}
+
 // K-major weights [N][9 taps][C] (fp16) viewed as 4-D (C, N, dx, dy): a box
 // {32, rows, 3, 1} holds the three dx taps of one dy as [dx][row][32 ch].
 int map_w_taps(CUtensorMap* m, const void* p, int C, int N, int bc, int rows) {
@@ -1981,21 +1998,27 @@ int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscal
   pl->y = y;
   pl->yhi = yhi;
   pl->ylo = ylo;
+  // the dy kernel stages [x][y][channels] (row = lane: conflict-free swizzle)
+  auto omap = [&](CUtensorMap* m, void* p, bool half) -> int {
+    const CUtensorMapSwizzle sw = sw_for(ec * (half ? 2 : 4));
+    return pl->dy ? map_out_yx(m, p, half, pl->N, pl->W, pl->H, ec, sw)
+                  : map_act(m, p, half, pl->N, pl->W, pl->H, ec, bw, bh, sw);
+  };
   if (y) {
-    N2F_TRY(map_act(&pl->my, y, false, pl->N, pl->W, pl->H, ec, bw, bh, sw_for(ec * 4)));
+    N2F_TRY(omap(&pl->my, y, false));
     pl->omask |= kOutY;
   }
   if (pl->f16) {
     if (yhi) {
-      N2F_TRY(map_act(&pl->myh, yhi, true, pl->N, pl->W, pl->H, ec, bw, bh, sw_for(ec * 2)));
+      N2F_TRY(omap(&pl->myh, yhi, true));
       pl->omask |= kOutHi;
     }
     if (ylo) {
-      N2F_TRY(map_act(&pl->myl, ylo, true, pl->N, pl->W, pl->H, ec, bw, bh, sw_for(ec * 2)));
+      N2F_TRY(omap(&pl->myl, ylo, true));
       pl->omask |= kOutLo;
     }
   } else if (ylo) {
-    N2F_TRY(map_act(&pl->myl, ylo, false, pl->N, pl->W, pl->H, ec, bw, bh, sw_for(ec * 4)));
+    N2F_TRY(omap(&pl->myl, ylo, false));
     pl->omask |= kOutLo;
   }
   return N2F_OK;
