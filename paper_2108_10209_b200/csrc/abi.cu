@@ -290,6 +290,7 @@ int n2f_adam(float* p, const float* g, float* m, float* v, int64_t n, int t, dou
   a.t[0].part = g;
   a.t[0].nsplit = 1;
   a.t[0].wt = nullptr;
+  adam_plan(a);
   N2F_TRY(launch_adam(a, nullptr, 1, S(stream)));
   N2F_CUDA(cudaStreamSynchronize(S(stream)));
   return N2F_OK;

@@ -136,59 +136,64 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
-// First layer (Cin = 1): direct 3x3, one thread per (pixel, 4 output channels).
+// First layer (Cin = 1): direct 3x3, one thread per (pixel, 8 output
+// channels), one image row per grid row (no 64-bit index division).  The
+// 9-tap sum order (fmaf over taps, then + bias) is the reference's im2col
+// dot order (tensor.py:268-282).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
     k_conv_first(const float* __restrict__ x, const float* __restrict__ w,
                  const float* __restrict__ b, float* __restrict__ y, float* __restrict__ ylo, int H,
                  int W, int N, int relu, __half* __restrict__ yh16, __half* __restrict__ yl16,
                  float oscale) {
-  __shared__ float ws[kMaxC * 9];
-  __shared__ float bs[kMaxC];
+  __shared__ __align__(16) float ws[kMaxC * 9];
+  __shared__ __align__(16) float bs[kMaxC];
   for (int i = threadIdx.x; i < N * 9; i += blockDim.x) ws[i] = w[i];
   for (int i = threadIdx.x; i < N; i += blockDim.x) bs[i] = b[i];
   __syncthreads();
-  const int nq = N / 4;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t P = (int64_t)H * W;
-  if (idx >= P * nq) return;
-  const int p = (int)(idx / nq);
-  const int q = (int)(idx - (int64_t)p * nq);
-  const int py = p / W, px = p - py * W;
+  const int nq = N >> 3, ppb = blockDim.x / nq;
+  const int q = threadIdx.x % nq;
+  const int px = blockIdx.x * ppb + threadIdx.x / nq, py = blockIdx.y;
+  if (px >= W) return;
   float xv[9];
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
-    xv[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + yy * W + xx) : 0.f;
+    xv[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
   }
-  float o[4];
+  float o[8];
+  const float* wq = ws + 8 * q * 9;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int n = 4 * q + j;
+  for (int j = 0; j < 8; ++j) {
     float a = 0.f;
 #pragma unroll
-    for (int t = 0; t < 9; ++t) a = fmaf(xv[t], ws[n * 9 + t], a);
-    o[j] = relu ? fmaxf(a + bs[n], 0.f) : a + bs[n];
+    for (int t = 0; t < 9; ++t) a = fmaf(xv[t], wq[j * 9 + t], a);
+    o[j] = relu ? fmaxf(a + bs[8 * q + j], 0.f) : a + bs[8 * q + j];
   }
-  if (y) *reinterpret_cast<float4*>(y + (size_t)p * N + 4 * q) = make_float4(o[0], o[1], o[2], o[3]);
+  const int64_t idx = ((int64_t)py * W + px) * N + 8 * q;
+  if (y) {
+    *reinterpret_cast<float4*>(y + idx) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(y + idx + 4) = make_float4(o[4], o[5], o[6], o[7]);
+  }
   if (yh16) {  // fp16 pair of y * oscale for the FP16 tcgen05 consumers
-    uint32_t hw[2], lw[2];
+    uint32_t hw[4], lw[4];
 #pragma unroll
-    for (int j = 0; j < 4; j += 2) {
+    for (int j = 0; j < 8; j += 2) {
       __half h0, l0, h1, l1;
       tc::split_f16(o[j] * oscale, h0, l0);
       tc::split_f16(o[j + 1] * oscale, h1, l1);
       hw[j / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
       lw[j / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
     }
-    *reinterpret_cast<uint2*>(yh16 + (size_t)p * N + 4 * q) = make_uint2(hw[0], hw[1]);
-    *reinterpret_cast<uint2*>(yl16 + (size_t)p * N + 4 * q) = make_uint2(lw[0], lw[1]);
+    *reinterpret_cast<uint4*>(yh16 + idx) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(yl16 + idx) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
   if (ylo) {  // tf32 residuals for a tcgen05 consumer
-    float l[4], hh;
+    float l[8], hh;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) tc::split_tf32(o[j], hh, l[j]);
-    *reinterpret_cast<float4*>(ylo + (size_t)p * N + 4 * q) = make_float4(l[0], l[1], l[2], l[3]);
+    for (int j = 0; j < 8; ++j) tc::split_tf32(o[j], hh, l[j]);
+    *reinterpret_cast<float4*>(ylo + idx) = make_float4(l[0], l[1], l[2], l[3]);
+    *reinterpret_cast<float4*>(ylo + idx + 4) = make_float4(l[4], l[5], l[6], l[7]);
   }
 }
 
@@ -314,41 +319,66 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // First-layer wgrad (Cin = 1): dw[o][tap], db[o]; 8 pixel lanes x 32 channels.
+// First-layer wgrad (Cin = 1, NO = 32 output channels): warp = 32 channels,
+// each warp walks 32-pixel row segments with a sliding 3x3 window of the
+// input in registers (3 broadcast loads + one coalesced 128-byte gradient
+// load per pixel).  Block partials [nsplit][NO * 9] / [nsplit][NO], warps
+// combined in fixed order (deterministic).
+constexpr int kFirstSeg = 32;
 __global__ void __launch_bounds__(kThreads)
     k_wgrad_first(const float* __restrict__ g, const float* __restrict__ x,
-                  float* __restrict__ dw_part, float* __restrict__ db_part, int H, int W, int NO,
-                  int chunk) {
-  // blockDim = 256 = (256/NO) lanes x NO channels; NO == 32 in the network.
-  __shared__ float red[kThreads][10];
-  const int o = threadIdx.x % NO, lane = threadIdx.x / NO, nl = blockDim.x / NO;
-  const int s = blockIdx.x;
-  const int P = H * W;
-  const int pbeg = s * chunk, pend = min(P, pbeg + chunk);
+                  float* __restrict__ dw_part, float* __restrict__ db_part, int H, int W, int upw) {
+  constexpr int NO = 32;
+  __shared__ float red[kThreads / 32][NO * 10];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int segs_x = (W + kFirstSeg - 1) / kFirstSeg;
+  const int nunits = H * segs_x;
+  const int gw = blockIdx.x * (kThreads / 32) + warp;
   float acc[10];
 #pragma unroll
   for (int t = 0; t < 10; ++t) acc[t] = 0.f;
+  auto X = [&](int yy, int xx) {
+    return (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
+  };
+  const int u1 = min(nunits, (gw + 1) * upw);
+  for (int u = gw * upw; u < u1; ++u) {
+    const int py = u / segs_x, x0 = (u - py * segs_x) * kFirstSeg;
+    const int x1 = min(W, x0 + kFirstSeg);
+    float a0 = X(py - 1, x0 - 1), a1 = X(py - 1, x0);
+    float b0 = X(py, x0 - 1), b1 = X(py, x0);
+    float c0 = X(py + 1, x0 - 1), c1 = X(py + 1, x0);
+    const float* gr = g + ((int64_t)py * W) * NO + lane;
 #pragma unroll 4
-  for (int p = pbeg + lane; p < pend; p += nl) {
-    const float gv = __ldg(g + (size_t)p * NO + o);
-    const int py = p / W, px = p - py * W;
-#pragma unroll
-    for (int t = 0; t < 9; ++t) {
-      const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
-      const float xv = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + yy * W + xx) : 0.f;
-      acc[t] = fmaf(gv, xv, acc[t]);
+    for (int px = x0; px < x1; ++px) {
+      const float a2 = X(py - 1, px + 1), b2 = X(py, px + 1), c2 = X(py + 1, px + 1);
+      const float gv = __ldg(gr + (int64_t)px * NO);
+      acc[0] = fmaf(gv, a0, acc[0]);
+      acc[1] = fmaf(gv, a1, acc[1]);
+      acc[2] = fmaf(gv, a2, acc[2]);
+      acc[3] = fmaf(gv, b0, acc[3]);
+      acc[4] = fmaf(gv, b1, acc[4]);
+      acc[5] = fmaf(gv, b2, acc[5]);
+      acc[6] = fmaf(gv, c0, acc[6]);
+      acc[7] = fmaf(gv, c1, acc[7]);
+      acc[8] = fmaf(gv, c2, acc[8]);
+      acc[9] += gv;
+      a0 = a1; a1 = a2;
+      b0 = b1; b1 = b2;
+      c0 = c1; c1 = c2;
     }
-    acc[9] += gv;
   }
 #pragma unroll
-  for (int t = 0; t < 10; ++t) red[threadIdx.x][t] = acc[t];
+  for (int t = 0; t < 10; ++t) red[warp][t * NO + lane] = acc[t];
   __syncthreads();
-  if (lane == 0) {
-    for (int l = 1; l < nl; ++l)
+  for (int i = threadIdx.x; i < NO * 10; i += kThreads) {
+    float s = red[0][i];
 #pragma unroll
-      for (int t = 0; t < 10; ++t) acc[t] += red[l * NO + o][t];
-#pragma unroll
-    for (int t = 0; t < 9; ++t) dw_part[(size_t)s * NO * 9 + o * 9 + t] = acc[t];
-    db_part[(size_t)s * NO + o] = acc[9];
+    for (int k = 1; k < kThreads / 32; ++k) s += red[k][i];
+    const int t = i / NO, o = i - t * NO;
+    if (t < 9)
+      dw_part[(int64_t)blockIdx.x * NO * 9 + o * 9 + t] = s;
+    else
+      db_part[(int64_t)blockIdx.x * NO + o] = s;
   }
 }
 
@@ -379,10 +409,12 @@ int conv3x3_simt(const float* x, const float* wk, const float* bias, const float
 int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
                     int cout, cudaStream_t st, int relu, float* ylo, void* yh16, void* yl16,
                     float oscale) {
-  if (cout % 4 || cout > kMaxC) return fail(N2F_ERR_ARG, "conv_first: cout %d", cout);
+  if (cout % 8 || cout > kMaxC || kThreads % (cout / 8))
+    return fail(N2F_ERR_ARG, "conv_first: cout %d", cout);
   if (ylo && !y) return fail(N2F_ERR_ARG, "conv_first: tf32 residual needs y");
-  const int64_t total = (int64_t)h * w_ * (cout / 4);
-  k_conv_first<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+  if (h > 65535) return fail(N2F_ERR_ARG, "conv_first: height %d", h);
+  const int ppb = kThreads / (cout / 8);
+  k_conv_first<<<dim3((unsigned)((w_ + ppb - 1) / ppb), (unsigned)h), kThreads, 0, st>>>(
       x, w, b, y, ylo, h, w_, cout, relu, reinterpret_cast<__half*>(yh16),
       reinterpret_cast<__half*>(yl16), oscale);
   N2F_LAUNCH_CHECK();
@@ -403,9 +435,10 @@ int wgrad_nsplit(int64_t pixels, int cin, int cout) {
   const int64_t tiles =
       (cin == 1) ? 1 : (int64_t)((cout + bm - 1) / bm) * ((9 * cin + bn - 1) / bn);
   int64_t want = (4 * 148 + tiles - 1) / tiles;
-  // the first layer's wgrad (one tile) is latency-bound: more, smaller splits
-  int64_t maxs = (pixels + (cin == 1 ? 127 : 511)) / (cin == 1 ? 128 : 512);
-  if (cin == 1) want = 8 * 148;
+  // the first layer's wgrad (k_wgrad_first): one block per ~512 pixels (8
+  // warps x two 32-pixel segments), at most 2048 blocks
+  int64_t maxs = (pixels + (cin == 1 ? 511 : 511)) / 512;
+  if (cin == 1) want = 2048;
   int64_t n = want < maxs ? want : maxs;
   if (n < 1) n = 1;
   if (n > 1024) n = 1024;
@@ -437,10 +470,11 @@ int wgrad3x3_simt(const float* g, const float* x, float* dw_part, float* db_part
 
 int wgrad_first_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
                      int cout, int nsplit, cudaStream_t st) {
-  if (kThreads % cout) return fail(N2F_ERR_ARG, "wgrad_first: cout %d", cout);
-  const int P = h * w;
-  const int chunk = (P + nsplit - 1) / nsplit;
-  k_wgrad_first<<<nsplit, kThreads, 0, st>>>(g, x, dw_part, db_part, h, w, cout, chunk);
+  if (cout != 32) return fail(N2F_ERR_ARG, "wgrad_first: cout %d", cout);
+  const int64_t nunits = (int64_t)h * ((w + kFirstSeg - 1) / kFirstSeg);
+  const int64_t warps = (int64_t)nsplit * (kThreads / 32);
+  const int upw = (int)((nunits + warps - 1) / warps);
+  k_wgrad_first<<<nsplit, kThreads, 0, st>>>(g, x, dw_part, db_part, h, w, upw);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

@@ -35,9 +35,18 @@
 #ifndef N2F_DY256_EC32
 #define N2F_DY256_EC32 1
 #endif
+// -DN2F_DY_STACK=0: dy kernels with N <= 128 issue 3 MMAs per K step (no
+// N-stacked weight parts)
+#ifndef N2F_DY_STACK
+#define N2F_DY_STACK 0
+#endif
 // -DN2F_DY_KC16=1: 16-channel K chunks for N = 256 (experiment)
 #ifndef N2F_DY_KC16
 #define N2F_DY_KC16 0
+#endif
+// stages (32 pixels each) per accumulation group of the FP16 pair wgrad
+#ifndef N2F_WG_GROUP_PAIR
+#define N2F_WG_GROUP_PAIR 4
 #endif
 #ifndef N2F_TC_TRACE
 #define N2F_TC_TRACE 0
@@ -123,6 +132,31 @@ __device__ __forceinline__ void drain_add(uint32_t taddr, float (&acc)[HALF]) {
 #pragma unroll
       for (int j = 0; j < CH; j += 2)
         add2(acc[(c + p) * CH + j], acc[(c + p) * CH + j + 1], r[p][j], r[p][j + 1]);
+  }
+}
+
+// Load this warp's 32 lanes x HALF accumulator columns at taddr (a tile that
+// accumulated its whole K loop in TMEM), two tcgen05.ld in flight per wait.
+template <int HALF>
+__device__ __forceinline__ void tmem_load_all(uint32_t taddr, float (&acc)[HALF]) {
+  constexpr int CH = HALF < 32 ? HALF : 32;
+  constexpr int NB = HALF / CH;
+  constexpr int PB = NB >= 2 ? 2 : 1;
+#pragma unroll
+  for (int c = 0; c < NB; c += PB) {
+    uint32_t r[PB][32];
+#pragma unroll
+    for (int p = 0; p < PB; ++p) {
+      if (CH == 16)
+        tmem_ld16(taddr + (c + p) * CH, r[p]);
+      else
+        tmem_ld32(taddr + (c + p) * CH, r[p]);
+    }
+    tmem_ld_wait();
+#pragma unroll
+    for (int p = 0; p < PB; ++p)
+#pragma unroll
+      for (int j = 0; j < CH; ++j) acc[(c + p) * CH + j] = __uint_as_float(r[p][j]);
   }
 }
 
@@ -739,9 +773,17 @@ struct DyCfg {
   static constexpr int kDxUnits = (8 * kRow) >> 4;    // a dx shift: 8 rows, descriptor units
   static constexpr int kRowsA = 18 * 8;               // halo columns x rows
   static constexpr int kStageA = kRowsA * kRow;       // one fp16 part (hi or lo)
-  static constexpr int kTapB = (BN / 2) * kRow;       // this CTA's weight rows of one tap
+  // N-stacked weight parts (N <= 128): the pair's B operand is [w_hi; w_lo]
+  // (2N rows: CTA 0 stages all of w_hi, CTA 1 all of w_lo), so one MMA per
+  // activation part yields (x_part . w_hi | x_part . w_lo) side by side in
+  // TMEM: 2 MMAs per K step instead of 3 (the activation operand, which the
+  // tensor core reads from smem at ~64 B/clk, bounds these narrow MMAs), and
+  // the epilogue adds the two column halves (the lo . lo term comes free)
+  static constexpr bool kStack = N2F_DY_STACK && BN <= 128;
+  static constexpr int kTapB = (kStack ? BN : BN / 2) * kRow;  // this CTA's weight rows of one tap
   static constexpr int kStageB = 3 * kTapB;           // the three dx taps
-  static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
+  static constexpr int kStageBytes = 2 * kStageA + (kStack ? 1 : 2) * kStageB;
+  static constexpr int kCols = kStack ? 2 * BN : BN;  // TMEM columns of one accumulator
   // staging slices: 32 channels (one fence + TMA issue per 32) where smem
   // allows, 16 for BN = 256 (whose three 66 KB dy stages fill the rest)
   static constexpr int kEpiCols = (BN == 256 && !N2F_DY256_EC32) ? 16 : (BN / 2 < 32 ? BN / 2 : 32);
@@ -752,8 +794,15 @@ struct DyCfg {
   static constexpr int kMaxStages = (218 * 1024 - kEpiBytes - 1024) / kStageBytes;
   static constexpr int kStages = kMaxStages > 8 ? 8 : kMaxStages;
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
-  static constexpr int kBufs = 512 / BN > 4 ? 4 : 512 / BN;  // TMEM group buffers
-  static constexpr int kTmemCols = kBufs * BN;
+  static constexpr int kBufs = 512 / kCols > 4 ? 4 : 512 / kCols;  // TMEM group buffers
+  // accumulation groups per tile: each group (a run of consecutive K stages)
+  // accumulates in a fresh TMEM buffer and is added into fp32 registers with
+  // round-to-nearest, bounding the tensor core's truncating accumulation to
+  // K / kGroupsPerTile.  The MMAs run kBufs groups ahead of the accumulate
+  // warps, so (kBufs / kGroupsPerTile) of a tile's MMA time hides that tile's
+  // predecessor's epilogue: 2/3 of a tile for N = 256, a whole tile below.
+  static constexpr int kGroupsPerTile = BN >= 256 ? 3 : 4;
+  static constexpr int kTmemCols = kBufs * kCols;
   static constexpr int kHalf = BN / 2;
 };
 
@@ -765,10 +814,13 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
                  const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
                  const __grid_constant__ CUtensorMap myl, int omask, float oscale, ConvOut out,
-                 int direct, const float* __restrict__ bias, const void* __restrict__ mask,
+                 int flags, const float* __restrict__ bias, const void* __restrict__ mask,
                  int mask_bits, uint32_t* __restrict__ mbits_out, float* __restrict__ colsum,
                  float unscale, int H, int W, int C, int epi, HeadTrainArgs ht, HeadValArgs hv) {
   using Cfg = DyCfg<BN>;
+  // flags: bit 0 direct stores (experiment); bits 8.. groups per tile
+  // (experiment override, 0 = DyCfg::kGroupsPerTile)
+  const bool direct = flags & 1;
   using P = Prec<true>;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
@@ -789,9 +841,9 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
   const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
   const int tiles_x = (W + 31) / 32;
   const int nunits = tiles_x * ((H + 7) / 8);
-  constexpr int G = Cfg::kGroup;
   const int KB = 3 * (C / Cfg::kKC);  // stages per tile
-  const int NG = KB / G;              // accumulation groups per tile
+  const int gpt_req = (flags >> 8) ? (flags >> 8) : Cfg::kGroupsPerTile;
+  const int NG = KB < gpt_req ? KB : gpt_req;  // accumulation groups per tile
 
   if (tid == 0) {
     if (HEAD == 1 && blockIdx.x == 0 && ht.step_counter) *ht.step_counter += 1;  // Adam t
@@ -837,8 +889,12 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
           if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
           tma_load_3d_2sm(st, &mx, fb, c0, y0 + dy - 1, x0 - 1);
           tma_load_3d_2sm(st + Cfg::kStageA, &mxl, fb, c0, y0 + dy - 1, x0 - 1);
-          tma_load_4d_2sm(st + 2 * Cfg::kStageA, &mw, fb, c0, n0, 0, dy);
-          tma_load_4d_2sm(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, fb, c0, n0, 0, dy);
+          if (Cfg::kStack) {  // CTA 0: w_hi rows, CTA 1: w_lo rows (all N of them)
+            tma_load_4d_2sm(st + 2 * Cfg::kStageA, rank == 0 ? &mw : &mwl, fb, c0, 0, 0, dy);
+          } else {
+            tma_load_4d_2sm(st + 2 * Cfg::kStageA, &mw, fb, c0, n0, 0, dy);
+            tma_load_4d_2sm(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, fb, c0, n0, 0, dy);
+          }
         }
         __syncwarp();
       }
@@ -846,7 +902,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
   } else if (warp == 1) {
     // ---- MMA issuer (the leader issues for the pair): one stage = one group
     if (rank == 0) {
-      constexpr uint32_t idesc = P::idesc(256, BN, false, false);
+      constexpr uint32_t idesc = P::idesc(256, Cfg::kCols, false, false);
       constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
                          kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4, kTap = Cfg::kTapB >> 4;
       const uint64_t desc0 = sw128_desc(smem_u32(base), 16, 8 * Cfg::kRow, Cfg::kLayout);
@@ -862,51 +918,59 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
 #endif
           if (gg >= NB) mbar_wait(&tempty[b], ((gg / NB) - 1) & 1);
 #if N2F_TC_TRACE
-          const long long c1 = clock64();
+          we_ += clock64() - c0;
 #endif
-          for (int j = 0; j < G; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
+          const uint32_t d = taddr + b * Cfg::kCols;
+          const int s0 = g * KB / NG, s1 = (g + 1) * KB / NG;
+          // stage by stage (the MMAs stream behind the TMA): the stage's cross
+          // terms, then its hi*hi; a dx shift is 8 rows (one swizzle atom), a
+          // K step 32 B = 2 descriptor units; the group's first MMA starts
+          // its TMEM buffer from zero
+          for (int kb = s0; kb < s1; ++kb, ++it) {
+            const int st = it % S;
 #if N2F_TC_TRACE
-          we_ += c1 - c0;
-          wf_ += clock64() - c1;
+            const long long c1 = clock64();
 #endif
-          tc_fence_after();
-          if (elect_one_sync()) {
-            const uint32_t d = taddr + b * BN;
-            uint64_t a0[G];
+            mbar_wait(&full[st], (it / S) & 1);
+#if N2F_TC_TRACE
+            wf_ += clock64() - c1;
+#endif
+            tc_fence_after();
+            if (elect_one_sync()) {
+              const uint64_t a0 = desc0 + (uint64_t)(st * (Cfg::kStageBytes >> 4));
+              if (Cfg::kStack) {  // x_lo . [w_hi; w_lo], then x_hi . [w_hi; w_lo]
 #pragma unroll
-            for (int j = 0; j < G; ++j)
-              a0[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
-            // cross terms of the whole group first, then hi*hi; a dx shift is
-            // 8 rows (one swizzle atom), a K step 32 B = 2 descriptor units
+                for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
-            for (int j = 0; j < G; ++j) {
+                  for (int k = 0; k < Cfg::kKSteps; ++k)
+                    mma_f16_2sm(d, a0 + kAl + Cfg::kDxUnits * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k,
+                                idesc, ((kb - s0) | dx | k) != 0);
+                }
+              } else {
 #pragma unroll
-              for (int dx = 0; dx < 3; ++dx) {
+                for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
-                for (int k = 0; k < Cfg::kKSteps; ++k) {
-                  const uint64_t a = a0[j] + Cfg::kDxUnits * dx + 2 * k;
-                  const uint64_t bh = a0[j] + kBh + kTap * dx + 2 * k;
-                  mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, (j | dx | k) != 0);
-                  mma_f16_2sm(d, a + kAl, bh, idesc, 1);
+                  for (int k = 0; k < Cfg::kKSteps; ++k) {
+                    const uint64_t a = a0 + Cfg::kDxUnits * dx + 2 * k;
+                    const uint64_t bh = a0 + kBh + kTap * dx + 2 * k;
+                    mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | dx | k) != 0);
+                    mma_f16_2sm(d, a + kAl, bh, idesc, 1);
+                  }
                 }
               }
-            }
-#pragma unroll
-            for (int j = 0; j < G; ++j) {
 #pragma unroll
               for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
                 for (int k = 0; k < Cfg::kKSteps; ++k)
-                  mma_f16_2sm(d, a0[j] + Cfg::kDxUnits * dx + 2 * k,
-                              a0[j] + kBh + kTap * dx + 2 * k, idesc, 1);
+                  mma_f16_2sm(d, a0 + Cfg::kDxUnits * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k,
+                              idesc, 1);
               }
+              mma_commit_2sm(&empty[st]);
             }
-#pragma unroll
-            for (int j = 0; j < G; ++j) mma_commit_2sm(&empty[(it + j) % S]);
-            mma_commit_2sm(&tfull[b]);
+            __syncwarp();
           }
+          if (elect_one_sync()) mma_commit_2sm(&tfull[b]);
           __syncwarp();
-          it += G;
         }
       }
 #if N2F_TC_TRACE
@@ -955,7 +1019,11 @@ __global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 
         tw += c1 - c0;
 #endif
         tc_fence_after();
-        drain_add<HALF>(lane_base + b * BN, acc);
+        if (g == 0)
+          tmem_load_all<HALF>(lane_base + b * Cfg::kCols, acc);
+        else
+          drain_add<HALF>(lane_base + b * Cfg::kCols, acc);
+        if (Cfg::kStack) drain_add<HALF>(lane_base + b * Cfg::kCols + BN, acc);  // x . w_lo half
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty0 + 8u * b);
@@ -1317,7 +1385,10 @@ struct WgCfg {
   static constexpr int kStageB = (BN / CS / 32) * kBlk;
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
   static constexpr bool kTwoPerSm = CS == 1 && BN <= 64 && SEG == 32;
-  static constexpr int kGroup = SEG == 64 ? 1 : P::kGroup;
+  // stages per TMEM accumulation group.  A group's drain reads BN fp32
+  // columns x 128 lanes from TMEM (~64 B/clk): the pair kernels (N >= 128)
+  // take 4 stages (128 pixels) so the MMAs of a group outlast its drain
+  static constexpr int kGroup = SEG == 64 ? 1 : (F16 && CS == 2 ? N2F_WG_GROUP_PAIR : P::kGroup);
   static constexpr int kMaxStages = (200 * 1024) / kStageBytes;
   static constexpr int kStages = kTwoPerSm ? 2 * P::kGroup : (kMaxStages > 8 ? 8 : kMaxStages);
   static constexpr int kSmem = kStages * kStageBytes + 1024;
@@ -1483,46 +1554,43 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
         we_ += c1 - c0;
 #endif
         const int ng = (g + 1) * G <= KB ? G : KB - g * G;
-        for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
+        const uint32_t d = taddr + b * BN;
 #if N2F_TC_TRACE
         const long long c2 = clock64();
-        wf_ += c2 - c1;
 #endif
-        tc_fence_after();
-        if (elect_one_sync()) {
-          const uint32_t d = taddr + b * BN;
-          uint64_t ah[G];
+        // stage by stage (the group's MMAs stream behind the TMA): cross terms
+        // of the stage, then its hi*hi; one K step = 1 KB = 64 descriptor units
+        for (int j = 0; j < ng; ++j) {
+          const int st = (it + j) % S;
+#if N2F_TC_TRACE
+          const long long w0 = clock64();
+#endif
+          mbar_wait(&full[st], ((it + j) / S) & 1);
+#if N2F_TC_TRACE
+          wf_ += clock64() - w0;
+#endif
+          tc_fence_after();
+          if (elect_one_sync()) {
+            const uint64_t ah = desc0 + (uint64_t)(st * (Cfg::kStageBytes >> 4));
 #pragma unroll
-          for (int j = 0; j < G; ++j)
-            ah[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
-          // cross terms of the group first, then hi*hi; one K step = 1 KB = 64 units
-#pragma unroll
-          for (int j = 0; j < G; ++j) {
-            if (j < ng) {
-#pragma unroll
-              for (int k = 0; k < Cfg::kKSteps; ++k) {
-                const uint64_t a = ah[j] + 64 * k;
-                P::template mma<CS>(d, a, a + kBl, idesc, (j | k) != 0);
-                P::template mma<CS>(d, a + kAl, a + kBh, idesc, 1);
-              }
+            for (int k = 0; k < Cfg::kKSteps; ++k) {
+              const uint64_t a = ah + 64 * k;
+              P::template mma<CS>(d, a, a + kBl, idesc, (j | k) != 0);
+              P::template mma<CS>(d, a + kAl, a + kBh, idesc, 1);
             }
-          }
 #pragma unroll
-          for (int j = 0; j < G; ++j) {
-            if (j < ng) {
-#pragma unroll
-              for (int k = 0; k < Cfg::kKSteps; ++k) {
-                const uint64_t a = ah[j] + 64 * k;
-                P::template mma<CS>(d, a, a + kBh, idesc, 1);
-              }
+            for (int k = 0; k < Cfg::kKSteps; ++k) {
+              const uint64_t a = ah + 64 * k;
+              P::template mma<CS>(d, a, a + kBh, idesc, 1);
             }
-          }
-          for (int j = 0; j < ng; ++j) {
             if (CS == 2)
-              mma_commit_2sm(&empty[(it + j) % S]);
+              mma_commit_2sm(&empty[st]);
             else
-              mma_commit(&empty[(it + j) % S]);
+              mma_commit(&empty[st]);
           }
+          __syncwarp();
+        }
+        if (elect_one_sync()) {
           if (CS == 2)
             mma_commit_2sm(&tfull[b]);
           else
@@ -1821,13 +1889,14 @@ int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, fl
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  static const int direct = [] {
+  static const int flags = [] {
     const char* e = getenv("N2F_DY_DIRECT");
-    return e ? atoi(e) : 0;
+    const char* g = getenv("N2F_DY_GROUPS");  // accumulation groups per tile (experiment)
+    return (e && atoi(e) ? 1 : 0) | ((g ? atoi(g) : 0) << 8);
   }();
   N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN, HEAD>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
                               pl.myh, pl.myl, pl.omask, pl.oscale,
-                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, HEAD ? 0 : direct, bias, mask,
+                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, HEAD ? (flags & ~1) : flags, bias, mask,
                               pl.mask_bits, pl.mbits_out, colsum, pl.unscale, pl.H, pl.W, pl.C, epi,
                               ht, hv));
   N2F_LAUNCH_CHECK();
@@ -1949,8 +2018,9 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
     const int kc = N2F_DY_KC16 && N == 256 ? 16 : 32;  // DyCfg<N>::kKC
     N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, kc, 8, 18));
     N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, kc, 8, 18));
-    N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, kc, N / 2));
-    N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, kc, N / 2));
+    const int wrows = (N2F_DY_STACK && N <= 128) ? N : N / 2;  // DyCfg<N>::kStack
+    N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, kc, wrows));
+    N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, kc, wrows));
     return N2F_OK;
   }
   // wide layers (N >= 128) run as CTA pairs (cta_group::2, M = 256: each CTA

@@ -121,8 +121,6 @@ struct n2f_ctx {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   int bias_tiles[2]{};
-  float* grad_red = nullptr;
-  ColReduceArgs grad_reduce[3]{};  // [0,1] tcgen05 shape classes, [2] SIMT path
   int wsplit[2][kLayers]{};
   int last_sc = 0;  // shape class of the last enqueued step (parity readback)
 };
@@ -245,7 +243,6 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
   }
   PROF(kPWgradFirst, 0, conv_flop(P, 0),
        wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
-  PROF(kPAdam, 0, 0.0, launch_col_reduce(c->grad_reduce[sc], st));
   PROF(kPAdam, 0, 0.0, launch_adam(c->adam_sc[sc], c->step_counter, 0, st));
   return N2F_OK;
 }
@@ -306,7 +303,6 @@ int enqueue_step(n2f_ctx* c, int k) {
     gn = t;
   }
   N2F_TRY(wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
-  N2F_TRY(launch_col_reduce(c->grad_reduce[2], st));
   N2F_TRY(launch_adam(c->adam, c->step_counter, 0, st));
   return N2F_OK;
 }
@@ -370,27 +366,16 @@ int build_graph(n2f_ctx* c) {
   return N2F_OK;
 }
 
-// Move the tall partial matrices (many split-K rows over few columns: per-tile
-// bias sums, the head, the first layer) onto a k_col_reduce pass (output slot =
-// the tensor's arena offset in grad_red); wide ones (the wgrad partials of the
-// 3x3 layers) are summed inline by Adam, one coalesced column per thread.
-constexpr int kMaxInlineSplits = 32, kMaxInlineSplitsWide = 256;
-int route_reductions(n2f_ctx* c, AdamArgs& a, ColReduceArgs& r) {
-  r.n = 0;
-  r.prefix[0] = 0;
-  for (int q = 0; q < a.ntensors; ++q) {
-    AdamTensor& T = a.t[q];
-    if (T.nsplit <= kMaxInlineSplits || (T.n >= 4096 && T.nsplit <= kMaxInlineSplitsWide)) continue;
-    if (r.n == kMaxColReduce) return fail(N2F_ERR_ARG, "too many reductions");
-    ColReduce& t = r.t[r.n];
-    t.part = T.part;
-    t.out = c->grad_red + T.off;
-    t.rows = T.nsplit;
-    t.cols = (int)T.n;
-    r.prefix[r.n + 1] = r.prefix[r.n] + (int)((T.n + 31) / 32);
-    ++r.n;
-    T.part = c->grad_red + T.off;
-    T.nsplit = 1;
+// Reduction plan of an Adam descriptor (k_adam sums the split-K partials
+// itself) plus its slab scratch and self-resetting arrival counters.
+int plan_adam(n2f_ctx* c, AdamArgs& a) {
+  adam_plan(a);
+  a.scratch = nullptr;
+  a.counters = nullptr;
+  if (a.scr_total) N2F_TRY(dalloc(c, &a.scratch, (size_t)a.scr_total));
+  if (a.cnt_total) {
+    N2F_TRY(dalloc(c, &a.counters, (size_t)a.cnt_total));
+    N2F_CUDA(cudaMemset(a.counters, 0, (size_t)a.cnt_total * sizeof(int)));
   }
   return N2F_OK;
 }
@@ -673,13 +658,9 @@ int setup(n2f_ctx* c) {
       }
     }
   }
-  // Tensors with many split-K partials (per-tile bias sums, the head, the
-  // first layer) are reduced by one parallel k_col_reduce launch into
-  // grad_red before Adam, which then reads a single partial.
-  N2F_TRY(dalloc(c, &c->grad_red, c->ptotal));
-  N2F_TRY(route_reductions(c, c->adam, c->grad_reduce[2]));
+  N2F_TRY(plan_adam(c, c->adam));
   if (c->tc) {
-    for (int sc = 0; sc < 2; ++sc) N2F_TRY(route_reductions(c, c->adam_sc[sc], c->grad_reduce[sc]));
+    for (int sc = 0; sc < 2; ++sc) N2F_TRY(plan_adam(c, c->adam_sc[sc]));
   }
 
   N2F_CUDA(cudaMallocHost(&c->h_mm, 4 * sizeof(double)));

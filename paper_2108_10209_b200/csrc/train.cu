@@ -194,41 +194,97 @@ __global__ void __launch_bounds__(kThreads)
 
 // ---------------------------------------------------------------------------
 // Multi-tensor Adam (tensor.py:125-141) with the split-K gradient reduction
-// fused in (fixed summation order), and the dgrad-transposed weight copy.
+// fused in, and the derived operand copies.  Each block reduces one (tensor,
+// column chunk, row slab) rectangle of the [nsplit][n] partials: rl row lanes
+// x cw columns, every lane summing its rows in a fixed order, lanes combined
+// in a fixed order; tensors with several slabs park slab sums in scratch and
+// the last-arriving block of the chunk adds them in slab order (the result
+// does not depend on block scheduling: deterministic).  Then Adam with
 // NumPy-2 semantics: every Python-float scalar is rounded to fp32 first and
 // each operation is rounded separately (no FMA contraction).
 // ---------------------------------------------------------------------------
+constexpr int kAdamRowsPerLane = 16;
+
 __global__ void __launch_bounds__(kThreads)
     k_adam(AdamArgs args, const int* __restrict__ step_counter, int fixed_t) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= args.total) return;
-  int tl = 0, th = args.ntensors - 1;  // the tensor holding parameter i (binary search)
+  __shared__ float red[kThreads];
+  __shared__ int last;
+  const int blk = blockIdx.x;
+  int tl = 0, th = args.ntensors - 1;  // the tensor owning this block (binary search)
   while (tl < th) {
     const int mid = (tl + th + 1) >> 1;
-    if (i >= args.t[mid].off)
+    if (blk >= args.t[mid].blk0)
       tl = mid;
     else
       th = mid - 1;
   }
   const AdamTensor& T = args.t[tl];
-  const int64_t j = i - T.off;
-  // fixed-order sum of the split-K partials; four independent loads in flight
-  const float* __restrict__ part = T.part + j;
-  float g = __ldg(part);
-  int s = 1;
-  for (; s + 3 < T.nsplit; s += 4) {
-    const float a0 = __ldg(part + (int64_t)s * T.n), a1 = __ldg(part + (int64_t)(s + 1) * T.n);
-    const float a2 = __ldg(part + (int64_t)(s + 2) * T.n), a3 = __ldg(part + (int64_t)(s + 3) * T.n);
-    g += a0;
-    g += a1;
-    g += a2;
-    g += a3;
+  const int local = blk - T.blk0;
+  const int chunk = local / T.ns, slab = local - chunk * T.ns;
+  const int cw = T.cw, rl = T.rl;
+  const int c = threadIdx.x % cw, r = threadIdx.x / cw;
+  const int64_t j = (int64_t)chunk * cw + c;
+  const bool colok = j < T.n;
+  const int rb = slab * kAdamRowsPerLane * rl;
+  const int re = min(T.nsplit, rb + kAdamRowsPerLane * rl);
+  // the Adam lanes fetch their moments and parameter while the partials load
+  const int64_t i = T.off + j;
+  const bool upd = r == 0 && colok;
+  float m = 0.f, v = 0.f, p = 0.f;
+  if (upd && T.ns == 1) {
+    m = args.m[i];
+    v = args.v[i];
+    p = args.p[i];
   }
-  for (; s < T.nsplit; ++s) g += __ldg(part + (int64_t)s * T.n);
+  float s = 0.f;
+  if (colok) {
+    // all (<= 16) partial rows of this lane in flight at once, then summed
+    // in row order
+    const float* __restrict__ part = T.part + j + (int64_t)(rb + r) * T.n;
+    const int64_t stride = (int64_t)rl * T.n;
+    const int nr = (re - rb - r + rl - 1) / rl;
+    float x[kAdamRowsPerLane];
+#pragma unroll
+    for (int q = 0; q < kAdamRowsPerLane; ++q) x[q] = q < nr ? __ldg(part + q * stride) : 0.f;
+    s = x[0];
+#pragma unroll
+    for (int q = 1; q < kAdamRowsPerLane; ++q)
+      if (q < nr) s += x[q];
+  }
+  float g = s;
+  if (rl > 1) {
+    red[threadIdx.x] = s;
+    __syncthreads();
+    if (r == 0)
+      for (int k = 1; k < rl; ++k) g += red[k * cw + c];
+  }
+  if (T.ns > 1) {
+    if (r == 0 && colok) args.scratch[T.scr0 + (int64_t)slab * T.n + j] = g;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int prev = atomicAdd(args.counters + T.cnt0 + chunk, 1);
+      last = prev == T.ns - 1;
+      if (last) args.counters[T.cnt0 + chunk] = 0;  // self-reset for the next launch
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (r == 0 && colok) {
+      const float* sc = args.scratch + T.scr0 + j;
+      g = __ldcg(sc);
+      for (int q = 1; q < T.ns; ++q) g += __ldcg(sc + (int64_t)q * T.n);
+    }
+  }
+  if (!upd) return;
+  if (T.ns > 1) {
+    m = args.m[i];
+    v = args.v[i];
+    p = args.p[i];
+  }
   const int t = step_counter ? *step_counter : fixed_t;
   const int ti = (t < args.table_len ? t : args.table_len) - 1;
   const float bc1 = args.bc1[ti], bc2 = args.bc2[ti];
-  float m = args.m[i], v = args.v[i], p = args.p[i];
   m = __fmul_rn(m, args.beta1);
   m = __fadd_rn(m, __fmul_rn(args.one_minus_beta1, g));
   v = __fmul_rn(v, args.beta2);
@@ -249,52 +305,17 @@ __global__ void __launch_bounds__(kThreads)
     args.plo16[i] = l16;
   }
   if (T.wt || T.wth16) {  // wt[c][8-tap][o] = w[o][tap][c]
-    const int c = (int)(j % T.cin);
-    const int tap = (int)((j / T.cin) % 9);
-    const int o = (int)(j / ((int64_t)T.cin * 9));
-    const int64_t q = ((int64_t)c * 9 + (8 - tap)) * T.cout + o;
+    const int jj = (int)j;
+    const int cc = jj % T.cin;
+    const int tap = (jj / T.cin) % 9;
+    const int o = jj / (T.cin * 9);
+    const int64_t q = ((int64_t)cc * 9 + (8 - tap)) * T.cout + o;
     if (T.wt) T.wt[q] = p;
     if (T.wtlo) T.wtlo[q] = lo;
     if (T.wth16) {
       T.wth16[q] = h16;
       T.wtl16[q] = l16;
     }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Column sums of per-tile partials [rows][cols] for several tensors in one
-// launch (the bias gradients): block = (tensor, 32-column chunk), 32 row
-// lanes x 32 columns, fixed-order tree over the row lanes (deterministic).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_col_reduce(ColReduceArgs a) {
-  __shared__ float sm[32][33];
-  const int b = blockIdx.x;
-  int k = 0;
-  while (k + 1 < a.n && b >= a.prefix[k + 1]) ++k;
-  const ColReduce& T = a.t[k];
-  const int col = (b - a.prefix[k]) * 32 + (threadIdx.x & 31);
-  const int r0 = threadIdx.x >> 5;
-  float s = 0.f;
-  if (col < T.cols) {  // fixed order; four independent loads in flight
-    const float* __restrict__ pc = T.part + col;
-    int r = r0;
-    for (; r + 96 < T.rows; r += 128) {
-      const float a0 = __ldg(pc + (int64_t)r * T.cols), a1 = __ldg(pc + (int64_t)(r + 32) * T.cols);
-      const float a2 = __ldg(pc + (int64_t)(r + 64) * T.cols), a3 = __ldg(pc + (int64_t)(r + 96) * T.cols);
-      s += a0;
-      s += a1;
-      s += a2;
-      s += a3;
-    }
-    for (; r < T.rows; r += 32) s += __ldg(pc + (int64_t)r * T.cols);
-  }
-  sm[r0][threadIdx.x & 31] = s;
-  __syncthreads();
-  if (r0 == 0 && col < T.cols) {
-    float t = sm[0][threadIdx.x];
-    for (int q = 1; q < 32; ++q) t += sm[q][threadIdx.x];
-    T.out[col] = t;
   }
 }
 
@@ -477,16 +498,37 @@ int launch_head_val(const float* a8, const float* w9, const float* b9, const flo
   return N2F_OK;
 }
 
-int launch_adam(const AdamArgs& args, const int* step_counter, int fixed_t, cudaStream_t st) {
-  k_adam<<<(unsigned)((args.total + kThreads - 1) / kThreads), kThreads, 0, st>>>(args, step_counter,
-                                                                                   fixed_t);
-  N2F_LAUNCH_CHECK();
-  return N2F_OK;
+void adam_plan(AdamArgs& a) {
+  int blk = 0, cnt = 0;
+  int64_t scr = 0;
+  for (int q = 0; q < a.ntensors; ++q) {
+    AdamTensor& T = a.t[q];
+    const int ns_rows = T.nsplit < 1 ? 1 : T.nsplit;
+    int rl = 1;
+    while (rl < 32 && ns_rows > kAdamRowsPerLane * rl) rl <<= 1;
+    T.rl = rl;
+    T.cw = kThreads / rl;
+    T.ns = (ns_rows + kAdamRowsPerLane * rl - 1) / (kAdamRowsPerLane * rl);
+    T.nchunk = (int)((T.n + T.cw - 1) / T.cw);
+    T.blk0 = blk;
+    blk += T.nchunk * T.ns;
+    T.cnt0 = cnt;
+    T.scr0 = scr;
+    if (T.ns > 1) {
+      cnt += T.nchunk;
+      scr += (int64_t)T.ns * T.n;
+    }
+  }
+  a.nblocks = blk;
+  a.cnt_total = cnt;
+  a.scr_total = scr;
 }
 
-int launch_col_reduce(const ColReduceArgs& a, cudaStream_t st) {
-  if (a.n == 0) return N2F_OK;
-  k_col_reduce<<<a.prefix[a.n], 1024, 0, st>>>(a);
+int launch_adam(const AdamArgs& args, const int* step_counter, int fixed_t, cudaStream_t st) {
+  if (args.nblocks < 1) return fail(N2F_ERR_ARG, "launch_adam: no plan (adam_plan)");
+  if (args.cnt_total && (!args.scratch || !args.counters))
+    return fail(N2F_ERR_ARG, "launch_adam: plan needs scratch and counters");
+  k_adam<<<(unsigned)args.nblocks, kThreads, 0, st>>>(args, step_counter, fixed_t);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

@@ -68,6 +68,11 @@ struct AdamTensor {
   __half* wth16;      // optional fp16 pair of the dgrad-transposed copy (scaled)
   __half* wtl16;
   int cin, cout;
+  // reduction plan (adam_plan): rl row lanes x cw columns per block, ns row
+  // slabs of <= 16 rl partial rows (slab sums combined by the last block of a
+  // column chunk through scratch + an arrival counter), blocks [blk0, ...)
+  int rl, cw, ns, nchunk, blk0, cnt0;
+  int64_t scr0;
 };
 
 constexpr int kMaxTensors = 18;
@@ -87,20 +92,16 @@ struct AdamArgs {
   const float* bc2;
   int table_len;
   float beta1, one_minus_beta1, beta2, one_minus_beta2, lr, eps;
+  int nblocks;         // set by adam_plan
+  int64_t scr_total;   // floats of slab scratch the plan needs
+  int cnt_total;       // arrival counters the plan needs (zeroed once; self-resetting)
+  float* scratch;
+  int* counters;
 };
 
-struct ColReduce {
-  const float* part;  // [rows][cols]
-  float* out;         // [cols]
-  int rows, cols;
-};
-constexpr int kMaxColReduce = 16;
-struct ColReduceArgs {
-  ColReduce t[kMaxColReduce];
-  int n;
-  int prefix[kMaxColReduce + 1];  // block offsets: tensor k owns blocks [prefix[k], prefix[k+1])
-};
-int launch_col_reduce(const ColReduceArgs& a, cudaStream_t st);
+// Fill the reduction plan of every tensor (needs t[].n / nsplit) and the
+// scratch / counter sizes; the caller allocates scratch and zeroed counters.
+void adam_plan(AdamArgs& a);
 
 int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
                       float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
