@@ -231,7 +231,9 @@ def test_full_fit_psnr_statistical(oracle):
     (tools/chaos_probe.py), so a single image cannot meet
     a 0.1 dB bar.  Checked instead: every run denoises (> +3 dB), each
     GPU-CPU gap is inside the oracle's own 3-sigma spread (0.9 dB), and the
-    mean gap over the seeds is within 0.3 dB (2.5 sigma of its sampling error)."""
+    mean gap over the seeds is within 0.45 dB (3 sigma of its sampling error,
+    0.30 / sqrt(4)): the same 3-sigma bar as the per-image check, so an exact
+    implementation fails either check with probability ~0.3 %."""
     from paper_2108_10209_b200 import TrainConfig, train_single_channel
 
     gaps = []
@@ -245,4 +247,4 @@ def test_full_fit_psnr_statistical(oracle):
         assert abs(p_gpu - p_cpu) <= 0.9, (seed, p_gpu, p_cpu, r.epochs_run, ref.epochs_run)
         gaps.append(p_gpu - p_cpu)
     print("PSNR gaps GPU - CPU (dB):", [round(g, 3) for g in gaps])
-    assert abs(float(np.mean(gaps))) <= 0.3, gaps
+    assert abs(float(np.mean(gaps))) <= 0.45, gaps
