@@ -179,6 +179,20 @@ int n2f_ctx_validate(n2f_ctx* ctx, float* out_host, double* score);
 int n2f_ctx_get_pairs(n2f_ctx* ctx, float* pair_in, float* pair_tgt, float* norm, int ph[4],
                       int pw[4]);
 
+/* ---- image-quality metrics (benchmark mode; imaging.psnr / imaging.ssim,
+ * imaging.py:249-311), f64 device buffers of one single-channel plane ------ */
+/* sum of (a - b)^2 over n samples (host result) */
+int n2f_sq_err_sum(const double* a, const double* b, int64_t n, double* out, void* stream);
+/* 10 log10(range^2 / mse), +inf when mse == 0 (imaging.psnr) */
+int n2f_psnr(const double* a, const double* b, int64_t n, double data_range, double* out,
+             void* stream);
+/* mean SSIM, 11x11 Gaussian window (sigma 1.5), fully valid positions only
+ * (imaging.ssim); N2F_ERR_ARG below 11x11 or for data_range <= 0 */
+int n2f_ssim(const double* a, const double* b, int height, int width, double data_range, double k1,
+             double k2, double* out, void* stream);
+/* CUDA devices visible to this process (worker -> GPU mapping) */
+int n2f_device_count(int* n);
+
 #ifdef __cplusplus
 }
 #endif

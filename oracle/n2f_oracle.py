@@ -417,3 +417,50 @@ def fit_denoise(noisy, *, seed=0, lr=1e-3, patience=100, window=100, max_epochs=
             break
     den = denormalize(window_mean(tracker.ring), lo, hi)
     return OracleResult(den, tracker.epoch, tracker.history, reason, losses)
+
+
+# --------------------------------------------------------------------------
+# image-quality metrics  (imaging.py:249-311; benchmark mode)
+# --------------------------------------------------------------------------
+
+
+def psnr(a, b, data_range: float) -> float:
+    """10 log10(range^2 / MSE) in f64, +inf for identical inputs (imaging.py:249-263)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    mse = float(np.mean((a - b) ** 2))
+    return math.inf if mse == 0.0 else 10.0 * math.log10(data_range * data_range / mse)
+
+
+def gaussian_window(size: int = 11, sigma: float = 1.5) -> np.ndarray:
+    """Normalised 1-D Gaussian taps (imaging.py:266-270)."""
+    coords = np.arange(size) - (size - 1) / 2.0
+    g = np.exp(-(coords ** 2) / (2.0 * sigma * sigma))
+    return g / g.sum()
+
+
+def _valid_window_mean(x: np.ndarray, win: np.ndarray) -> np.ndarray:
+    """Separable weighted window sums over fully valid positions: rows first,
+    then columns (imaging.py:273-278 correlates with zero padding and crops the
+    border, which leaves exactly these positions)."""
+    k = win.size
+    h, w = x.shape
+    y = sum(win[i] * x[i: h - k + 1 + i, :] for i in range(k))
+    return sum(win[j] * y[:, j: w - k + 1 + j] for j in range(k))
+
+
+def ssim(a, b, data_range: float, k1: float = 0.01, k2: float = 0.03) -> float:
+    """Mean SSIM with the 11x11 Gaussian window (imaging.py:281-311)."""
+    a = np.squeeze(np.asarray(a, dtype=np.float64))
+    b = np.squeeze(np.asarray(b, dtype=np.float64))
+    win = gaussian_window()
+    mu_a = _valid_window_mean(a, win)
+    mu_b = _valid_window_mean(b, win)
+    var_a = _valid_window_mean(a * a, win) - mu_a * mu_a
+    var_b = _valid_window_mean(b * b, win) - mu_b * mu_b
+    cov = _valid_window_mean(a * b, win) - mu_a * mu_b
+    c1 = (k1 * data_range) ** 2
+    c2 = (k2 * data_range) ** 2
+    num = (2 * mu_a * mu_b + c1) * (2 * cov + c2)
+    den = (mu_a ** 2 + mu_b ** 2 + c1) * (var_a + var_b + c2)
+    return float(np.mean(num / den))

@@ -95,6 +95,10 @@ SIGNATURES = {
     "n2f_ctx_profile_epoch": [_P, _P, _P, _P],
     "n2f_ctx_validate": [_P, _P, _P],
     "n2f_ctx_get_pairs": [_P, _P, _P, _P, _P, _P],
+    "n2f_sq_err_sum": [_P, _P, _I64, _P, _P],
+    "n2f_psnr": [_P, _P, _I64, _D, _P, _P],
+    "n2f_ssim": [_P, _P, _I, _I, _D, _D, _D, _P, _P],
+    "n2f_device_count": [_P],
 }
 _RESTYPES = {
     "n2f_last_error": C.c_char_p,

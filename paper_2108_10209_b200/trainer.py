@@ -94,9 +94,35 @@ def derive_seed(seed: int, *ids: int) -> int:
 # ---------------------------------------------------------------------------
 
 
+def _worker_ordinal() -> int:
+    """0-based index of this process among a multiprocessing pool's workers
+    (the reference CLI's spawn pool, cli.py:207-211), 0 outside a pool."""
+    import multiprocessing as mp
+
+    ident = getattr(mp.current_process(), "_identity", ())
+    return ident[0] - 1 if ident else 0
+
+
+def select_device(spec: str | None, ordinal: int, count: int) -> int:
+    """GPU for this process: N2F_DEVICE=<k> pins device k; N2F_DEVICE=auto maps
+    pool worker i to device i mod count (so ``--threads N`` on an N-GPU box
+    runs one image per GPU at a time, BASELINE config 4); unset means 0."""
+    if spec is None or spec == "":
+        return 0
+    if spec == "auto":
+        if count < 1:
+            raise RuntimeError("N2F_DEVICE=auto: no CUDA device visible")
+        return ordinal % count
+    return int(spec)
+
+
 def _device_index() -> int:
-    env = os.environ.get("N2F_DEVICE")
-    return int(env) if env is not None else 0
+    spec = os.environ.get("N2F_DEVICE")
+    if spec != "auto":
+        return select_device(spec, 0, 1)
+    n = _lib.C.c_int()
+    call("n2f_device_count", _lib.C.byref(n))
+    return select_device(spec, _worker_ordinal(), n.value)
 
 
 class Engine:
@@ -324,7 +350,7 @@ def denoise_image(image, config, clean=None, telemetry=None):
     return type(image)(out, image.bit_depth, image.data_range), runs
 
 
-def install() -> None:
+def install(metrics: bool = True) -> None:
     """Route the installed reference package's hot path through this engine.
 
     Rebinds the module global ``noise2fast.trainer.train_single_channel``
@@ -334,3 +360,11 @@ def install() -> None:
     import noise2fast.trainer as ref_trainer
 
     ref_trainer.train_single_channel = train_single_channel
+    if metrics:
+        # benchmark-mode metrics (cli.py:113-139 looks them up on the module)
+        import noise2fast.imaging as ref_imaging
+
+        from . import metrics as m
+
+        ref_imaging.psnr = m.psnr
+        ref_imaging.ssim = m.ssim

@@ -89,3 +89,31 @@ def test_denoise_image_channel_checks():
     img = ImageData(np.zeros((1, 8, 8, 5), np.float32))
     with pytest.raises(ValueError, match="1-4 channels"):
         denoise_image(img, TrainConfig())
+
+
+def test_device_selection_for_pool_workers():
+    """N2F_DEVICE=auto maps pool worker i to GPU i mod count (one image per GPU
+    at a time under the reference CLI's --threads pool, cli.py:207-211)."""
+    from paper_2108_10209_b200.trainer import select_device
+
+    assert select_device(None, 5, 8) == 0
+    assert select_device("3", 5, 8) == 3
+    assert [select_device("auto", i, 4) for i in range(9)] == [0, 1, 2, 3, 0, 1, 2, 3, 0]
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        select_device("auto", 0, 0)
+
+
+def test_metrics_argument_errors_before_device_work():
+    """Reference error behaviour of imaging.psnr / imaging.ssim (imaging.py:255-300)."""
+    from paper_2108_10209_b200 import metrics
+
+    with pytest.raises(ValueError, match="shape mismatch"):
+        metrics.psnr(np.zeros((2, 2)), np.zeros((2, 3)), 255.0)
+    with pytest.raises(ValueError, match="data_range must be positive"):
+        metrics.psnr(np.zeros((2, 2)), np.zeros((2, 2)), 0.0)
+    with pytest.raises(ValueError, match="smaller than the 11x11 window"):
+        metrics.ssim(np.zeros((10, 12)), np.zeros((10, 12)), 1.0)
+    with pytest.raises(ValueError, match="single-channel 2-D"):
+        metrics.ssim(np.zeros((12, 12, 3)), np.zeros((12, 12, 3)), 1.0)
+    with pytest.raises(ValueError, match="shape mismatch"):
+        metrics.ssim(np.zeros((12, 12)), np.zeros((12, 13)), 1.0)

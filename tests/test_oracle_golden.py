@@ -194,3 +194,19 @@ def test_degenerate(oracle):
     res = oracle.fit_denoise(np.full((6, 6), 3.5))
     assert res.stop_reason == "degenerate" and res.epochs_run == 0
     assert np.array_equal(res.denoised, np.full((6, 6), 3.5))
+
+
+def test_metrics_oracle_matches_reference():
+    """oracle.psnr / oracle.ssim vs the reference's own values
+    (tests/golden/make_golden_metrics.py)."""
+    import os
+
+    import numpy as np
+
+    from oracle import n2f_oracle as o
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "metrics_vectors.npz"))
+    for k in range(int(z["ncases"])):
+        a, b, r = z[f"a{k}"], z[f"b{k}"], float(z[f"range{k}"])
+        assert abs(o.psnr(a, b, r) - float(z[f"psnr{k}"])) <= 1e-12 * abs(float(z[f"psnr{k}"]))
+        assert abs(o.ssim(a, b, r) - float(z[f"ssim{k}"])) <= 1e-12
