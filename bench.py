@@ -51,6 +51,10 @@ def parse():
     p.add_argument("--ref-epochs", type=int, default=None,
                    help="epochs of a full fit used to extrapolate the CPU per-epoch time")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--host-loop", action="store_true",
+                   help="launch every kernel from the host instead of the captured while-graph "
+                        "(the same kernels; for ncu launch lists, which cannot see kernels inside "
+                        "conditional graph nodes)")
     p.add_argument("--workload", choices=["config2", "batch64"], default="config2",
                    help="config2: K fits of the 512x512 image per GPU (weak scaling); batch64: "
                         "BASELINE config 4, 64 images shared by all GPUs through a dynamic "
@@ -241,7 +245,7 @@ def run_ours(args):
 
     noisy, clean = workload()
     cfg = TrainConfig(seed=SEED)
-    eng = Engine(SIZE, SIZE, cfg, device=local, conv_impl=args.conv_impl)
+    eng = Engine(SIZE, SIZE, cfg, device=local, conv_impl=args.conv_impl, use_graph=not args.host_loop)
     stream = torch.cuda.ExternalStream(eng.stream)
     img = torch.from_numpy(noisy).cuda()
     out = torch.empty((SIZE, SIZE), dtype=torch.float64, device="cuda")
@@ -387,7 +391,8 @@ def run_batch64(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_img = 64
     images = [synthetic.config_image(4, seed=1000 + i)[0] for i in range(n_img)]
-    eng = Engine(SIZE, SIZE, TrainConfig(seed=0), device=local, conv_impl=args.conv_impl)
+    eng = Engine(SIZE, SIZE, TrainConfig(seed=0), device=local, conv_impl=args.conv_impl,
+                 use_graph=not args.host_loop)
     stream = torch.cuda.ExternalStream(eng.stream)
     out = torch.empty((SIZE, SIZE), dtype=torch.float64, device="cuda")
     img = torch.empty((SIZE, SIZE), dtype=torch.float32, device="cuda")

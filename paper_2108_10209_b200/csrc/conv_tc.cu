@@ -40,6 +40,9 @@
 #ifndef N2F_DY_STACK
 #define N2F_DY_STACK 0
 #endif
+#ifndef N2F_DY_STACK_MAXN
+#define N2F_DY_STACK_MAXN 64
+#endif
 // -DN2F_DY_KC16=1: 16-channel K chunks for N = 256 (experiment)
 #ifndef N2F_DY_KC16
 #define N2F_DY_KC16 0
@@ -779,7 +782,7 @@ struct DyCfg {
   // TMEM: 2 MMAs per K step instead of 3 (the activation operand, which the
   // tensor core reads from smem at ~64 B/clk, bounds these narrow MMAs), and
   // the epilogue adds the two column halves (the lo . lo term comes free)
-  static constexpr bool kStack = N2F_DY_STACK && BN <= 128;
+  static constexpr bool kStack = N2F_DY_STACK && BN <= N2F_DY_STACK_MAXN;
   static constexpr int kTapB = (kStack ? BN : BN / 2) * kRow;  // this CTA's weight rows of one tap
   static constexpr int kStageB = 3 * kTapB;           // the three dx taps
   static constexpr int kStageBytes = 2 * kStageA + (kStack ? 1 : 2) * kStageB;
@@ -2018,7 +2021,7 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
     const int kc = N2F_DY_KC16 && N == 256 ? 16 : 32;  // DyCfg<N>::kKC
     N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, kc, 8, 18));
     N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, kc, 8, 18));
-    const int wrows = (N2F_DY_STACK && N <= 128) ? N : N / 2;  // DyCfg<N>::kStack
+    const int wrows = (N2F_DY_STACK && N <= N2F_DY_STACK_MAXN) ? N : N / 2;  // DyCfg<N>::kStack
     N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, kc, wrows));
     N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, kc, wrows));
     return N2F_OK;
