@@ -149,7 +149,7 @@ int n2f_conv_fwd(const float* x, const float* w, const float* b, float* y, int h
   if (k == 1) {
     k_conv1x1_fwd<<<nb(P * cout), 256, 0, S(stream)>>>(x, w, b, y, P, cin, cout, relu);
     N2F_LAUNCH_CHECK();
-  } else if (k == 3 && cin == 1 && cout % 4 == 0) {
+  } else if (k == 3 && cin == 1) {
     N2F_TRY(conv_first_simt(x, w, b, y, h, wd, cout, S(stream), relu));
   } else if (k == 3 && (impl == kImplTc || impl == kImplTcF16) && tc_supported(cin, cout)) {
     static Scratch s;  // kept alive across async calls on an explicit stream

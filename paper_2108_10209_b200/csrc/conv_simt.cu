@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kThreads)
 // 9-tap sum order (fmaf over taps, then + bias) is the reference's im2col
 // dot order (tensor.py:268-282).
 // ---------------------------------------------------------------------------
+template <int CPT>  // output channels per thread: 8 (the network, N % 8 == 0) or 1 (any N, fp32 out)
 __global__ void __launch_bounds__(kThreads)
     k_conv_first(const float* __restrict__ x, const float* __restrict__ w,
                  const float* __restrict__ b, float* __restrict__ y, float* __restrict__ ylo, int H,
@@ -151,6 +152,21 @@ __global__ void __launch_bounds__(kThreads)
   for (int i = threadIdx.x; i < N * 9; i += blockDim.x) ws[i] = w[i];
   for (int i = threadIdx.x; i < N; i += blockDim.x) bs[i] = b[i];
   __syncthreads();
+  if constexpr (CPT == 1) {  // parity entry point for arbitrary N (fp32 output only)
+    const int ppb = blockDim.x / N;
+    const int n = threadIdx.x % N;
+    const int px = blockIdx.x * ppb + threadIdx.x / N, py = blockIdx.y;
+    if (px >= W || threadIdx.x >= ppb * N) return;
+    float a = 0.f;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
+      const float xv = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
+      a = fmaf(xv, ws[n * 9 + t], a);
+    }
+    y[((int64_t)py * W + px) * N + n] = relu ? fmaxf(a + bs[n], 0.f) : a + bs[n];
+    return;
+  }
   const int nq = N >> 3, ppb = blockDim.x / nq;
   const int q = threadIdx.x % nq;
   const int px = blockIdx.x * ppb + threadIdx.x / nq, py = blockIdx.y;
@@ -409,14 +425,20 @@ int conv3x3_simt(const float* x, const float* wk, const float* bias, const float
 int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
                     int cout, cudaStream_t st, int relu, float* ylo, void* yh16, void* yl16,
                     float oscale) {
-  if (cout % 8 || cout > kMaxC || kThreads % (cout / 8))
-    return fail(N2F_ERR_ARG, "conv_first: cout %d", cout);
+  if (cout < 1 || cout > kMaxC) return fail(N2F_ERR_ARG, "conv_first: cout %d", cout);
   if (ylo && !y) return fail(N2F_ERR_ARG, "conv_first: tf32 residual needs y");
   if (h > 65535) return fail(N2F_ERR_ARG, "conv_first: height %d", h);
-  const int ppb = kThreads / (cout / 8);
-  k_conv_first<<<dim3((unsigned)((w_ + ppb - 1) / ppb), (unsigned)h), kThreads, 0, st>>>(
-      x, w, b, y, ylo, h, w_, cout, relu, reinterpret_cast<__half*>(yh16),
-      reinterpret_cast<__half*>(yl16), oscale);
+  if (cout % 8 == 0 && kThreads % (cout / 8) == 0) {
+    const int ppb = kThreads / (cout / 8);
+    k_conv_first<8><<<dim3((unsigned)((w_ + ppb - 1) / ppb), (unsigned)h), kThreads, 0, st>>>(
+        x, w, b, y, ylo, h, w_, cout, relu, reinterpret_cast<__half*>(yh16),
+        reinterpret_cast<__half*>(yl16), oscale);
+  } else {
+    if (!y || ylo || yh16) return fail(N2F_ERR_ARG, "conv_first: cout %d supports fp32 output only", cout);
+    const int ppb = kThreads / cout;
+    k_conv_first<1><<<dim3((unsigned)((w_ + ppb - 1) / ppb), (unsigned)h), kThreads, 0, st>>>(
+        x, w, b, y, nullptr, h, w_, cout, relu, nullptr, nullptr, 1.f);
+  }
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
