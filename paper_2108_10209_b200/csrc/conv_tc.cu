@@ -40,6 +40,10 @@
 #ifndef N2F_DY_STACK
 #define N2F_DY_STACK 0
 #endif
+// dy kernels with N <= N2F_DY_2SM_MAXN run two CTAs per SM (0 disables)
+#ifndef N2F_DY_2SM_MAXN
+#define N2F_DY_2SM_MAXN 32
+#endif
 #ifndef N2F_DY_STACK_MAXN
 #define N2F_DY_STACK_MAXN 64
 #endif
@@ -789,12 +793,18 @@ struct DyCfg {
   static constexpr int kCols = kStack ? 2 * BN : BN;  // TMEM columns of one accumulator
   // staging slices: 32 channels (one fence + TMA issue per 32) where smem
   // allows, 16 for BN = 256 (whose three 66 KB dy stages fill the rest)
-  static constexpr int kEpiCols = (BN == 256 && !N2F_DY256_EC32) ? 16 : (BN / 2 < 32 ? BN / 2 : 32);
+  // narrow layers (N <= N2F_DY_2SM_MAXN) run two CTAs per SM: their short
+  // launches are bound by per-tile latency (TMA round trips, epilogue), which
+  // a second co-resident CTA pair hides; they take half the smem budget
+  static constexpr int kPerSm = BN <= N2F_DY_2SM_MAXN ? 2 : 1;
+  static constexpr int kEpiCols = (BN == 256 && !N2F_DY256_EC32) ? 16
+                                  : kPerSm == 2 ? (BN / 2 < 16 ? BN / 2 : 16)
+                                                : (BN / 2 < 32 ? BN / 2 : 32);
   static constexpr int kEpiBuf = 32 * kEpiCols * 4;  // one staging buffer (fp32 y, or the fp16 pair)
   static constexpr int kEpiNBuf = 1;
   static constexpr int kEpiWarpBytes = kEpiNBuf * kEpiBuf;
   static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
-  static constexpr int kMaxStages = (218 * 1024 - kEpiBytes - 1024) / kStageBytes;
+  static constexpr int kMaxStages = ((kPerSm == 2 ? 108 : 218) * 1024 - kEpiBytes - 1024) / kStageBytes;
   static constexpr int kStages = kMaxStages > 8 ? 8 : kMaxStages;
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
   static constexpr int kBufs = 512 / kCols > 4 ? 4 : 512 / kCols;  // TMEM group buffers
@@ -812,7 +822,7 @@ struct DyCfg {
 // HEAD: 0 plain conv; 1 / 2 (BN = 256 only) = the L9 training / validation
 // head fused into the epilogue (see HeadTrainArgs / HeadValArgs).
 template <int BN, int HEAD>
-__global__ void __launch_bounds__(kThreadsTc, 1)  // 168 registers: 3 of the 10 warps share an SMSP
+__global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registers at 1 CTA/SM
     k_conv3x3_dy(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
                  const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
@@ -2015,7 +2025,7 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
   if (pl->dy) {
     pl->cs = 2;
     const int units = ((W + 31) / 32) * ((H + 7) / 8);
-    const int max_units = sm_count() / 2;
+    const int max_units = (N <= N2F_DY_2SM_MAXN ? 2 : 1) * sm_count() / 2;  // DyCfg<N>::kPerSm
     pl->grid = 2 * (units < max_units ? units : max_units);
     pl->tiles = 2 * units;
     const int kc = N2F_DY_KC16 && N == 256 ? 16 : 32;  // DyCfg<N>::kKC
@@ -2047,6 +2057,16 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
   return N2F_OK;
 }
 
+// DyCfg<N>::kEpiCols on the host (the TMA-store box must match the staging slice)
+int dy_epi_cols(int N) {
+  switch (N) {
+    case 32: return DyCfg<32>::kEpiCols;
+    case 64: return DyCfg<64>::kEpiCols;
+    case 128: return DyCfg<128>::kEpiCols;
+    default: return DyCfg<256>::kEpiCols;
+  }
+}
+
 int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any cluster size
   return ((W + kTW - 1) / kTW) * 2 * ((H + 2 * kTH - 1) / (2 * kTH));
 }
@@ -2056,8 +2076,7 @@ int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any c
 int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale) {
   if (!pl->f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
   // staging slice geometry: dy kernel {EC channels, 4 x, 8 y}, else {EC, 32 x, 1 y}
-  const int ec = pl->dy ? ((pl->N == 256 && !N2F_DY256_EC32) ? 16 : (pl->N / 2 < 32 ? pl->N / 2 : 32))
-                        : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
+  const int ec = pl->dy ? dy_epi_cols(pl->N) : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
   const int bw = pl->dy ? 4 : kTW, bh = pl->dy ? 8 : 1;
   auto sw_for = [](int row_bytes) {
     return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
