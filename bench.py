@@ -416,6 +416,9 @@ def run_batch64(args):
     ms = e0.elapsed_time(e1)
     max_ms = pool.max_over_ranks(ms, device="cuda")
     total_epochs = pool.sum_over_ranks(sum(epochs), device="cuda")
+    busy_ms = pool.gather_over_ranks(ms, device="cuda")
+    n_per_rank = pool.gather_over_ranks(len(done), device="cuda")
+    flop = 16_392_512.0 * SIZE * SIZE * total_epochs  # FLOP per pixel-epoch
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": n_img / (max_ms / 1e3), "unit": UNIT, "n_gpus": world,
@@ -425,6 +428,9 @@ def run_batch64(args):
                                    "seed, gaussian sigma ~ U(15,50)/255, dynamic queue over GPUs",
                        "images": n_img, "parallelism": f"{world} GPU(s), no collective on the data path"},
             "rank0_images": len(done), "rank0_ms": ms, "total_epochs": total_epochs,
+            "per_gpu_busy_ms": busy_ms, "per_gpu_images": n_per_rank,
+            "imbalance_max_over_mean": pool.imbalance(busy_ms),
+            "algorithmic_tflops_per_gpu": flop / (max_ms * 1e-3) / world / 1e12,
         }), flush=True)
     eng.close()
     if dist is not None:

@@ -68,3 +68,22 @@ def sum_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def gather_over_ranks(value: float, device=None) -> list[float]:
+    """Every rank's scalar (e.g. per-GPU busy time), in rank order."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return [float(value)]
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]
+
+
+def imbalance(busy: list[float]) -> float:
+    """max / mean of the per-rank busy times (1.0 = perfectly balanced)."""
+    mean = sum(busy) / len(busy)
+    return max(busy) / mean if mean > 0 else 1.0

@@ -31,8 +31,9 @@ def _worker(rank, world, port, total, out):
     dist.all_gather_object(got, mine)
     t_max = pool.max_over_ranks(10.0 + rank)
     n_sum = pool.sum_over_ranks(len(mine))
+    busy = pool.gather_over_ranks(10.0 + rank)
     if rank == 0:
-        out.put((got, t_max, n_sum))
+        out.put((got, t_max, n_sum, busy, pool.imbalance(busy)))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -45,13 +46,14 @@ def test_dynamic_queue_partitions_images(total):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, total, q)) for r in range(2)]
     for p in procs:
         p.start()
-    got, t_max, n_sum = q.get(timeout=120)
+    got, t_max, n_sum, busy, imb = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     flat = sorted(i for shard in got for i in shard)
     assert flat == list(range(total))  # every image exactly once
     assert t_max == 11.0 and n_sum == total
+    assert busy == [10.0, 11.0] and abs(imb - 11.0 / 10.5) < 1e-12
 
 
 def test_static_shard_and_single_process_queue():
