@@ -191,6 +191,32 @@ class Engine:
         n = r.epochs_run
         return out, r, hist[:n].copy(), losses[: 4 * n].reshape(n, 4).copy(), secs[:n].copy()
 
+    def params(self) -> np.ndarray:
+        """The parameter arena (w0, b0, ..., w8, b8; weights K-major) on the host."""
+        n = _lib.C.c_int64()
+        call("n2f_ctx_param_count", self.handle, _lib.C.byref(n))
+        out = np.empty(n.value, np.float32)
+        call("n2f_ctx_get_arena", self.handle, 0, out.ctypes.data)
+        return out
+
+    def set_params(self, arena: np.ndarray) -> None:
+        """Overwrite the parameters (resets Adam moments, step count and stop state)."""
+        a = np.ascontiguousarray(arena, np.float32)
+        call("n2f_ctx_set_params", self.handle, a.ctypes.data)
+
+    def save_checkpoint(self, path) -> None:
+        """N2FW v1 checkpoint of the current parameters (model.py:143-152)."""
+        from . import checkpoint
+
+        checkpoint.save_checkpoint(self.params(), path, self.cfg.seed)
+
+    def load_checkpoint(self, path) -> None:
+        """Load an N2FW v1 checkpoint into this context (model.py:155-184)."""
+        from . import checkpoint
+
+        arena, _, _ = checkpoint.load_checkpoint(path)
+        self.set_params(arena)
+
     PROF_CLASSES = ("first_fwd", "conv_fwd", "head_loss", "wgrad", "dgrad", "first_wgrad", "adam",
                     "val_first", "val_conv", "val_head", "stop")
 
