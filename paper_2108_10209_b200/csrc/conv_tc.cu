@@ -774,7 +774,6 @@ struct DyCfg {
   // stages for N = 256) measured no faster.  A group spans K = 96 either way.
   static constexpr int kKC = N2F_DY_KC16 && BN == 256 ? 16 : 32;
   static constexpr int kRow = kKC * 2;                // bytes per GEMM row (fp16)
-  static constexpr int kGroup = 32 / kKC;             // stages per group
   static constexpr int kKSteps = kKC / 16;            // MMA K steps per tap and stage
   static constexpr uint32_t kLayout = kKC == 32 ? 4 : 6;  // UMMA SWIZZLE_64B / _32B
   static constexpr int kDxUnits = (8 * kRow) >> 4;    // a dx shift: 8 rows, descriptor units

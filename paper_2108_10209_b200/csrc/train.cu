@@ -204,6 +204,48 @@ __global__ void __launch_bounds__(kThreads)
 // each operation is rounded separately (no FMA contraction).
 // ---------------------------------------------------------------------------
 constexpr int kAdamRowsPerLane = 16;
+#ifndef N2F_ADAM_NO_WT  // experiment only: skip the transposed weight copies (wrong dgrads)
+#define N2F_ADAM_NO_WT 0
+#endif
+
+// One element's Adam update (NumPy-2 fp32 semantics, tensor.py:125-141) in
+// registers, plus the scattered derived copies (tf32 residual, fp16 pair of
+// the dgrad-transposed weight); m, v, p and the forward fp16 pair are stored
+// by the caller.
+__device__ __forceinline__ void adam_elem(const AdamArgs& args, const AdamTensor& T, int64_t j,
+                                          float g, float bc1, float bc2, float& m, float& v, float& p,
+                                          __half& h16, __half& l16, float& lo) {
+  m = __fmul_rn(m, args.beta1);
+  m = __fadd_rn(m, __fmul_rn(args.one_minus_beta1, g));
+  v = __fmul_rn(v, args.beta2);
+  v = __fadd_rn(v, __fmul_rn(args.one_minus_beta2, __fmul_rn(g, g)));
+  const float mh = __fdiv_rn(m, bc1);
+  const float vh = __fdiv_rn(v, bc2);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(args.lr, mh), __fadd_rn(__fsqrt_rn(vh), args.eps)));
+  float hi;
+  lo = 0.f;
+  if (T.want_lo || T.wtlo) tc::split_tf32(p, hi, lo);
+  if (T.want16) tc::split_f16(__fmul_rn(p, args.wscale), h16, l16);  // p * 2^kExpW
+  if (!N2F_ADAM_NO_WT && (T.wt || T.wth16)) {  // wt[c][8-tap][o] = w[o][tap][c]
+    const int jj = (int)j;
+    // cin is a power of two in the network (shift); 9 is a compile-time divisor
+    const int r = T.cin_log2 >= 0 ? jj >> T.cin_log2 : jj / T.cin;
+    const int cc = jj - r * T.cin;
+    const int o = r / 9;
+    const int tap = r - 9 * o;
+    const int64_t q = ((int64_t)cc * 9 + (8 - tap)) * T.cout + o;
+    if (T.wt) T.wt[q] = p;
+    if (T.wtlo) T.wtlo[q] = lo;
+    if (T.wth16) {
+      T.wth16[q] = h16;
+      T.wtl16[q] = l16;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
+  return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+}
 
 __global__ void __launch_bounds__(kThreads)
     k_adam(AdamArgs args, const int* __restrict__ step_counter, int fixed_t) {
@@ -220,6 +262,53 @@ __global__ void __launch_bounds__(kThreads)
   }
   const AdamTensor& T = args.t[tl];
   const int local = blk - T.blk0;
+  if (T.vec == 4) {
+    // wide tensors with <= 16 split rows: 4 columns per thread, every row of
+    // partials in flight as float4 loads, then the update on a float4 of
+    // moments / parameters (same per-element arithmetic and sum order)
+    const int64_t j4 = ((int64_t)local * kThreads + threadIdx.x) * 4;
+    if (j4 >= T.n) return;
+    const int64_t i4 = T.off + j4;
+    float4 m4 = *reinterpret_cast<const float4*>(args.m + i4);
+    float4 v4 = *reinterpret_cast<const float4*>(args.v + i4);
+    float4 p4 = *reinterpret_cast<const float4*>(args.p + i4);
+    const float* __restrict__ part = T.part + j4;
+    float4 x[kAdamRowsPerLane];
+#pragma unroll
+    for (int q = 0; q < kAdamRowsPerLane; ++q)
+      x[q] = q < T.nsplit ? __ldg(reinterpret_cast<const float4*>(part + (int64_t)q * T.n))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 g4 = x[0];
+#pragma unroll
+    for (int q = 1; q < kAdamRowsPerLane; ++q) {
+      if (q < T.nsplit) {
+        g4.x += x[q].x;
+        g4.y += x[q].y;
+        g4.z += x[q].z;
+        g4.w += x[q].w;
+      }
+    }
+    const int t = step_counter ? *step_counter : fixed_t;
+    const int ti = (t < args.table_len ? t : args.table_len) - 1;
+    const float bc1 = args.bc1[ti], bc2 = args.bc2[ti];
+    float* mv = &m4.x;
+    float* vv = &v4.x;
+    float* pv = &p4.x;
+    const float* gv = &g4.x;
+    __half h[4], l[4];
+    float lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) adam_elem(args, T, j4 + e, gv[e], bc1, bc2, mv[e], vv[e], pv[e], h[e], l[e], lo[e]);
+    *reinterpret_cast<float4*>(args.m + i4) = m4;
+    *reinterpret_cast<float4*>(args.v + i4) = v4;
+    *reinterpret_cast<float4*>(args.p + i4) = p4;
+    if (T.want_lo) *reinterpret_cast<float4*>(args.plo + i4) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    if (T.want16) {
+      *reinterpret_cast<uint2*>(args.phi16 + i4) = make_uint2(pack_h2(h[0], h[1]), pack_h2(h[2], h[3]));
+      *reinterpret_cast<uint2*>(args.plo16 + i4) = make_uint2(pack_h2(l[0], l[1]), pack_h2(l[2], l[3]));
+    }
+    return;
+  }
   const int chunk = local / T.ns, slab = local - chunk * T.ns;
   const int cw = T.cw, rl = T.rl;
   const int c = threadIdx.x % cw, r = threadIdx.x / cw;
@@ -285,37 +374,16 @@ __global__ void __launch_bounds__(kThreads)
   const int t = step_counter ? *step_counter : fixed_t;
   const int ti = (t < args.table_len ? t : args.table_len) - 1;
   const float bc1 = args.bc1[ti], bc2 = args.bc2[ti];
-  m = __fmul_rn(m, args.beta1);
-  m = __fadd_rn(m, __fmul_rn(args.one_minus_beta1, g));
-  v = __fmul_rn(v, args.beta2);
-  v = __fadd_rn(v, __fmul_rn(args.one_minus_beta2, __fmul_rn(g, g)));
-  const float mh = __fdiv_rn(m, bc1);
-  const float vh = __fdiv_rn(v, bc2);
-  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(args.lr, mh), __fadd_rn(__fsqrt_rn(vh), args.eps)));
+  __half h16, l16;
+  float lo;
+  adam_elem(args, T, j, g, bc1, bc2, m, v, p, h16, l16, lo);
   args.m[i] = m;
   args.v[i] = v;
   args.p[i] = p;
-  float hi, lo = 0.f;
-  if (T.want_lo || T.wtlo) tc::split_tf32(p, hi, lo);
   if (T.want_lo) args.plo[i] = lo;  // tf32 residual of the forward operand
-  __half h16, l16;
-  if (T.want16) {  // FP16 pair of p * 2^kExpW for the FP16 tensor-core path
-    tc::split_f16(__fmul_rn(p, args.wscale), h16, l16);
+  if (T.want16) {                   // FP16 pair for the FP16 tensor-core path
     args.phi16[i] = h16;
     args.plo16[i] = l16;
-  }
-  if (T.wt || T.wth16) {  // wt[c][8-tap][o] = w[o][tap][c]
-    const int jj = (int)j;
-    const int cc = jj % T.cin;
-    const int tap = (jj / T.cin) % 9;
-    const int o = jj / (T.cin * 9);
-    const int64_t q = ((int64_t)cc * 9 + (8 - tap)) * T.cout + o;
-    if (T.wt) T.wt[q] = p;
-    if (T.wtlo) T.wtlo[q] = lo;
-    if (T.wth16) {
-      T.wth16[q] = h16;
-      T.wtl16[q] = l16;
-    }
   }
 }
 
@@ -507,7 +575,13 @@ void adam_plan(AdamArgs& a) {
     int rl = 1;
     while (rl < 32 && ns_rows > kAdamRowsPerLane * rl) rl <<= 1;
     T.rl = rl;
-    T.cw = kThreads / rl;
+    T.cin_log2 = -1;
+    for (int b = 0; b < 31; ++b)
+      if (T.cin == (1 << b)) T.cin_log2 = b;
+    // float4 columns: one row lane, 16-byte aligned rows and arena offset
+    T.vec = (rl == 1 && T.n % 4 == 0 && T.off % 4 == 0 &&
+             (reinterpret_cast<uintptr_t>(T.part) & 15) == 0) ? 4 : 1;
+    T.cw = kThreads * T.vec / rl;
     T.ns = (ns_rows + kAdamRowsPerLane * rl - 1) / (kAdamRowsPerLane * rl);
     T.nchunk = (int)((T.n + T.cw - 1) / T.cw);
     T.blk0 = blk;

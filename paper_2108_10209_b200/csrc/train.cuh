@@ -72,6 +72,8 @@ struct AdamTensor {
   // slabs of <= 16 rl partial rows (slab sums combined by the last block of a
   // column chunk through scratch + an arrival counter), blocks [blk0, ...)
   int rl, cw, ns, nchunk, blk0, cnt0;
+  int vec;  // 4: float4 columns per thread (one row lane, aligned), else 1
+  int cin_log2;  // log2(cin) when cin is a power of two, else -1
   int64_t scr0;
 };
 
