@@ -35,17 +35,9 @@
 #ifndef N2F_DY256_EC32
 #define N2F_DY256_EC32 1
 #endif
-// -DN2F_DY_STACK=0: dy kernels with N <= 128 issue 3 MMAs per K step (no
-// N-stacked weight parts)
-#ifndef N2F_DY_STACK
-#define N2F_DY_STACK 0
-#endif
 // dy kernels with N <= N2F_DY_2SM_MAXN run two CTAs per SM (0 disables)
 #ifndef N2F_DY_2SM_MAXN
 #define N2F_DY_2SM_MAXN 32
-#endif
-#ifndef N2F_DY_STACK_MAXN
-#define N2F_DY_STACK_MAXN 64
 #endif
 // -DN2F_DY_KC16=1: 16-channel K chunks for N = 256 (experiment)
 #ifndef N2F_DY_KC16
@@ -779,17 +771,10 @@ struct DyCfg {
   static constexpr int kDxUnits = (8 * kRow) >> 4;    // a dx shift: 8 rows, descriptor units
   static constexpr int kRowsA = 18 * 8;               // halo columns x rows
   static constexpr int kStageA = kRowsA * kRow;       // one fp16 part (hi or lo)
-  // N-stacked weight parts (N <= 128): the pair's B operand is [w_hi; w_lo]
-  // (2N rows: CTA 0 stages all of w_hi, CTA 1 all of w_lo), so one MMA per
-  // activation part yields (x_part . w_hi | x_part . w_lo) side by side in
-  // TMEM: 2 MMAs per K step instead of 3 (the activation operand, which the
-  // tensor core reads from smem at ~64 B/clk, bounds these narrow MMAs), and
-  // the epilogue adds the two column halves (the lo . lo term comes free)
-  static constexpr bool kStack = N2F_DY_STACK && BN <= N2F_DY_STACK_MAXN;
-  static constexpr int kTapB = (kStack ? BN : BN / 2) * kRow;  // this CTA's weight rows of one tap
+  static constexpr int kTapB = (BN / 2) * kRow;       // this CTA's weight rows of one tap
   static constexpr int kStageB = 3 * kTapB;           // the three dx taps
-  static constexpr int kStageBytes = 2 * kStageA + (kStack ? 1 : 2) * kStageB;
-  static constexpr int kCols = kStack ? 2 * BN : BN;  // TMEM columns of one accumulator
+  static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
+  static constexpr int kCols = BN;                    // TMEM columns of one accumulator
   // staging slices: 32 channels (one fence + TMA issue per 32) where smem
   // allows, 16 for BN = 256 (whose three 66 KB dy stages fill the rest)
   // narrow layers (N <= N2F_DY_2SM_MAXN) run two CTAs per SM: their short
@@ -830,9 +815,8 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
                  int mask_bits, uint32_t* __restrict__ mbits_out, float* __restrict__ colsum,
                  float unscale, int H, int W, int C, int epi, HeadTrainArgs ht, HeadValArgs hv) {
   using Cfg = DyCfg<BN>;
-  // flags: bit 0 direct stores (experiment); bits 8.. groups per tile
-  // (experiment override, 0 = DyCfg::kGroupsPerTile)
-  const bool direct = flags & 1;
+  // flags: bits 8.. accumulation groups per tile (experiment override, 0 =
+  // DyCfg::kGroupsPerTile)
   using P = Prec<true>;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
@@ -901,12 +885,8 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
           if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
           tma_load_3d_2sm(st, &mx, fb, c0, y0 + dy - 1, x0 - 1);
           tma_load_3d_2sm(st + Cfg::kStageA, &mxl, fb, c0, y0 + dy - 1, x0 - 1);
-          if (Cfg::kStack) {  // CTA 0: w_hi rows, CTA 1: w_lo rows (all N of them)
-            tma_load_4d_2sm(st + 2 * Cfg::kStageA, rank == 0 ? &mw : &mwl, fb, c0, 0, 0, dy);
-          } else {
-            tma_load_4d_2sm(st + 2 * Cfg::kStageA, &mw, fb, c0, n0, 0, dy);
-            tma_load_4d_2sm(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, fb, c0, n0, 0, dy);
-          }
+          tma_load_4d_2sm(st + 2 * Cfg::kStageA, &mw, fb, c0, n0, 0, dy);
+          tma_load_4d_2sm(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, fb, c0, n0, 0, dy);
         }
         __syncwarp();
       }
@@ -950,24 +930,14 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
             tc_fence_after();
             if (elect_one_sync()) {
               const uint64_t a0 = desc0 + (uint64_t)(st * (Cfg::kStageBytes >> 4));
-              if (Cfg::kStack) {  // x_lo . [w_hi; w_lo], then x_hi . [w_hi; w_lo]
 #pragma unroll
-                for (int dx = 0; dx < 3; ++dx) {
+              for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
-                  for (int k = 0; k < Cfg::kKSteps; ++k)
-                    mma_f16_2sm(d, a0 + kAl + Cfg::kDxUnits * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k,
-                                idesc, ((kb - s0) | dx | k) != 0);
-                }
-              } else {
-#pragma unroll
-                for (int dx = 0; dx < 3; ++dx) {
-#pragma unroll
-                  for (int k = 0; k < Cfg::kKSteps; ++k) {
-                    const uint64_t a = a0 + Cfg::kDxUnits * dx + 2 * k;
-                    const uint64_t bh = a0 + kBh + kTap * dx + 2 * k;
-                    mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | dx | k) != 0);
-                    mma_f16_2sm(d, a + kAl, bh, idesc, 1);
-                  }
+                for (int k = 0; k < Cfg::kKSteps; ++k) {
+                  const uint64_t a = a0 + Cfg::kDxUnits * dx + 2 * k;
+                  const uint64_t bh = a0 + kBh + kTap * dx + 2 * k;
+                  mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | dx | k) != 0);
+                  mma_f16_2sm(d, a + kAl, bh, idesc, 1);
                 }
               }
 #pragma unroll
@@ -1035,7 +1005,6 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
           tmem_load_all<HALF>(lane_base + b * Cfg::kCols, acc);
         else
           drain_add<HALF>(lane_base + b * Cfg::kCols, acc);
-        if (Cfg::kStack) drain_add<HALF>(lane_base + b * Cfg::kCols + BN, acc);  // x . w_lo half
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty0 + 8u * b);
@@ -1256,36 +1225,6 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
             }
           }
           if ((lane & (32 / EC - 1)) == 0) csum[q][n + ch] = r[0];
-        }
-        if (direct) {  // direct stores from registers: 16 channels of this lane's pixel
-          if (valid) {
-            const int64_t idx = pix * BN + n;
-            if (out.y) {
-#pragma unroll
-              for (int k = 0; k < CH; ++k)
-                *reinterpret_cast<float4*>(out.y + idx + 4 * k) =
-                    make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-            }
-            if (out.yhi) {
-              uint32_t hw[EC / 2], lw[EC / 2];
-#pragma unroll
-              for (int i = 0; i < EC; i += 2) {
-                __half h0, l0, h1, l1;
-                split_f16(v[i] * oscale, h0, l0);
-                split_f16(v[i + 1] * oscale, h1, l1);
-                hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-                lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-              }
-#pragma unroll
-              for (int k = 0; k < EC / 8; ++k) {
-                *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out.yhi) + idx + 8 * k) =
-                    make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
-                *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out.ylo) + idx + 8 * k) =
-                    make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
-              }
-            }
-          }
-          continue;
         }
         // staging buffer sb: its previous TMA stores (two slices ago) must be done reading
         uint8_t* stg = stg0 + sb * Cfg::kEpiBuf;
@@ -1902,13 +1841,12 @@ int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, fl
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   static const int flags = [] {
-    const char* e = getenv("N2F_DY_DIRECT");
     const char* g = getenv("N2F_DY_GROUPS");  // accumulation groups per tile (experiment)
-    return (e && atoi(e) ? 1 : 0) | ((g ? atoi(g) : 0) << 8);
+    return (g ? atoi(g) : 0) << 8;
   }();
   N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN, HEAD>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
                               pl.myh, pl.myl, pl.omask, pl.oscale,
-                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, HEAD ? (flags & ~1) : flags, bias, mask,
+                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, flags, bias, mask,
                               pl.mask_bits, pl.mbits_out, colsum, pl.unscale, pl.H, pl.W, pl.C, epi,
                               ht, hv));
   N2F_LAUNCH_CHECK();
@@ -2030,9 +1968,8 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
     const int kc = N2F_DY_KC16 && N == 256 ? 16 : 32;  // DyCfg<N>::kKC
     N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, kc, 8, 18));
     N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, kc, 8, 18));
-    const int wrows = (N2F_DY_STACK && N <= N2F_DY_STACK_MAXN) ? N : N / 2;  // DyCfg<N>::kStack
-    N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, kc, wrows));
-    N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, kc, wrows));
+    N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, kc, N / 2));
+    N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, kc, N / 2));
     return N2F_OK;
   }
   // wide layers (N >= 128) run as CTA pairs (cta_group::2, M = 256: each CTA
