@@ -1773,6 +1773,10 @@ int set_attr_one() {
     N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1, 64>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   WgCfg<BN, F16, 1, 64>::kSmem));
+    if constexpr (BN <= 64)
+      N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1, 128>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    WgCfg<BN, F16, 1, 128>::kSmem));
   }
   if (BN >= 128) {
     N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 2, 32>,
@@ -1908,7 +1912,10 @@ int launch_wgrad_tc_n(const WgradTcPlan& pl, float* part, cudaStream_t st) {
     if constexpr (BN >= 128) return launch_wgrad_tc_bn<BN, F16, 2, 32>(pl, part, st);
     return fail(N2F_ERR_ARG, "wgrad pair with N=%d", BN);
   }
-  if (F16 && pl.seg == 64) return launch_wgrad_tc_bn<BN, F16, 1, F16 ? 64 : 32>(pl, part, st);
+  if (F16 && pl.seg == 128) {
+    if constexpr (BN <= 64) return launch_wgrad_tc_bn<BN, F16, 1, F16 ? 128 : 32>(pl, part, st);
+  }
+  if (F16 && pl.seg >= 64) return launch_wgrad_tc_bn<BN, F16, 1, F16 ? 64 : 32>(pl, part, st);
   return launch_wgrad_tc_bn<BN, F16, 1, 32>(pl, part, st);
 }
 
@@ -2122,10 +2129,14 @@ int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H
   // share a tap when C % 128 == 0 (else one box per block), the gradient's
   // N / 32 blocks always come as one box
   pl->xblk = C % 128 == 0;
-  // FP16 single-CTA wgrads take 64-pixel stages (N2F_WGRAD_SEG overrides)
+  // FP16 single-CTA wgrads take 64-pixel stages, 128 for C = 32 (N2F_WGRAD_SEG overrides)
   const char* segenv = getenv("N2F_WGRAD_SEG");
-  pl->seg = (f16 && pl->cs == 1) ? (segenv ? atoi(segenv) : 64) : kSegW;
-  if (pl->seg != 32 && pl->seg != 64) pl->seg = kSegW;
+  // (C = 32 layers: 128-pixel stages halve the TMA instructions per pixel --
+  // their 4 per-tap activation boxes per part make them TMA-issue bound)
+  const int seg_default = (C == 32 && N <= 64) ? 128 : 64;
+  pl->seg = (f16 && pl->cs == 1) ? (segenv ? atoi(segenv) : seg_default) : kSegW;
+  if (pl->seg == 128 && N > 64) pl->seg = 64;
+  if (pl->seg != 32 && pl->seg != 64 && pl->seg != 128) pl->seg = kSegW;
   const int bpt = pl->xblk ? 4 : C / 32;  // activation blocks per box (one tap)
   N2F_TRY(map_act_blk(&pl->mx, x.hi, f16, C, W, H, pl->seg, bpt, sw));
   N2F_TRY(map_act_blk(&pl->mxl, x.lo, f16, C, W, H, pl->seg, bpt, sw));
