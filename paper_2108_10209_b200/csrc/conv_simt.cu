@@ -147,9 +147,11 @@ __global__ void __launch_bounds__(kThreads)
                  const float* __restrict__ b, float* __restrict__ y, float* __restrict__ ylo, int H,
                  int W, int N, int relu, __half* __restrict__ yh16, __half* __restrict__ yl16,
                  float oscale) {
+  // weights staged tap-major (ws[t][n]) so a thread's 8 channels of one tap
+  // are two 16-byte smem loads
   __shared__ __align__(16) float ws[kMaxC * 9];
   __shared__ __align__(16) float bs[kMaxC];
-  for (int i = threadIdx.x; i < N * 9; i += blockDim.x) ws[i] = w[i];
+  for (int i = threadIdx.x; i < N * 9; i += blockDim.x) ws[(i % 9) * N + i / 9] = w[i];
   for (int i = threadIdx.x; i < N; i += blockDim.x) bs[i] = b[i];
   __syncthreads();
   if constexpr (CPT == 1) {  // parity entry point for arbitrary N (fp32 output only)
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int t = 0; t < 9; ++t) {
       const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
       const float xv = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
-      a = fmaf(xv, ws[n * 9 + t], a);
+      a = fmaf(xv, ws[t * N + n], a);
     }
     y[((int64_t)py * W + px) * N + n] = relu ? fmaxf(a + bs[n], 0.f) : a + bs[n];
     return;
@@ -178,14 +180,18 @@ __global__ void __launch_bounds__(kThreads)
     xv[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
   }
   float o[8];
-  const float* wq = ws + 8 * q * 9;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    float a = 0.f;
+  for (int j = 0; j < 8; ++j) o[j] = 0.f;
 #pragma unroll
-    for (int t = 0; t < 9; ++t) a = fmaf(xv[t], wq[j * 9 + t], a);
-    o[j] = relu ? fmaxf(a + bs[8 * q + j], 0.f) : a + bs[8 * q + j];
+  for (int t = 0; t < 9; ++t) {  // per channel the same fmaf order over taps as before
+    const float4 w0 = *reinterpret_cast<const float4*>(ws + t * N + 8 * q);
+    const float4 w1 = *reinterpret_cast<const float4*>(ws + t * N + 8 * q + 4);
+    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = fmaf(xv[t], wv[j], o[j]);
   }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = relu ? fmaxf(o[j] + bs[8 * q + j], 0.f) : o[j] + bs[8 * q + j];
   const int64_t idx = ((int64_t)py * W + px) * N + 8 * q;
   if (y) {
     *reinterpret_cast<float4*>(y + idx) = make_float4(o[0], o[1], o[2], o[3]);
@@ -457,9 +463,9 @@ int wgrad_nsplit(int64_t pixels, int cin, int cout) {
   const int64_t tiles =
       (cin == 1) ? 1 : (int64_t)((cout + bm - 1) / bm) * ((9 * cin + bn - 1) / bn);
   int64_t want = (4 * 148 + tiles - 1) / tiles;
-  // the first layer's wgrad (k_wgrad_first): one block per ~512 pixels (8
-  // warps x two 32-pixel segments), at most 2048 blocks
-  int64_t maxs = (pixels + (cin == 1 ? 511 : 511)) / 512;
+  // the first layer's wgrad (k_wgrad_first): one block per ~256 pixels (8
+  // warps x one 32-pixel segment: latency-bound, so many warps), at most 2048
+  int64_t maxs = cin == 1 ? (pixels + 255) / 256 : (pixels + 511) / 512;
   if (cin == 1) want = 2048;
   int64_t n = want < maxs ? want : maxs;
   if (n < 1) n = 1;
