@@ -5,7 +5,7 @@ set -x
 mkdir -p gpurun_out
 timeout 600 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err || exit 1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+  --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --host-loop --no-cpu-baseline \
   > gpurun_out/ncu_bench.log 2>&1
 python tools/ncu_target.py 1 > gpurun_out/nt.log 2>&1 || exit 1
 # one host-loop epoch: k_conv3x3_dy launches 0..6 = fwd L2..L8 (6 = L8 + head), 7 = dgrad L8
