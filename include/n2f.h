@@ -154,6 +154,8 @@ int n2f_window_mean(const float* ring, int n_slots, int first_slot, int n, int64
 int n2f_ctx_prepare(n2f_ctx* ctx, const void* image, int dtype, const void* clean,
                     int init_from_seed);
 int n2f_ctx_param_count(n2f_ctx* ctx, int64_t* n);
+/* seed of the next fit's He-uniform init (TrainConfig.seed, trainer.py:178) */
+int n2f_ctx_set_seed(n2f_ctx* ctx, uint64_t seed);
 int n2f_ctx_get_arena(n2f_ctx* ctx, int which, float* host);
 int n2f_ctx_set_params(n2f_ctx* ctx, const float* host);
 int n2f_ctx_set_arena(n2f_ctx* ctx, int which, const float* host, int adam_step);

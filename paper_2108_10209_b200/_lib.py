@@ -99,6 +99,7 @@ SIGNATURES = {
     "n2f_psnr": [_P, _P, _I64, _D, _P, _P],
     "n2f_ssim": [_P, _P, _I, _I, _D, _D, _D, _P, _P],
     "n2f_device_count": [_P],
+    "n2f_ctx_set_seed": [_P, C.c_uint64],
 }
 _RESTYPES = {
     "n2f_last_error": C.c_char_p,

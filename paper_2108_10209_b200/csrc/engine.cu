@@ -944,6 +944,15 @@ int n2f_ctx_get_arena(n2f_ctx* c, int which, float* host) {
   return N2F_OK;
 }
 
+// Network seed for the next fit's initialisation (model.py:46-65): the only
+// per-image setting that is not baked into the workspaces or the captured
+// graph, so one context serves every seed (denoise_image, CLI per-file seeds).
+int n2f_ctx_set_seed(n2f_ctx* c, uint64_t seed) {
+  if (!c) return fail(N2F_ERR_ARG, "null ctx");
+  c->cfg.seed = seed;
+  return N2F_OK;
+}
+
 // Overwrite params (engine layout) and reset Adam moments/step and stop state.
 int n2f_ctx_set_params(n2f_ctx* c, const float* host) {
   if (!c || !host) return fail(N2F_ERR_ARG, "null argument");

@@ -191,6 +191,11 @@ class Engine:
         n = r.epochs_run
         return out, r, hist[:n].copy(), losses[: 4 * n].reshape(n, 4).copy(), secs[:n].copy()
 
+    def set_seed(self, seed: int) -> None:
+        """Network seed of the next fit (TrainConfig.seed)."""
+        self.cfg.seed = int(seed) & _M64
+        call("n2f_ctx_set_seed", self.handle, self.cfg.seed)
+
     def params(self) -> np.ndarray:
         """The parameter arena (w0, b0, ..., w8, b8; weights K-major) on the host."""
         n = _lib.C.c_int64()
@@ -243,8 +248,10 @@ _cache: dict = {}
 
 
 def _engine_for(shape, config) -> Engine:
+    # the seed is set per fit (n2f_ctx_set_seed): one context serves every
+    # seed of a shape/config (denoise_image's per-channel seeds, CLI files)
     key = (shape, config.loss, config.scheme, float(config.lr), int(config.patience_epochs),
-           int(config.avg_window), int(config.max_epochs), int(config.seed) & _M64, _device_index())
+           int(config.avg_window), int(config.max_epochs), _device_index())
     with _cache_lock:
         eng = _cache.get(key)
         if eng is None:
@@ -253,6 +260,7 @@ def _engine_for(shape, config) -> Engine:
                 _cache.pop(k).close()
             eng = Engine(shape[0], shape[1], config)
             _cache[key] = eng
+        eng.set_seed(config.seed)
         return eng
 
 

@@ -288,3 +288,23 @@ def test_ragged_sizes_fit(oracle, hw):
     assert res.epochs_run == ref.epochs_run == 2
     assert abs(res.val_history[0] - ref.val_history[0]) <= 5e-3 * ref.val_history[0]
     assert norm_rel(res.denoised, ref.denoised) < 2e-2
+
+
+def test_context_reuse_across_seeds():
+    """One cached context serves every seed (denoise_image's per-channel seeds,
+    trainer.py:240): a fit after a different-seed fit on the same context is
+    bitwise the fit of a fresh context."""
+    from paper_2108_10209_b200 import TrainConfig, train_single_channel
+    from paper_2108_10209_b200 import trainer as T
+
+    img, _ = _image(40, 40, seed=17)
+    mk = lambda s: TrainConfig(seed=s, patience_epochs=4, avg_window=3, max_epochs=8)  # noqa: E731
+    T.release_engines()
+    a1 = train_single_channel(img, mk(1))
+    a2 = train_single_channel(img, mk(2))  # same cached context, new seed
+    assert len(T._cache) == 1
+    T.release_engines()
+    b2 = train_single_channel(img, mk(2))
+    assert np.array_equal(a2.denoised, b2.denoised) and a2.val_history == b2.val_history
+    assert not np.array_equal(a1.denoised, a2.denoised)
+    T.release_engines()
