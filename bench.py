@@ -422,6 +422,7 @@ def run_batch64(args):
     done, epochs = [], []
     for i in pool.claim(store, "bench/batch64", n_img):
         img.copy_(torch.from_numpy(images[i]), non_blocking=False)
+        eng.set_seed(1000 + i)  # per-image network seed, like the CLI's per-file seeds
         r = eng.fit_device(img.data_ptr(), _lib.N2F_F32, out.data_ptr())
         done.append(i)
         epochs.append(r.epochs_run)
