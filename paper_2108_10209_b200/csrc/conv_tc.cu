@@ -112,7 +112,7 @@ __device__ __forceinline__ void add2(float& a0, float& a1, uint32_t r0, uint32_t
 // into the fp32 register accumulators, two tcgen05.ld in flight per wait.
 template <int HALF>
 __device__ __forceinline__ void drain_add(uint32_t taddr, float (&acc)[HALF]) {
-  constexpr int CH = HALF < 32 ? HALF : 32;  // columns per load
+  constexpr int CH = HALF % 32 == 0 ? 32 : 16;  // columns per load (HALF = 16, 32, 48, 64, 96, 128)
   constexpr int NB = HALF / CH;
   constexpr int PB = NB >= 2 ? 2 : 1;        // loads per wait
 #pragma unroll
@@ -120,17 +120,20 @@ __device__ __forceinline__ void drain_add(uint32_t taddr, float (&acc)[HALF]) {
     uint32_t r[PB][32];
 #pragma unroll
     for (int p = 0; p < PB; ++p) {
-      if (CH == 16)
-        tmem_ld16(taddr + (c + p) * CH, r[p]);
-      else
-        tmem_ld32(taddr + (c + p) * CH, r[p]);
+      if (c + p < NB) {
+        if (CH == 16)
+          tmem_ld16(taddr + (c + p) * CH, r[p]);
+        else
+          tmem_ld32(taddr + (c + p) * CH, r[p]);
+      }
     }
     tmem_ld_wait();
 #pragma unroll
     for (int p = 0; p < PB; ++p)
+      if (c + p < NB)
 #pragma unroll
-      for (int j = 0; j < CH; j += 2)
-        add2(acc[(c + p) * CH + j], acc[(c + p) * CH + j + 1], r[p][j], r[p][j + 1]);
+        for (int j = 0; j < CH; j += 2)
+          add2(acc[(c + p) * CH + j], acc[(c + p) * CH + j + 1], r[p][j], r[p][j + 1]);
   }
 }
 
@@ -138,7 +141,7 @@ __device__ __forceinline__ void drain_add(uint32_t taddr, float (&acc)[HALF]) {
 // accumulated its whole K loop in TMEM), two tcgen05.ld in flight per wait.
 template <int HALF>
 __device__ __forceinline__ void tmem_load_all(uint32_t taddr, float (&acc)[HALF]) {
-  constexpr int CH = HALF < 32 ? HALF : 32;
+  constexpr int CH = HALF % 32 == 0 ? 32 : 16;
   constexpr int NB = HALF / CH;
   constexpr int PB = NB >= 2 ? 2 : 1;
 #pragma unroll
@@ -146,16 +149,19 @@ __device__ __forceinline__ void tmem_load_all(uint32_t taddr, float (&acc)[HALF]
     uint32_t r[PB][32];
 #pragma unroll
     for (int p = 0; p < PB; ++p) {
-      if (CH == 16)
-        tmem_ld16(taddr + (c + p) * CH, r[p]);
-      else
-        tmem_ld32(taddr + (c + p) * CH, r[p]);
+      if (c + p < NB) {
+        if (CH == 16)
+          tmem_ld16(taddr + (c + p) * CH, r[p]);
+        else
+          tmem_ld32(taddr + (c + p) * CH, r[p]);
+      }
     }
     tmem_ld_wait();
 #pragma unroll
     for (int p = 0; p < PB; ++p)
+      if (c + p < NB)
 #pragma unroll
-      for (int j = 0; j < CH; ++j) acc[(c + p) * CH + j] = __uint_as_float(r[p][j]);
+        for (int j = 0; j < CH; ++j) acc[(c + p) * CH + j] = __uint_as_float(r[p][j]);
   }
 }
 
@@ -760,7 +766,7 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 //   TMA instruction count by 3x.  A stage is one TMEM accumulation group
 //   (K = 96: 18 MMAs, 6 of them hi*hi).  Epilogue: TMA tensor stores.
 // ---------------------------------------------------------------------------
-template <int BN>
+template <int BN, bool DX3 = false>
 struct DyCfg {
   // K chunk of a stage: 32 channels (SWIZZLE_64B rows); 16 (SWIZZLE_32B, five
   // stages for N = 256) measured no faster.  A group spans K = 96 either way.
@@ -768,13 +774,19 @@ struct DyCfg {
   static constexpr int kRow = kKC * 2;                // bytes per GEMM row (fp16)
   static constexpr int kKSteps = kKC / 16;            // MMA K steps per tap and stage
   static constexpr uint32_t kLayout = kKC == 32 ? 4 : 6;  // UMMA SWIZZLE_64B / _32B
-  static constexpr int kDxUnits = (8 * kRow) >> 4;    // a dx shift: 8 rows, descriptor units
-  static constexpr int kRowsA = 18 * 8;               // halo columns x rows
+  static constexpr int kDxUnits = DX3 ? 0 : (8 * kRow) >> 4;  // a dx shift: 8 rows, descriptor units
+  // DX3 (narrow layers): the three dx taps are stacked into one N = 3 BN MMA
+  // on an unshifted 16 x 8 activation box (3x fewer activation-operand smem
+  // reads, which bound these narrow MMAs); the epilogue adds the taps of the
+  // neighbouring columns (lane shuffles by 8, a cross-warp exchange at the
+  // quarter edges) and a CTA tile keeps the 14 centre columns
+  static constexpr int kRowsA = (DX3 ? 16 : 18) * 8;  // halo columns x rows
   static constexpr int kStageA = kRowsA * kRow;       // one fp16 part (hi or lo)
   static constexpr int kTapB = (BN / 2) * kRow;       // this CTA's weight rows of one tap
   static constexpr int kStageB = 3 * kTapB;           // the three dx taps
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
-  static constexpr int kCols = BN;                    // TMEM columns of one accumulator
+  static constexpr int kCols = DX3 ? 3 * BN : BN;     // TMEM columns of one accumulator
+  static constexpr int kTileW = DX3 ? 14 : 16;        // output columns per CTA
   // staging slices: 32 channels (one fence + TMA issue per 32) where smem
   // allows, 16 for BN = 256 (whose three 66 KB dy stages fill the rest)
   // narrow layers (N <= N2F_DY_2SM_MAXN) run two CTAs per SM: their short
@@ -787,26 +799,32 @@ struct DyCfg {
   static constexpr int kEpiBuf = 32 * kEpiCols * 4;  // one staging buffer (fp32 y, or the fp16 pair)
   static constexpr int kEpiNBuf = 1;
   static constexpr int kEpiWarpBytes = kEpiNBuf * kEpiBuf;
-  static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
+  // DX3 stores directly (its 4-column warp boxes would overlap the neighbour
+  // tiles) and instead needs the tap-exchange buffer: [tile parity][half][q]
+  // [side][8 lanes][BN / 2] floats
+  static constexpr int kXchBytes = DX3 ? 2 * 2 * 4 * 2 * 8 * (BN / 2) * 4 : 0;
+  static constexpr int kEpiBytes = DX3 ? kXchBytes : 8 * kEpiWarpBytes;
   static constexpr int kMaxStages = ((kPerSm == 2 ? 108 : 218) * 1024 - kEpiBytes - 1024) / kStageBytes;
   static constexpr int kStages = kMaxStages > 8 ? 8 : kMaxStages;
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
-  static constexpr int kBufs = 512 / kCols > 4 ? 4 : 512 / kCols;  // TMEM group buffers
+  static constexpr int kTmemBudget = kPerSm == 2 ? 256 : 512;
+  static constexpr int kBufs = kTmemBudget / kCols > 4 ? 4 : kTmemBudget / kCols;  // TMEM group buffers
   // accumulation groups per tile: each group (a run of consecutive K stages)
   // accumulates in a fresh TMEM buffer and is added into fp32 registers with
   // round-to-nearest, bounding the tensor core's truncating accumulation to
   // K / kGroupsPerTile.  The MMAs run kBufs groups ahead of the accumulate
   // warps, so (kBufs / kGroupsPerTile) of a tile's MMA time hides that tile's
   // predecessor's epilogue: 2/3 of a tile for N = 256, a whole tile below.
-  static constexpr int kGroupsPerTile = BN >= 256 ? 3 : 4;
-  static constexpr int kTmemCols = kBufs * kCols;
+  static constexpr int kGroupsPerTile = BN >= 256 ? 3 : DX3 ? 2 : 4;
+  static constexpr int kTmemCols = kBufs * kCols <= 32 ? 32 : kBufs * kCols <= 64 ? 64
+                                   : kBufs * kCols <= 128 ? 128 : kBufs * kCols <= 256 ? 256 : 512;
   static constexpr int kHalf = BN / 2;
 };
 
 // HEAD: 0 plain conv; 1 / 2 (BN = 256 only) = the L9 training / validation
 // head fused into the epilogue (see HeadTrainArgs / HeadValArgs).
-template <int BN, int HEAD>
-__global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registers at 1 CTA/SM
+template <int BN, int HEAD, bool DX3 = false>
+__global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 registers at 1 CTA/SM
     k_conv3x3_dy(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
                  const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
@@ -814,7 +832,8 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
                  int flags, const float* __restrict__ bias, const void* __restrict__ mask,
                  int mask_bits, uint32_t* __restrict__ mbits_out, float* __restrict__ colsum,
                  float unscale, int H, int W, int C, int epi, HeadTrainArgs ht, HeadValArgs hv) {
-  using Cfg = DyCfg<BN>;
+  using Cfg = DyCfg<BN, DX3>;
+  static_assert(!DX3 || (HEAD == 0 && BN <= 64), "dx-stacked tiles: narrow plain convolutions");
   // flags: bits 8.. accumulation groups per tile (experiment override, 0 =
   // DyCfg::kGroupsPerTile)
   using P = Prec<true>;
@@ -835,7 +854,7 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
-  const int tiles_x = (W + 31) / 32;
+  const int tiles_x = (W + 2 * Cfg::kTileW - 1) / (2 * Cfg::kTileW);
   const int nunits = tiles_x * ((H + 7) / 8);
   const int KB = 3 * (C / Cfg::kKC);  // stages per tile
   const int gpt_req = (flags >> 8) ? (flags >> 8) : Cfg::kGroupsPerTile;
@@ -874,7 +893,7 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
     const int n0 = (int)rank * (BN / 2);
     int it = 0;
     for (int ut = cid; ut < nunits; ut += ncl) {
-      const int x0 = (ut % tiles_x) * 32 + 16 * (int)rank, y0 = (ut / tiles_x) * 8;
+      const int x0 = (ut % tiles_x) * 2 * Cfg::kTileW + Cfg::kTileW * (int)rank, y0 = (ut / tiles_x) * 8;
       for (int kb = 0; kb < KB; ++kb, ++it) {
         const int s = it % S, round = it / S;
         if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
@@ -930,22 +949,33 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
             tc_fence_after();
             if (elect_one_sync()) {
               const uint64_t a0 = desc0 + (uint64_t)(st * (Cfg::kStageBytes >> 4));
-#pragma unroll
-              for (int dx = 0; dx < 3; ++dx) {
+              if constexpr (DX3) {  // one MMA covers the three taps (B rows = [tap][n])
 #pragma unroll
                 for (int k = 0; k < Cfg::kKSteps; ++k) {
-                  const uint64_t a = a0 + Cfg::kDxUnits * dx + 2 * k;
-                  const uint64_t bh = a0 + kBh + kTap * dx + 2 * k;
-                  mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | dx | k) != 0);
+                  const uint64_t a = a0 + 2 * k, bh = a0 + kBh + 2 * k;
+                  mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | k) != 0);
                   mma_f16_2sm(d, a + kAl, bh, idesc, 1);
                 }
-              }
 #pragma unroll
-              for (int dx = 0; dx < 3; ++dx) {
+                for (int k = 0; k < Cfg::kKSteps; ++k) mma_f16_2sm(d, a0 + 2 * k, a0 + kBh + 2 * k, idesc, 1);
+              } else {
 #pragma unroll
-                for (int k = 0; k < Cfg::kKSteps; ++k)
-                  mma_f16_2sm(d, a0 + Cfg::kDxUnits * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k,
-                              idesc, 1);
+                for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+                  for (int k = 0; k < Cfg::kKSteps; ++k) {
+                    const uint64_t a = a0 + Cfg::kDxUnits * dx + 2 * k;
+                    const uint64_t bh = a0 + kBh + kTap * dx + 2 * k;
+                    mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | dx | k) != 0);
+                    mma_f16_2sm(d, a + kAl, bh, idesc, 1);
+                  }
+                }
+#pragma unroll
+                for (int dx = 0; dx < 3; ++dx) {
+#pragma unroll
+                  for (int k = 0; k < Cfg::kKSteps; ++k)
+                    mma_f16_2sm(d, a0 + Cfg::kDxUnits * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k,
+                                idesc, 1);
+                }
               }
               mma_commit_2sm(&empty[st]);
             }
@@ -965,7 +995,9 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
     // ---- group accumulation in registers (round-to-nearest fp32 adds)
     const int q = warp & 3;            // TMEM lane quarter
     const int half = (warp - 2) >> 2;  // column half
-    const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * HALF;
+    // DX3: this warp's columns are its channel half's three tap blocks
+    constexpr int ACOLS = DX3 ? 3 * HALF : HALF;
+    const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * ACOLS;
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
 #if N2F_TC_TRACE
     long long tw = 0, td = 0, te = 0, twr = 0, tcomp = 0, tstg = 0, tiss = 0, t_0 = clock64();
@@ -979,17 +1011,18 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
     }
     // this lane's pixel: GEMM row m = 32 q + lane = 8 * xl + yl
     const int xl = 4 * q + (lane >> 3), yl = lane & 7;
-    constexpr int EC = DyCfg<BN>::kEpiCols, CH = EC / 4;
+    constexpr int EC = Cfg::kEpiCols, CH = EC / 4;
     constexpr int RBY = EC * 4, RBH = EC * 2;  // staging row bytes: fp32 / fp16
     const int srow = lane;  // staging row: box {EC ch, 8 y, 4 x} staged [x][y][ch]
     uint8_t* stg0 = base + S * Cfg::kStageBytes + (warp - 2) * Cfg::kEpiWarpBytes;
     int gg = 0, sb = 0;
+    int tpar = 0;  // DX3 exchange buffer parity
     for (int ut = cid; ut < nunits; ut += ncl) {
-      const int x0 = (ut % tiles_x) * 32 + 16 * (int)rank, y0 = (ut / tiles_x) * 8;
+      const int x0 = (ut % tiles_x) * 2 * Cfg::kTileW + Cfg::kTileW * (int)rank, y0 = (ut / tiles_x) * 8;
       const int tile = ut * 2 + (int)rank;  // colsum row
-      float acc[HALF];
+      float acc[ACOLS];
 #pragma unroll
-      for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
+      for (int j = 0; j < ACOLS; ++j) acc[j] = 0.f;
       for (int g = 0; g < NG; ++g, ++gg) {
         const int b = gg % NB;
 #if N2F_TC_TRACE
@@ -1002,9 +1035,9 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
 #endif
         tc_fence_after();
         if (g == 0)
-          tmem_load_all<HALF>(lane_base + b * Cfg::kCols, acc);
+          tmem_load_all<ACOLS>(lane_base + b * Cfg::kCols, acc);
         else
-          drain_add<HALF>(lane_base + b * Cfg::kCols, acc);
+          drain_add<ACOLS>(lane_base + b * Cfg::kCols, acc);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty0 + 8u * b);
@@ -1016,11 +1049,37 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
       const long long ce = clock64();
 #endif
 
+      if constexpr (DX3) {
+        // out(column xl - 1) = tap0(xl - 1) + tap1(xl) + tap2(xl + 1): the
+        // neighbouring columns are 8 lanes away; at the quarter edges they
+        // come from the adjacent warp of this channel half through smem
+        float* xch = reinterpret_cast<float*>(base + S * Cfg::kStageBytes) +
+                     (size_t)((tpar * 2 + half) * 4) * 2 * 8 * HALF;
+        if (lane >= 24) {  // tap0 of this warp's last column, for warp q + 1
+#pragma unroll
+          for (int j = 0; j < HALF; ++j) xch[((q * 2 + 0) * 8 + (lane - 24)) * HALF + j] = acc[j];
+        }
+        if (lane < 8) {  // tap2 of this warp's first column, for warp q - 1
+#pragma unroll
+          for (int j = 0; j < HALF; ++j) xch[((q * 2 + 1) * 8 + lane) * HALF + j] = acc[2 * HALF + j];
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) {
+          float left = __shfl_up_sync(0xffffffffu, acc[j], 8);
+          float right = __shfl_down_sync(0xffffffffu, acc[2 * HALF + j], 8);
+          if (lane < 8) left = q > 0 ? xch[(((q - 1) * 2 + 0) * 8 + lane) * HALF + j] : 0.f;
+          if (lane >= 24) right = q < 3 ? xch[(((q + 1) * 2 + 1) * 8 + (lane - 24)) * HALF + j] : 0.f;
+          acc[j] = __fadd_rn(__fadd_rn(left, acc[HALF + j]), right);
+        }
+        tpar ^= 1;
+      }
+
       // ---- epilogue (see k_conv3x3_tc): scale removal, bias+ReLU or the ReLU
       // mask, column sums, bit masks, staging in the TMA swizzle layout and
-      // TMA tensor stores of {EC channels, 4 x, 8 y} boxes
-      const int px = x0 + xl, py = y0 + yl;
-      const bool valid = py < H && px < W;
+      // TMA tensor stores of {EC channels, 4 x, 8 y} boxes (DX3: direct stores)
+      const int px = x0 + xl - (DX3 ? 1 : 0), py = y0 + yl;
+      const bool valid = py < H && px < W && (!DX3 || (xl >= 1 && xl <= 14));
       const int n0 = half * HALF;
       constexpr int WPP = BN / 32, MW = HALF / 32 > 0 ? HALF / 32 : 1;
       const int64_t pix = (int64_t)py * W + px;
@@ -1225,6 +1284,38 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
             }
           }
           if ((lane & (32 / EC - 1)) == 0) csum[q][n + ch] = r[0];
+        }
+        if constexpr (DX3) {  // direct stores of this lane's pixel (EC channels)
+          if (valid) {
+            const int64_t idx = pix * BN + n;
+            if (omask & kOutY) {
+#pragma unroll
+              for (int k = 0; k < CH; ++k)
+                *reinterpret_cast<float4*>(out.y + idx + 4 * k) =
+                    make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            }
+            if (omask & (kOutHi | kOutLo)) {
+              uint32_t hw[EC / 2], lw[EC / 2];
+#pragma unroll
+              for (int i = 0; i < EC; i += 2) {
+                __half h0, l0, h1, l1;
+                split_f16(v[i] * oscale, h0, l0);
+                split_f16(v[i + 1] * oscale, h1, l1);
+                hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+                lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+              }
+#pragma unroll
+              for (int k = 0; k < EC / 8; ++k) {
+                if (omask & kOutHi)
+                  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out.yhi) + idx + 8 * k) =
+                      make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
+                if (omask & kOutLo)
+                  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out.ylo) + idx + 8 * k) =
+                      make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
+              }
+            }
+          }
+          continue;
         }
         // staging buffer sb: its previous TMA stores (two slices ago) must be done reading
         uint8_t* stg = stg0 + sb * Cfg::kEpiBuf;
@@ -1759,6 +1850,9 @@ int set_attr_one() {
   if (F16) {
     N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<BN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   DyCfg<BN>::kSmem));
+    if constexpr (BN <= 64)
+      N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<BN, 0, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, DyCfg<BN, true>::kSmem));
     if (BN == 256) {
       N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<256, 1>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, DyCfg<256>::kSmem));
@@ -1827,13 +1921,16 @@ int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask,
   return N2F_OK;
 }
 
-template <int BN, int HEAD>
+template <int BN, int HEAD, bool DX3 = false>
 int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
                    const HeadTrainArgs& ht, const HeadValArgs& hv, cudaStream_t st) {
+  if constexpr (HEAD == 0 && !DX3 && BN <= 64) {
+    if (pl.dx3) return launch_conv_dy<BN, 0, true>(pl, bias, mask, colsum, epi, ht, hv, st);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.grid);
   cfg.blockDim = dim3(kThreadsTc);
-  cfg.dynamicSmemBytes = DyCfg<BN>::kSmem;
+  cfg.dynamicSmemBytes = DyCfg<BN, DX3>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1848,7 +1945,7 @@ int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, fl
     const char* g = getenv("N2F_DY_GROUPS");  // accumulation groups per tile (experiment)
     return (g ? atoi(g) : 0) << 8;
   }();
-  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN, HEAD>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
+  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN, HEAD, DX3>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
                               pl.myh, pl.myl, pl.omask, pl.oscale,
                               ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, flags, bias, mask,
                               pl.mask_bits, pl.mbits_out, colsum, pl.unscale, pl.H, pl.W, pl.C, epi,
@@ -1966,15 +2063,21 @@ int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, 
   const char* dyenv = getenv("N2F_CONV_DY");
   const int dymode = dyenv ? atoi(dyenv) : 2;
   pl->dy = f16 && (dymode == 2 || (dymode == 1 && N <= 128));
+  // N2F_DY_DX3=1: narrow layers stack the dx taps in N (experiment: correct,
+  // but measured 1.5-2.4x slower than the per-tap MMAs)
+  const char* dx3env = getenv("N2F_DY_DX3");
+  pl->dx3 = pl->dy && N <= 64 && dx3env && atoi(dx3env) == 1;
   if (pl->dy) {
     pl->cs = 2;
-    const int units = ((W + 31) / 32) * ((H + 7) / 8);
+    const int pairw = pl->dx3 ? 28 : 32;  // 2 x DyCfg::kTileW output columns per pair tile
+    const int units = ((W + pairw - 1) / pairw) * ((H + 7) / 8);
     const int max_units = (N <= N2F_DY_2SM_MAXN ? 2 : 1) * sm_count() / 2;  // DyCfg<N>::kPerSm
     pl->grid = 2 * (units < max_units ? units : max_units);
     pl->tiles = 2 * units;
     const int kc = N2F_DY_KC16 && N == 256 ? 16 : 32;  // DyCfg<N>::kKC
-    N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, kc, 8, 18));
-    N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, kc, 8, 18));
+    const int boxw = pl->dx3 ? 16 : 18;  // DyCfg::kRowsA / 8 activation columns
+    N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, kc, 8, boxw));
+    N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, kc, 8, boxw));
     N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, kc, N / 2));
     N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, kc, N / 2));
     return N2F_OK;
@@ -2010,8 +2113,10 @@ int dy_epi_cols(int N) {
   }
 }
 
-int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any cluster size
-  return ((W + kTW - 1) / kTW) * 2 * ((H + 2 * kTH - 1) / (2 * kTH));
+int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any plan
+  const int per_tap = ((W + kTW - 1) / kTW) * 2 * ((H + 2 * kTH - 1) / (2 * kTH));
+  const int dx3 = 2 * ((W + 27) / 28) * ((H + 7) / 8);  // 14 x 8 tiles of the dx-stacked dy kernel
+  return per_tap > dx3 ? per_tap : dx3;
 }
 
 // Output tensor maps of a conv plan: NHWC [H][W][N] viewed as (N, W, H), box

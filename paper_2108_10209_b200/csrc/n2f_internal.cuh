@@ -95,6 +95,7 @@ struct ConvTcPlan {
   int dbg;        // profiling experiments only (N2F_TC_DEBUG)
   int cs;         // CTAs per cluster (2: cta_group::2 pair, M = 256)
   int dy;         // FP16 dy-stage halo kernel (16 x 8 pixel tiles per CTA)
+  int dx3;        // dy kernel with the dx taps stacked in N (14 x 8 output tiles, N <= 64)
   int tiles;      // 128-pixel tiles = rows of the colsum output
 };
 bool tc_supported(int cin, int cout);
