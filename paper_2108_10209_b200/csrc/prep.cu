@@ -35,7 +35,7 @@ double wall_seconds() {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kScanBlocks = 296;
+constexpr int kScanBlocks = 1184;  // 8 blocks per SM: the scan is HBM-bound
 
 template <typename T>
 __device__ __forceinline__ double load_as_double(const void* p, int64_t i) {
@@ -47,20 +47,45 @@ __device__ __forceinline__ double load_img(const void* p, int dtype, int64_t i) 
 }
 
 // min / max / non-finite count, stage 1 (per-block partials)
+__device__ __forceinline__ void minmax_acc(double v, double& lo, double& hi, double& bad) {
+  if (isfinite(v)) {
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  } else {
+    bad += 1.0;
+  }
+}
+
+// (min and max are exact in any order; the non-finite count is an exact
+// integer: the result does not depend on the partition)
 __global__ void __launch_bounds__(kThreads)
     k_minmax_part(const void* __restrict__ img, int dtype, int64_t n, double* __restrict__ part) {
   __shared__ double smin[kThreads], smax[kThreads], scnt[kThreads];
   double lo = INFINITY, hi = -INFINITY, bad = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = load_img(img, dtype, i);
-    if (isfinite(v)) {
-      lo = fmin(lo, v);
-      hi = fmax(hi, v);
-    } else {
-      bad += 1.0;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  int64_t head = 0;  // elements before the 16-byte vector body
+  if (dtype == N2F_F32 && (reinterpret_cast<uintptr_t>(img) & 15) == 0) {
+    const float4* v4 = reinterpret_cast<const float4*>(img);
+    const int64_t n4 = n / 4;
+    for (int64_t i = tid; i < n4; i += nth) {
+      const float4 v = __ldg(v4 + i);
+      minmax_acc(v.x, lo, hi, bad);
+      minmax_acc(v.y, lo, hi, bad);
+      minmax_acc(v.z, lo, hi, bad);
+      minmax_acc(v.w, lo, hi, bad);
     }
+    head = n4 * 4;
+  } else if (dtype == N2F_F64 && (reinterpret_cast<uintptr_t>(img) & 15) == 0) {
+    const double2* v2 = reinterpret_cast<const double2*>(img);
+    const int64_t n2 = n / 2;
+    for (int64_t i = tid; i < n2; i += nth) {
+      const double2 v = __ldg(v2 + i);
+      minmax_acc(v.x, lo, hi, bad);
+      minmax_acc(v.y, lo, hi, bad);
+    }
+    head = n2 * 2;
   }
+  for (int64_t i = head + tid; i < n; i += nth) minmax_acc(load_img(img, dtype, i), lo, hi, bad);
   smin[threadIdx.x] = lo;
   smax[threadIdx.x] = hi;
   scnt[threadIdx.x] = bad;
@@ -80,17 +105,32 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-__global__ void k_minmax_final(const double* __restrict__ part, int nparts, double* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(kThreads)
+    k_minmax_final(const double* __restrict__ part, int nparts, double* __restrict__ out) {
+  __shared__ double smin[kThreads], smax[kThreads], scnt[kThreads];
   double lo = INFINITY, hi = -INFINITY, bad = 0.0;
-  for (int i = 0; i < nparts; ++i) {
+  for (int i = threadIdx.x; i < nparts; i += kThreads) {
     lo = fmin(lo, part[3 * i]);
     hi = fmax(hi, part[3 * i + 1]);
     bad += part[3 * i + 2];
   }
-  out[0] = lo;
-  out[1] = hi;
-  out[2] = bad;
+  smin[threadIdx.x] = lo;
+  smax[threadIdx.x] = hi;
+  scnt[threadIdx.x] = bad;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + s]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+      scnt[threadIdx.x] += scnt[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = smin[0];
+    out[1] = smax[0];
+    out[2] = scnt[0];
+  }
 }
 
 // (x - vmin) / (vmax - vmin) in f64, rounded once to f32 (imaging.py:204, trainer.py:163)
@@ -102,9 +142,21 @@ __global__ void __launch_bounds__(kThreads)
     k_normalize(const void* __restrict__ img, int dtype, int64_t n, const double* __restrict__ mm,
                 float* __restrict__ norm) {
   const double vmin = mm[0], range = __dsub_rn(mm[1], mm[0]);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    norm[i] = norm_value(load_img(img, dtype, i), vmin, range);
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  int64_t head = 0;
+  if (dtype == N2F_F32 && (reinterpret_cast<uintptr_t>(img) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(norm) & 15) == 0) {  // 16-byte loads and stores
+    const float4* v4 = reinterpret_cast<const float4*>(img);
+    float4* o4 = reinterpret_cast<float4*>(norm);
+    const int64_t n4 = n / 4;
+    for (int64_t i = tid; i < n4; i += nth) {
+      const float4 v = __ldg(v4 + i);
+      o4[i] = make_float4(norm_value(v.x, vmin, range), norm_value(v.y, vmin, range),
+                          norm_value(v.z, vmin, range), norm_value(v.w, vmin, range));
+    }
+    head = n4 * 4;
+  }
+  for (int64_t i = head + tid; i < n; i += nth) norm[i] = norm_value(load_img(img, dtype, i), vmin, range);
 }
 
 __device__ __forceinline__ float clip01(float v, int clip) {
@@ -214,7 +266,7 @@ inline unsigned nblocks(int64_t n) { return (unsigned)((n + kThreads - 1) / kThr
 int launch_minmax(const void* img, int dtype, int64_t n, double* part, double* out3,
                   cudaStream_t st) {
   k_minmax_part<<<kScanBlocks, kThreads, 0, st>>>(img, dtype, n, part);
-  k_minmax_final<<<1, 32, 0, st>>>(part, kScanBlocks, out3);
+  k_minmax_final<<<1, kThreads, 0, st>>>(part, kScanBlocks, out3);
   ++g_launches;
   N2F_LAUNCH_CHECK();
   return N2F_OK;

@@ -467,8 +467,17 @@ __global__ void __launch_bounds__(kThreads)
   }
   const double vmin = mm ? mm[0] : vmin_arg;
   const double vmax = mm ? mm[1] : vmax_arg;
-  float acc = ring[(int64_t)first * plane + p];
-  for (int k = 1; k < n; ++k) acc = __fadd_rn(acc, ring[(int64_t)((first + k) % window) * plane + p]);
+  auto slot = [&](int k) { return __ldg(ring + (int64_t)((first + k) % window) * plane + p); };
+  float acc = slot(0);
+  int k = 1;
+  for (; k + 3 < n; k += 4) {  // four loads in flight, added in epoch order
+    const float a0 = slot(k), a1 = slot(k + 1), a2 = slot(k + 2), a3 = slot(k + 3);
+    acc = __fadd_rn(acc, a0);
+    acc = __fadd_rn(acc, a1);
+    acc = __fadd_rn(acc, a2);
+    acc = __fadd_rn(acc, a3);
+  }
+  for (; k < n; ++k) acc = __fadd_rn(acc, slot(k));
   const float mean = __fdiv_rn(acc, (float)n);
   out[p] = __dadd_rn(__dmul_rn((double)mean, __dsub_rn(vmax, vmin)), vmin);
 }
