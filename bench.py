@@ -380,6 +380,9 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "clocks": clk,
             "epochs_run": epochs, "psnr_noisy_db": psnr_in, "psnr_denoised_db": psnr_out,
+            # the stable kernel-side number: the early-stop epoch count of one
+            # image moves with last-bit changes (chaotic training)
+            "ms_per_epoch": max_ms / args.steps / epochs[-1],
         }
         print(json.dumps(line), flush=True)
     eng.close()
