@@ -15,5 +15,4 @@ cap dgL3 "k_conv3x3_dy" 12
 cap first_fwd "k_conv_first" 0
 cap first_wg "k_wgrad_first" 0
 cap adam "k_adam" 0
-cap colred "k_col_reduce" 0
 echo done
