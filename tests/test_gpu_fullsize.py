@@ -255,3 +255,21 @@ def test_config4_member_window_identity(oracle, seed):
     expect = oracle.denormalize(v.reshape(H, W), lo, hi)
     assert np.array_equal(out, expect)
     eng.close()
+
+
+def test_oversized_image_fails_cleanly_and_device_recovers():
+    """Beyond one GPU's memory (a 12288^2 context needs ~700 GB): a clean
+    error naming the allocation, nothing leaked, and the next fit works."""
+    from paper_2108_10209_b200 import TrainConfig, _lib, synthetic, train_single_channel
+    from paper_2108_10209_b200 import trainer as T
+
+    T.release_engines()
+    big = np.random.default_rng(0).random((12288, 12288), dtype=np.float32)
+    with pytest.raises(_lib.N2FError, match="memory|cudaMalloc"):
+        train_single_channel(big, TrainConfig(seed=0, max_epochs=1))
+    del big
+    clean = synthetic.blob_rect_image(64, 64, 2)
+    img = synthetic.gaussian_noisy(clean, 25 / 255, 3).astype(np.float64)
+    r = train_single_channel(img, TrainConfig(seed=0, max_epochs=2))
+    assert r.epochs_run == 2 and np.isfinite(r.denoised).all()
+    T.release_engines()
