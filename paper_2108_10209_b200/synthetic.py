@@ -86,8 +86,11 @@ def microscopy_image(h: int, w: int, seed: int) -> np.ndarray:
                     sig[ys + dy, xs + dx] += 0.6
     photons = 30.0 * sig / sig.max()
     counts = r.poisson(photons).astype(np.float64) + r.normal(0, 2.0, size=(h, w))
-    counts -= counts.min()
-    return (counts / counts.max()).astype(np.float32), (photons / 30.0).astype(np.float32)
+    lo = counts.min()
+    scale = (counts - lo).max()
+    # the clean signal on the noisy image's scale (the expected counts through
+    # the same affine normalisation), so PSNR compares like with like
+    return ((counts - lo) / scale).astype(np.float32), ((photons - lo) / scale).astype(np.float32)
 
 
 def config_image(cfg: int, seed: int = 0):
