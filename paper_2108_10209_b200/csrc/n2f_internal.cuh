@@ -17,13 +17,17 @@ void set_error(const std::string& msg);
 const std::string& error_text();
 int fail(int code, const char* fmt, ...);
 
+// On failure the runtime's (non-sticky) last-error slot is cleared too, so a
+// failed allocation is not reported again by the next launch check.
 #define N2F_CUDA(call)                                                                   \
   do {                                                                                   \
     cudaError_t e_ = (call);                                                             \
-    if (e_ != cudaSuccess)                                                               \
+    if (e_ != cudaSuccess) {                                                             \
+      (void)cudaGetLastError();                                                          \
       return ::n2f::fail(e_ == cudaErrorMemoryAllocation ? N2F_ERR_OOM : N2F_ERR_CUDA,   \
                          "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
                          __LINE__);                                                      \
+    }                                                                                    \
   } while (0)
 
 #define N2F_TRY(call)            \
