@@ -6,16 +6,25 @@
 
 A "step" is one complete fit-and-denoise of one image (normalise, pairs,
 init, every epoch until the early stop, window mean) with the reference's
-default TrainConfig.  N > 1 runs under torchrun, one process per GPU, each
-rank fitting its own images (no collective on the data path: weak scaling).
+default TrainConfig.  One process per GPU: under torchrun the ranks come from
+the environment; `--gpus N` without a torchrun environment launches the N
+ranks itself (torch.distributed.run on 127.0.0.1).  Images share nothing, so
+there is no collective on the data path: the process group is gloo, used
+only for the barriers around the timed region and the host-side MAX / SUM of
+per-rank device times (north_star (4): no NCCL).
 
-ours:       value = images/s with the input resident in HBM (Engine.fit_device,
-            CUDA events on the engine stream, max over ranks); e2e = the same
+ours:       value = images/s of config 2 with the input resident in HBM
+            (Engine.fit_device, CUDA events on the engine stream, max over
+            ranks; each rank fits K images: weak scaling); e2e = the same
             metric through the public API train_single_channel() with the
-            input in pinned host memory (H2D + D2H inside the timed region).
-reference:  the CPU oracle port (oracle/n2f_oracle.py) on the host cores, one
-            training epoch per step, extrapolated to a full fit with the
-            epoch count of the GPU fit of the same image (see --ref-epochs).
+            input in pinned host memory (H2D + D2H inside the timed region);
+            "config4" = BASELINE config 4, 64 images through a dynamic queue
+            over the N ranks (strong scaling: 64 / makespan).
+reference:  the STOCK reference package (baseline/_ref/noise2fast, installed
+            from /root/reference with pip; its own model.forward / backward /
+            apply_gradients and trainer.validate) on the host cores, one
+            training epoch per step, extrapolated to a full fit with the epoch
+            count of the GPU fit of the same image (profiles/bench_epochs.json).
 """
 
 from __future__ import annotations
@@ -23,6 +32,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,6 +41,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 import numpy as np  # noqa: E402
 
@@ -39,32 +50,93 @@ UNIT = "images/s"
 SIZE = 512
 SEED = 0
 EPOCHS_FILE = os.path.join(ROOT, "profiles", "bench_epochs.json")
+FLOP_PER_PIXEL_EPOCH = 16_392_512.0
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--conv-impl", type=int, default=0)
     p.add_argument("--ref-epochs", type=int, default=None,
                    help="epochs of a full fit used to extrapolate the CPU per-epoch time")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-config4", action="store_true",
+                   help="skip the BASELINE config-4 batch (64 images over the N GPUs)")
     p.add_argument("--host-loop", action="store_true",
                    help="launch every kernel from the host instead of the captured while-graph "
                         "(the same kernels; for ncu launch lists, which cannot see kernels inside "
                         "conditional graph nodes)")
-    p.add_argument("--workload", choices=["config2", "batch64"], default="config2",
-                   help="config2: K fits of the 512x512 image per GPU (weak scaling); batch64: "
-                        "BASELINE config 4, 64 images shared by all GPUs through a dynamic "
-                        "queue (strong scaling)")
-    return p.parse_args()
+    p.add_argument("--dry-run", action="store_true",
+                   help="launcher / process-group / reduction path only, no GPU work (CPU tests)")
+    return p.parse_args(argv)
 
 
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(n: int, argv: list[str]) -> int:
+    """Re-run this script as n ranks (one process per GPU) on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+           *argv]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+class Group:
+    """gloo process group for the host-side bookkeeping (barrier, MAX/SUM of
+    per-rank timings, the TCPStore queue); a no-op for one process."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def reduce(self, value: float, op: str) -> float:
+        if self.dist is None:
+            return float(value)
+        import torch
+
+        t = torch.tensor([float(value)], dtype=torch.float64)
+        self.dist.all_reduce(t, op=getattr(self.dist.ReduceOp, op))
+        return float(t.item())
+
+    def gather(self, value: float) -> list[float]:
+        if self.dist is None:
+            return [float(value)]
+        import torch
+
+        t = torch.tensor([float(value)], dtype=torch.float64)
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t)
+        return [float(x.item()) for x in out]
+
+    def store(self):
+        if self.dist is None:
+            return None
+        return self.dist.distributed_c10d._get_default_store()
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
 
 
 def workload():
@@ -77,10 +149,11 @@ def workload():
 def config_block(n_gpus):
     return {"workload": "config2: one 512x512 blob+rect image, gaussian sigma=50/255, seed 0; full "
                         "fit-and-denoise, reference default TrainConfig (bce, checkerboard, lr 1e-3, "
-                        "patience 100, window 100)",
+                        "patience 100, window 100); each GPU fits it K times",
             "image": [SIZE, SIZE], "images_per_step_per_gpu": 1,
-            "parallelism": f"independent images, {n_gpus} GPU(s), no collective",
-            "l2": "working set (activations ~1.5 GB) exceeds the 126 MB L2; no flush needed"}
+            "parallelism": f"independent images, {n_gpus} process(es) x 1 GPU, no collective "
+                           "(gloo for timing barriers only)",
+            "l2": "working set (activations ~1.4 GB per fit) exceeds the 126 MB L2; no flush needed"}
 
 
 def load_peaks():
@@ -155,37 +228,71 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU legs (oracle port) -- only here may bench.py execute oracle/
+# CPU legs: the stock reference from baseline/_ref (or, if it was not
+# installed, the oracle port) -- only here may bench.py execute them
 # ---------------------------------------------------------------------------
 
 
-def cpu_epoch_seconds(noisy: np.ndarray, reps: int = 1) -> tuple[float, int]:
-    """Time one training epoch (4 Adam steps + full-res validation) of the
-    oracle on the host cores; returns (seconds per epoch, BLAS threads)."""
-    from oracle import n2f_oracle as o
-
+def blas_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
 
-        threads = max([d.get("num_threads", 1) for d in threadpool_info()
-                       if d.get("user_api") == "blas"] or [1])
+        return max([d.get("num_threads", 1) for d in threadpool_info()
+                    if d.get("user_api") == "blas"] or [1])
     except Exception:
-        threads = os.cpu_count() or 1
-    norm, lo, hi, _ = o.normalize(noisy)
+        return os.cpu_count() or 1
+
+
+def reference_epoch_fn(noisy: np.ndarray):
+    """One training epoch (4 Adam steps + full-resolution validation) of the
+    reference CPU path on this image; returns (run_epoch, kind)."""
+    if os.path.isdir(os.path.join(REF_DIR, "noise2fast")):
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/n2f_numba_cache")
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from noise2fast import downsample, imaging, model, trainer  # the stock package
+
+        norm, _ = imaging.normalize_plane(np.asarray(noisy, np.float64))
+        norm = norm.astype(np.float32)
+        pairs = [(p.input[None, None], np.clip(p.target, 0.0, 1.0)[None, None])
+                 for p in downsample.make_training_pairs(norm, "checkerboard")]
+        net = model.build_network(1, SEED, lr=1e-3)
+
+        def run():  # trainer.py:182-190, the stock functions
+            for inp, tgt in pairs:
+                logits, cache = model.forward(net, inp, keep_cache=True)
+                _, grad = trainer._loss_and_grad(logits, tgt, "bce")
+                model.apply_gradients(net, model.backward(net, cache, grad))
+            trainer.validate(net, norm)
+
+        return run, "reference"
+    from oracle import n2f_oracle as o
+
+    norm, _, _, _ = o.normalize(noisy)
     n32 = norm.astype(np.float32)
     pairs = o.training_pairs(n32)
     net = o.init_net(SEED)
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
+
+    def run_port():
         for a, b in pairs:
             z, cache = o.net_forward(net, a, keep=True)
             _, gz = o.bce_logits(z, b)
             o.net_step(net, o.net_backward(net, cache, gz), 1e-3)
-        out = o.predict(net, n32)
-        o.val_score(out, n32)
+        o.val_score(o.predict(net, n32), n32)
+
+    return run_port, "port"
+
+
+def cpu_epoch_seconds(noisy: np.ndarray, reps: int = 1, warm: int = 0):
+    run, kind = reference_epoch_fn(noisy)
+    for _ in range(warm):
+        run()
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
         times.append(time.perf_counter() - t0)
-    return min(times), threads
+    return times, blas_threads(), kind
 
 
 def recorded_epochs(default=None):
@@ -198,30 +305,25 @@ def recorded_epochs(default=None):
 
 def run_reference(args):
     rank, _, world = dist_env()
-    if rank != 0:
+    if rank != 0:  # the reference is a single-process CPU path: rank 0 alone runs it
         return
     noisy, _ = workload()
     epochs = args.ref_epochs or recorded_epochs(150)
-    for _ in range(max(0, min(args.warmup, 1))):  # one warm-up epoch primes BLAS/allocations
-        cpu_epoch_seconds(noisy)
     t0 = time.perf_counter()
-    per = []
-    threads = 1
-    for _ in range(args.steps):
-        s, threads = cpu_epoch_seconds(noisy)
-        per.append(s)
+    per, threads, kind = cpu_epoch_seconds(noisy, reps=args.steps, warm=min(args.warmup, 1))
     wall = time.perf_counter() - t0
     s_epoch = sum(per) / len(per)
     value = 1.0 / (s_epoch * epochs)
-    sample = (f"one training epoch (4 Adam steps + 512x512 validation) of the oracle port per step, "
-              f"{s_epoch:.2f} s/epoch, extrapolated x{epochs} epochs (epochs_run of the GPU fit of the "
-              f"same image)")
+    sample = (f"one training epoch (4 Adam steps + 512x512 validation) per step through the "
+              f"{'stock reference package (baseline/_ref/noise2fast)' if kind == 'reference' else 'oracle port'}"
+              f", {s_epoch:.2f} s/epoch on {threads} BLAS threads, extrapolated x{epochs} epochs "
+              f"(epochs_run of the GPU fit of the same image)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * s_epoch * epochs, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_block(world), "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": sample, "s_per_epoch": per, "extrapolation_epochs": epochs},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": wall}
     print(json.dumps(line), flush=True)
@@ -232,29 +334,81 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 
+def run_config4(group, rank, local, world, warm_eng):
+    """BASELINE config 4: 64 independent 512x512 images (per-image seed, sigma
+    ~ U(15,50)/255) shared by all ranks through the TCPStore dynamic queue;
+    value = 64 / max-over-ranks device time (strong scaling)."""
+    import torch
+
+    from paper_2108_10209_b200 import _lib, pool, synthetic
+
+    n_img = 64
+    eng = warm_eng
+    stream = torch.cuda.ExternalStream(eng.stream)
+    out = torch.empty((SIZE, SIZE), dtype=torch.float64, device="cuda")
+    img = torch.empty((SIZE, SIZE), dtype=torch.float32, device="cuda")
+    host = {}
+    group.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    done, epochs = [], []
+    for i in pool.claim(group.store(), "bench/config4", n_img):
+        if i not in host:
+            host[i] = torch.from_numpy(synthetic.config_image(4, seed=1000 + i)[0]).pin_memory()
+        img.copy_(host[i], non_blocking=True)
+        eng.set_seed(1000 + i)  # per-image network seed, like the CLI's per-file seeds
+        r = eng.fit_device(img.data_ptr(), _lib.N2F_F32, out.data_ptr())
+        done.append(i)
+        epochs.append(r.epochs_run)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    max_ms = group.reduce(ms, "MAX")
+    total_epochs = group.reduce(sum(epochs), "SUM")
+    busy_ms = group.gather(ms)
+    per_rank = group.gather(len(done))
+    flop = FLOP_PER_PIXEL_EPOCH * SIZE * SIZE * total_epochs
+    return {"value": n_img / (max_ms / 1e3), "unit": UNIT, "scaling": "strong",
+            "workload": "config4: 64 independent 512x512 blob+rect images, per-image seed, gaussian "
+                        "sigma ~ U(15,50)/255, dynamic queue (TCPStore counter) over the GPUs",
+            "makespan_ms": max_ms, "total_epochs": total_epochs, "per_gpu_busy_ms": busy_ms,
+            "per_gpu_images": per_rank, "imbalance_max_over_mean": pool.imbalance(busy_ms),
+            "algorithmic_tflops_per_gpu": flop / (max_ms * 1e-3) / world / 1e12}
+
+
 def run_ours(args):
+    rank, local, world = dist_env()
+    group = Group(world)
+    if args.dry_run:
+        t0 = time.perf_counter()
+        group.barrier()
+        ms = 1e3 * (time.perf_counter() - t0)
+        max_ms = group.reduce(ms, "MAX")
+        pids = group.gather(os.getpid())
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                              "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms,
+                              "dry_run": True, "rank_pids": [int(p) for p in pids],
+                              "backend": "gloo" if world > 1 else "none"}), flush=True)
+        group.close()
+        return
+
     import torch
 
     from paper_2108_10209_b200 import Engine, TrainConfig, _lib, train_single_channel
     from paper_2108_10209_b200 import trainer as T
 
-    rank, local, world = dist_env()
     torch.cuda.set_device(local)
     os.environ["N2F_DEVICE"] = str(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
-        if dist is not None:
-            dist.barrier()
         torch.cuda.synchronize()
+        group.barrier()
 
     noisy, clean = workload()
     cfg = TrainConfig(seed=SEED)
-    eng = Engine(SIZE, SIZE, cfg, device=local, conv_impl=args.conv_impl, use_graph=not args.host_loop)
+    eng = Engine(SIZE, SIZE, cfg, device=local, use_graph=not args.host_loop)
     stream = torch.cuda.ExternalStream(eng.stream)
     img = torch.from_numpy(noisy).cuda()
     out = torch.empty((SIZE, SIZE), dtype=torch.float64, device="cuda")
@@ -279,10 +433,7 @@ def run_ours(args):
     e1.synchronize()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = group.reduce(ms, "MAX")
     value = world * args.steps / (max_ms / 1e3)
     denoised = out.cpu().numpy()
 
@@ -300,12 +451,11 @@ def run_ours(args):
         res = train_single_channel(host_in, cfg)
     a1.record(api_stream)
     a1.synchronize()
-    t2 = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
-    if dist is not None:
-        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_value = world * args.steps / (float(t2.item()) / 1e3)
+    e2e_ms = group.reduce(a0.elapsed_time(a1), "MAX")
+    e2e_value = world * args.steps / (e2e_ms / 1e3)
     h2d = SIZE * SIZE * 4
     d2h = SIZE * SIZE * 8 + res.epochs_run * (8 + 32 + 8) + 64
+    T.release_engines()
 
     # ---- dominant kernel roofline: one profiled epoch on the same engine and
     # stream right after the timed region (CUDA events around every launch)
@@ -319,14 +469,6 @@ def run_ours(args):
     shares = {name: round(float(pms[i].sum() / pms.sum()), 4) for i, name in enumerate(Engine.PROF_CLASSES)}
     epoch_ms_profiled = float(pms.sum())
     conv_tf = float(pfl[[1, 3, 4, 8]].sum() / (pms[[1, 3, 4, 8]].sum() * 1e-3) / 1e12)
-    # the split-precision kernels issue 3 MMAs per algorithmic MAC: FP16x3 at
-    # the fp16/bf16 dense rate (the default), 3xTF32 at half that rate
-    if args.conv_impl == 2:
-        mma_note, mma_cost = "3xTF32: 3 tf32 MMAs (half the bf16 rate) per algorithmic MAC", 2.0
-    elif args.conv_impl == 1:
-        mma_note, mma_cost = "SIMT fp32 (no tensor cores)", 0.0
-    else:
-        mma_note, mma_cost = "FP16x3: 3 fp16 MMAs (bf16 dense rate) per algorithmic MAC", 1.0
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")) as f:
@@ -337,6 +479,10 @@ def run_ours(args):
     except Exception:
         pass
 
+    config4 = None
+    if not args.no_config4:
+        config4 = run_config4(group, rank, local, world, eng)
+
     if rank == 0:
         os.makedirs(os.path.dirname(EPOCHS_FILE), exist_ok=True)
         try:
@@ -346,14 +492,16 @@ def run_ours(args):
             pass
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        s_epoch, threads = cpu_epoch_seconds(noisy)
-        cpu_value = 1.0 / (s_epoch * epochs[-1])
-        cpu = {"value": cpu_value, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"one training epoch (4 Adam steps + 512x512 validation) of the oracle port, "
-                         f"{s_epoch:.2f} s, extrapolated x{epochs[-1]} epochs (this GPU fit's epochs_run)"}
+        per, threads, kind = cpu_epoch_seconds(noisy)
+        cpu_value = 1.0 / (per[0] * epochs[-1])
+        cpu = {"value": cpu_value, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"one training epoch (4 Adam steps + 512x512 validation) of the "
+                         f"{'stock reference (baseline/_ref)' if kind == 'reference' else 'oracle port'}"
+                         f", {per[0]:.2f} s on {threads} BLAS threads, extrapolated x{epochs[-1]} "
+                         f"epochs (this GPU fit's epochs_run)"}
     psnr_in = 10 * np.log10(1.0 / np.mean((noisy.astype(np.float64) - clean) ** 2))
     psnr_out = 10 * np.log10(1.0 / np.mean((denoised - clean) ** 2))
-    epoch_flop = 16392512.0 * SIZE * SIZE
+    epoch_flop = FLOP_PER_PIXEL_EPOCH * SIZE * SIZE
     path_tflops = epoch_flop * epochs[-1] * world * args.steps / (max_ms * 1e-3) / 1e12
     sus_tf = load_sustained_tflops()
     if rank == 0:
@@ -368,17 +516,19 @@ def run_ours(args):
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved / peak_tf, "traffic": traffic,
                          "kernel": kname, "kernel_ms": kms, "kernel_algorithmic_flop": kflop,
-                         "peak_kind": f"{peak_kind} bf16 dense burst; {mma_note}",
-                         "mma_frac": achieved * 3 * mma_cost / peak_tf,
+                         "peak_kind": f"{peak_kind} bf16 dense burst; FP16x3: 3 fp16 MMAs (bf16 "
+                                      "dense rate) per algorithmic MAC, so the 3-pass ceiling is 1/3",
+                         "mma_frac": achieved * 3 / peak_tf,
                          "conv_kernels_tflops": conv_tf, "epoch_ms_profiled": epoch_ms_profiled,
                          "time_share": shares,
                          "path_tflops": path_tflops, "path_frac": path_tflops / peak_tf,
                          # the whole timed fit against the sustained tensor rate (cuBLAS bf16
                          # back to back, MEASURED_PEAKS.json), with the 3 MMAs per MAC counted
                          "peak_sustained": sus_tf,
-                         "path_mma_frac_sustained": (path_tflops * 3 * mma_cost / sus_tf) if sus_tf else None},
+                         "path_mma_frac_sustained": (path_tflops * 3 / sus_tf) if sus_tf else None},
             "cpu_baseline": cpu,
             "clocks": clk,
+            "config4": config4,
             "epochs_run": epochs, "psnr_noisy_db": psnr_in, "psnr_denoised_db": psnr_out,
             # the stable kernel-side number: the early-stop epoch count of one
             # image moves with last-bit changes (chaotic training)
@@ -386,81 +536,16 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     eng.close()
-    T.release_engines()
-    if dist is not None:
-        dist.destroy_process_group()
+    group.close()
 
 
-def run_batch64(args):
-    """BASELINE config 4: 64 independent 512x512 images (per-image seed, sigma
-    ~ U(15,50)/255) shared by all ranks through a store-backed dynamic queue;
-    value = 64 / max-over-ranks device time (strong scaling)."""
-    import torch
-
-    from paper_2108_10209_b200 import Engine, TrainConfig, _lib, pool, synthetic
-
-    rank, local, world = pool.dist_env()
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n_img = 64
-    images = [synthetic.config_image(4, seed=1000 + i)[0] for i in range(n_img)]
-    eng = Engine(SIZE, SIZE, TrainConfig(seed=0), device=local, conv_impl=args.conv_impl,
-                 use_graph=not args.host_loop)
-    stream = torch.cuda.ExternalStream(eng.stream)
-    out = torch.empty((SIZE, SIZE), dtype=torch.float64, device="cuda")
-    img = torch.empty((SIZE, SIZE), dtype=torch.float32, device="cuda")
-    for _ in range(max(1, args.warmup)):  # warm the engine (graph, caches) on image 0
-        img.copy_(torch.from_numpy(images[0]))
-        eng.fit_device(img.data_ptr(), _lib.N2F_F32, out.data_ptr())
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    store = pool.default_store()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    done, epochs = [], []
-    for i in pool.claim(store, "bench/batch64", n_img):
-        img.copy_(torch.from_numpy(images[i]), non_blocking=False)
-        eng.set_seed(1000 + i)  # per-image network seed, like the CLI's per-file seeds
-        r = eng.fit_device(img.data_ptr(), _lib.N2F_F32, out.data_ptr())
-        done.append(i)
-        epochs.append(r.epochs_run)
-    e1.record(stream)
-    e1.synchronize()
-    ms = e0.elapsed_time(e1)
-    max_ms = pool.max_over_ranks(ms, device="cuda")
-    total_epochs = pool.sum_over_ranks(sum(epochs), device="cuda")
-    busy_ms = pool.gather_over_ranks(ms, device="cuda")
-    n_per_rank = pool.gather_over_ranks(len(done), device="cuda")
-    flop = 16_392_512.0 * SIZE * SIZE * total_epochs  # SURVEY.md §8(a): FLOP per pixel-epoch
-    if rank == 0:
-        print(json.dumps({
-            "metric": METRIC, "value": n_img / (max_ms / 1e3), "unit": UNIT, "n_gpus": world,
-            "steps": 1, "warmup": args.warmup, "ms_per_step": max_ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "config4: 64 independent 512x512 blob+rect images, per-image "
-                                   "seed, gaussian sigma ~ U(15,50)/255, dynamic queue over GPUs",
-                       "images": n_img, "parallelism": f"{world} GPU(s), no collective on the data path"},
-            "rank0_images": len(done), "rank0_ms": ms, "total_epochs": total_epochs,
-            "per_gpu_busy_ms": busy_ms, "per_gpu_images": n_per_rank,
-            "imbalance_max_over_mean": pool.imbalance(busy_ms),
-            "algorithmic_tflops_per_gpu": flop / (max_ms * 1e-3) / world / 1e12,
-        }), flush=True)
-    eng.close()
-    if dist is not None:
-        dist.destroy_process_group()
-
-
-def main():
-    args = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args.gpus, argv))
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload == "batch64":
-        run_batch64(args)
     else:
         run_ours(args)
 

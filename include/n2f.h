@@ -30,7 +30,9 @@ typedef enum n2f_status {
   N2F_ERR_NONFINITE = 2,  /* image contains NaN/Inf (trainer.py:142-143)  */
   N2F_ERR_CUDA = 3,       /* CUDA runtime/driver failure                   */
   N2F_ERR_OOM = 4,        /* device allocation failed                      */
-  N2F_ERR_UNSUPPORTED = 5 /* config value not implemented                  */
+  N2F_ERR_UNSUPPORTED = 5, /* config value not implemented                 */
+  N2F_ERR_RANGE = 6        /* an FP16x3 operand left fp16's range (see the
+                              range guard below); the fit was stopped      */
 } n2f_status;
 
 /* TrainConfig (trainer.py:29-51). loss: 0 = "bce", 1 = "mse";
@@ -42,14 +44,16 @@ typedef struct n2f_config {
   int32_t patience_epochs;
   int32_t avg_window;
   int32_t max_epochs;
-  int32_t conv_impl;      /* 0 = auto (= 3), 1 = SIMT fp32, 2 = tcgen05 3xTF32, 3 = tcgen05 FP16x3 */
+  int32_t conv_impl;      /* 0 = auto (= 3) or 3 = tcgen05 FP16x3, the only implementation;
+                             any other value is N2F_ERR_UNSUPPORTED */
   uint64_t seed;
   int32_t use_graph;      /* 1 = whole loop in one CUDA graph (while node), 0 = host loop */
   int32_t reserved[7];
 } n2f_config;
 
 /* stop_reason codes (trainer.py:74) */
-enum { N2F_STOP_PATIENCE = 0, N2F_STOP_MAX_EPOCHS = 1, N2F_STOP_DEGENERATE = 2 };
+enum { N2F_STOP_PATIENCE = 0, N2F_STOP_MAX_EPOCHS = 1, N2F_STOP_DEGENERATE = 2,
+       N2F_STOP_RANGE = 3 /* internal: the fit returns N2F_ERR_RANGE */ };
 
 /* Per-image outcome (DenoiseResult, trainer.py:69-75).  The optional history
  * buffers are HOST arrays supplied by the caller, each sized for max_epochs
@@ -110,13 +114,21 @@ int n2f_init_layer(uint64_t seed, int layer, int cin, int cout, int k, float* w_
                    void* stream);
 
 /* conv forward (+bias, +ReLU when relu != 0), NHWC activations:
- * x [h*w][cin], w [cout][k][k][cin], y [h*w][cout] (tensor.py:490-506). */
+ * x [h*w][cin], w [cout][k][k][cin], y [h*w][cout] (tensor.py:490-506).
+ * Runs the engine's kernels: 3x3 with cin % 32 == 0 and cout in {32, 64,
+ * 128, 256} on the tcgen05 FP16x3 kernel (operands split at the engine's
+ * scales), 3x3 with cin == 1 on the first-layer kernel, and 1x1 (the head,
+ * fused into the L8 epilogue inside the engine) on a direct kernel; other
+ * shapes return N2F_ERR_UNSUPPORTED.  impl: 0 or 3. */
 int n2f_conv_fwd(const float* x, const float* w, const float* b, float* y, int h, int wd,
                  int cin, int cout, int k, int relu, int impl, void* stream);
 
 /* conv backward (tensor.py:509-530): g is the gradient at the pre-activation
  * [h*w][cout]; dx [h*w][cin] = conv^T(g) masked by (mask > 0) when mask != NULL;
- * dw [cout][k][k][cin], db [cout].  Any of dx/dw may be NULL to skip it. */
+ * dw [cout][k][k][cin], db [cout].  Any of dx/dw/db may be NULL to skip it.
+ * Same kernels and shape rules as n2f_conv_fwd (dgrad: the tcgen05 kernel
+ * with cout % 32 == 0 and cin in {32, 64, 128, 256}; dw: tcgen05 wgrad, or
+ * the first-layer wgrad for cin == 1 and cout == 32). */
 int n2f_conv_bwd(const float* g, const float* x, const float* w, const float* mask, float* dx,
                  float* dw, float* db, int h, int wd, int cin, int cout, int k, int impl,
                  void* stream);
@@ -159,16 +171,6 @@ int n2f_ctx_set_seed(n2f_ctx* ctx, uint64_t seed);
 int n2f_ctx_get_arena(n2f_ctx* ctx, int which, float* host);
 int n2f_ctx_set_params(n2f_ctx* ctx, const float* host);
 int n2f_ctx_set_arena(n2f_ctx* ctx, int which, const float* host, int adam_step);
-/* tcgen05 self-test: D[128 x n] = A[128 x 32] . B[n x 32]^T through one
- * kind::tf32 MMA chain with K-major (0) or MN-major (1) SWIZZLE_128B operands. */
-int n2f_tc_selftest(const float* a, const float* b, float* d, int n, int a_mn, int b_mn,
-                    void* stream);
-/* kind::f16 self-test: fp16 A[128 x 64], B[n x 64] (K-major 0 / MN-major 1). */
-int n2f_tc_selftest_f16(const uint16_t* a, const uint16_t* b, float* d, int n, int a_mn, int b_mn,
-                        void* stream);
-/* 2-SM (cta_group::2, cluster of 2) kind::f16 self-test: D[256 x n] = A[256 x 64] . B[n x 64]^T,
- * K-major SWIZZLE_128B, CTA r staging A rows [128r, 128r+128) and B rows [rn/2, (r+1)n/2). */
-int n2f_tc_selftest_2sm(const uint16_t* a, const uint16_t* b, float* d, int n, void* stream);
 int n2f_ctx_step(n2f_ctx* ctx, int pair, float* logits_host);
 int n2f_ctx_epoch(n2f_ctx* ctx, int* stopped);
 /* Profile one epoch: per (class, layer) device ms / algorithmic FLOPs / launches
@@ -180,6 +182,20 @@ int n2f_ctx_profile_epoch(n2f_ctx* ctx, double* ms, double* flop, int* launches)
 int n2f_ctx_validate(n2f_ctx* ctx, float* out_host, double* score);
 int n2f_ctx_get_pairs(n2f_ctx* ctx, float* pair_in, float* pair_tgt, float* norm, int ph[4],
                       int pw[4]);
+
+/* ---- FP16x3 range guard ----------------------------------------------------
+ * Every tensor-core operand is an fp16 pair of x * 2^e (activations and
+ * weights e = 8, gradients e = ceil(log2 P) + 8).  Each epoch the kernels
+ * that write such pairs record max |x * 2^e| per (tensor class, layer) slot:
+ * slot = class * 9 + layer, classes 0 training activations (output of
+ * layer), 1 validation activations, 2 gradients (at the output of layer),
+ * 3 weights.  A slot >= 2^15 (or a non-finite validation score) stops the
+ * fit: n2f_fit_denoise_* and n2f_ctx_epoch return N2F_ERR_RANGE naming the
+ * slot.  range_history copies the per-epoch maxima of the last fit (or of the
+ * epochs run since n2f_ctx_prepare / set_params): [n_epochs][N2F_RANGE_SLOTS]
+ * floats (0 = no pair written in that slot), at most max_rows rows. */
+#define N2F_RANGE_SLOTS 36
+int n2f_ctx_range_history(n2f_ctx* ctx, float* host, int max_rows, int* n_rows);
 
 /* ---- image-quality metrics (benchmark mode; imaging.psnr / imaging.ssim,
  * imaging.py:249-311), f64 device buffers of one single-channel plane ------ */

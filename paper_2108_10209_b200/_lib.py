@@ -14,7 +14,10 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("N2F_LIB") or os.path.join(_HERE, "libn2f.so")  # N2F_LIB: A/B variants
 
-N2F_OK, N2F_ERR_ARG, N2F_ERR_NONFINITE, N2F_ERR_CUDA, N2F_ERR_OOM, N2F_ERR_UNSUPPORTED = range(6)
+(N2F_OK, N2F_ERR_ARG, N2F_ERR_NONFINITE, N2F_ERR_CUDA, N2F_ERR_OOM, N2F_ERR_UNSUPPORTED,
+ N2F_ERR_RANGE) = range(7)
+N2F_RANGE_SLOTS = 36  # range guard: class * 9 + layer (include/n2f.h)
+RANGE_CLASSES = ("act", "val_act", "grad", "weight")
 N2F_F32, N2F_F64 = 0, 1
 STOP_REASONS = {0: "patience", 1: "max_epochs", 2: "degenerate"}
 
@@ -87,9 +90,6 @@ SIGNATURES = {
     "n2f_ctx_get_arena": [_P, _I, _P],
     "n2f_ctx_set_params": [_P, _P],
     "n2f_ctx_set_arena": [_P, _I, _P, _I],
-    "n2f_tc_selftest": [_P, _P, _P, _I, _I, _I, _P],
-    "n2f_tc_selftest_f16": [_P, _P, _P, _I, _I, _I, _P],
-    "n2f_tc_selftest_2sm": [_P, _P, _P, _I, _P],
     "n2f_ctx_step": [_P, _I, _P],
     "n2f_ctx_epoch": [_P, _P],
     "n2f_ctx_profile_epoch": [_P, _P, _P, _P],
@@ -100,6 +100,7 @@ SIGNATURES = {
     "n2f_ssim": [_P, _P, _I, _I, _D, _D, _D, _P, _P],
     "n2f_device_count": [_P],
     "n2f_ctx_set_seed": [_P, C.c_uint64],
+    "n2f_ctx_range_history": [_P, _P, _I, C.POINTER(C.c_int)],
 }
 _RESTYPES = {
     "n2f_last_error": C.c_char_p,

@@ -73,21 +73,21 @@ __global__ void k_conv1x1_dw(const float* __restrict__ g, const float* __restric
 
 unsigned nb(int64_t n) { return (unsigned)((n + 255) / 256); }
 
-// Tensor-core operand pair of an fp32 device tensor (scratch-owned).
-int make_operand(Scratch& s, const float* x, int64_t n, bool f16, int exp, TcOperand* op,
-                 cudaStream_t st) {
-  if (!f16) {
-    float* lo;
-    N2F_TRY(s.get(&lo, (size_t)n));
-    N2F_TRY(split_lo(x, lo, n, st));
-    *op = {x, lo, 0};
-    return N2F_OK;
-  }
+// Tensor-core operand (fp16 pair of x * 2^exp) of an fp32 device tensor
+// (scratch-owned).
+int make_operand(Scratch& s, const float* x, int64_t n, int exp, TcOperand* op, cudaStream_t st) {
   uint16_t *hi, *lo;
   N2F_TRY(s.get(&hi, (size_t)n));
   N2F_TRY(s.get(&lo, (size_t)n));
   N2F_TRY(split_f16(x, hi, lo, exp, n, st));
   *op = {hi, lo, exp};
+  return N2F_OK;
+}
+
+int check_impl(int impl) {
+  if (impl != kImplAuto && impl != kImplTcF16)
+    return fail(N2F_ERR_UNSUPPORTED, "conv impl %d: this library implements only tcgen05 FP16x3 (0/3)",
+                impl);
   return N2F_OK;
 }
 
@@ -143,29 +143,25 @@ int n2f_init_layer(uint64_t seed, int layer, int cin, int cout, int k, float* w,
 
 int n2f_conv_fwd(const float* x, const float* w, const float* b, float* y, int h, int wd, int cin,
                  int cout, int k, int relu, int impl, void* stream) {
-  (void)impl;
   if (!x || !w || !b || !y || h < 1 || wd < 1) return fail(N2F_ERR_ARG, "n2f_conv_fwd");
+  N2F_TRY(check_impl(impl));
   const int64_t P = (int64_t)h * wd;
   if (k == 1) {
     k_conv1x1_fwd<<<nb(P * cout), 256, 0, S(stream)>>>(x, w, b, y, P, cin, cout, relu);
     N2F_LAUNCH_CHECK();
   } else if (k == 3 && cin == 1) {
     N2F_TRY(conv_first_simt(x, w, b, y, h, wd, cout, S(stream), relu));
-  } else if (k == 3 && (impl == kImplTc || impl == kImplTcF16) && tc_supported(cin, cout)) {
+  } else if (k == 3 && tc_supported(cin, cout)) {
     static Scratch s;  // kept alive across async calls on an explicit stream
     for (void* q : s.ptrs) cudaFree(q);
     s.ptrs.clear();
-    const bool f16 = impl == kImplTcF16;
     TcOperand ox, ow;
-    N2F_TRY(make_operand(s, x, P * cin, f16, kExpAct, &ox, S(stream)));
-    N2F_TRY(make_operand(s, w, (int64_t)cout * 9 * cin, f16, kExpW, &ow, S(stream)));
+    N2F_TRY(make_operand(s, x, P * cin, kExpAct, &ox, S(stream)));
+    N2F_TRY(make_operand(s, w, (int64_t)cout * 9 * cin, kExpW, &ow, S(stream)));
     ConvTcPlan pl;
-    N2F_TRY(conv_tc_plan(&pl, ox, ow, h, wd, cin, cout, f16));
+    N2F_TRY(conv_tc_plan(&pl, ox, ow, h, wd, cin, cout));
     N2F_TRY(conv_tc_plan_out(&pl, y, nullptr, nullptr, 1.f));
     N2F_TRY(conv_tc_launch(pl, b, nullptr, nullptr, relu ? kEpiBiasRelu : kEpiBias, S(stream)));
-  } else if (k == 3 && cin % 8 == 0 && cout % 32 == 0) {
-    N2F_TRY(conv3x3_simt(x, w, b, nullptr, y, h, wd, cin, cout, relu ? kEpiBiasRelu : kEpiBias,
-                         S(stream)));
   } else {
     return fail(N2F_ERR_UNSUPPORTED, "conv_fwd: unsupported shape cin=%d cout=%d k=%d", cin, cout, k);
   }
@@ -176,8 +172,8 @@ int n2f_conv_fwd(const float* x, const float* w, const float* b, float* y, int h
 int n2f_conv_bwd(const float* g, const float* x, const float* w, const float* mask, float* dx,
                  float* dw, float* db, int h, int wd, int cin, int cout, int k, int impl,
                  void* stream) {
-  (void)impl;
   if (!g || h < 1 || wd < 1) return fail(N2F_ERR_ARG, "n2f_conv_bwd");
+  N2F_TRY(check_impl(impl));
   const int64_t P = (int64_t)h * wd;
   Scratch s;
   if (k == 1) {
@@ -193,54 +189,49 @@ int n2f_conv_bwd(const float* g, const float* x, const float* w, const float* ma
     return N2F_OK;
   }
   if (k != 3) return fail(N2F_ERR_UNSUPPORTED, "conv_bwd: k=%d", k);
-  if (dw || db) {
-    const int ns = wgrad_nsplit(P, cin, cout);
+  if (dx && !tc_supported(cout, cin))
+    return fail(N2F_ERR_UNSUPPORTED, "conv_bwd dgrad: cin %d cout %d", cin, cout);
+  if (dw && !(cin == 1 && cout == 32) && !tc_supported(cin, cout))
+    return fail(N2F_ERR_UNSUPPORTED, "conv_bwd wgrad: cin %d cout %d", cin, cout);
+  // db: the column sums of g ([P][cout]) -- the fixed-order partial reduction
+  // with one "split" per pixel (inside the engine they come from the dgrad /
+  // head epilogues and the first-layer wgrad)
+  if (db) N2F_TRY(reduce_partials(g, db, (int)P, cout, S(stream)));
+  if (dw && cin == 1) {
+    const int ns = wgrad_first_nsplit(P);
     float *pw, *pb;
-    N2F_TRY(s.get(&pw, (size_t)ns * cout * 9 * cin));
+    N2F_TRY(s.get(&pw, (size_t)ns * cout * 9));
     N2F_TRY(s.get(&pb, (size_t)ns * cout));
-    if (cin == 1)
-      N2F_TRY(wgrad_first_simt(g, x, pw, pb, h, wd, cout, ns, S(stream)));
-    else
-      N2F_TRY(wgrad3x3_simt(g, x, pw, pb, h, wd, cin, cout, ns, S(stream)));
-    if (dw) N2F_TRY(reduce_partials(pw, dw, ns, (int64_t)cout * 9 * cin, S(stream)));
-    if (db) N2F_TRY(reduce_partials(pb, db, ns, cout, S(stream)));
-    const bool tcimpl = impl == kImplTc || impl == kImplTcF16, f16 = impl == kImplTcF16;
-    if (dw && tcimpl && tc_supported(cin, cout)) {  // dW on the tensor cores
-      const int nst = wgrad_tc_nsplit(cin, cout, h, wd);
-      float* ptc;
-      N2F_TRY(s.get(&ptc, (size_t)nst * cout * 9 * cin));
-      TcOperand ox, og;
-      N2F_TRY(make_operand(s, x, P * cin, f16, kExpAct, &ox, S(stream)));
-      N2F_TRY(make_operand(s, g, P * cout, f16, kExpAct, &og, S(stream)));
-      WgradTcPlan pl;
-      N2F_TRY(wgrad_tc_plan(&pl, ox, og, h, wd, cin, cout, nst, f16));
-      N2F_TRY(wgrad_tc_launch(pl, ptc, S(stream)));
-      N2F_TRY(reduce_partials(ptc, dw, nst, (int64_t)cout * 9 * cin, S(stream)));
-    }
+    N2F_TRY(wgrad_first_simt(g, x, pw, pb, h, wd, cout, ns, S(stream)));
+    N2F_TRY(reduce_partials(pw, dw, ns, (int64_t)cout * 9, S(stream)));
+  } else if (dw) {
+    const int nst = wgrad_tc_nsplit(cin, cout, h, wd);
+    float* ptc;
+    N2F_TRY(s.get(&ptc, (size_t)nst * cout * 9 * cin));
+    TcOperand ox, og;
+    N2F_TRY(make_operand(s, x, P * cin, kExpAct, &ox, S(stream)));
+    N2F_TRY(make_operand(s, g, P * cout, kExpAct, &og, S(stream)));
+    WgradTcPlan pl;
+    N2F_TRY(wgrad_tc_plan(&pl, ox, og, h, wd, cin, cout, nst));
+    N2F_TRY(wgrad_tc_launch(pl, ptc, S(stream)));
+    N2F_TRY(reduce_partials(ptc, dw, nst, (int64_t)cout * 9 * cin, S(stream)));
   }
   if (dx) {
-    if (cout % 8 || cin % 32) return fail(N2F_ERR_UNSUPPORTED, "dgrad: cin %d cout %d", cin, cout);
     float* wt;
     N2F_TRY(s.get(&wt, (size_t)cout * 9 * cin));
     N2F_TRY(transpose_dgrad_weights(w, wt, cin, cout, S(stream)));
-    if ((impl == kImplTc || impl == kImplTcF16) && tc_supported(cout, cin)) {
-      const bool f16 = impl == kImplTcF16;
-      TcOperand og, owt, omask;
-      N2F_TRY(make_operand(s, g, P * cout, f16, kExpAct, &og, S(stream)));
-      N2F_TRY(make_operand(s, wt, (int64_t)cout * 9 * cin, f16, kExpW, &owt, S(stream)));
-      const void* mk = mask;
-      if (mask && f16) {  // the FP16 epilogue tests the sign of the fp16 hi tensor
-        N2F_TRY(make_operand(s, mask, P * cin, true, kExpAct, &omask, S(stream)));
-        mk = omask.hi;
-      }
-      ConvTcPlan pl;
-      N2F_TRY(conv_tc_plan(&pl, og, owt, h, wd, cout, cin, f16));
-      N2F_TRY(conv_tc_plan_out(&pl, dx, nullptr, nullptr, 1.f));
-      N2F_TRY(conv_tc_launch(pl, nullptr, mk, nullptr, mask ? kEpiMask : kEpiNone, S(stream)));
-    } else {
-      N2F_TRY(conv3x3_simt(g, wt, nullptr, mask, dx, h, wd, cout, cin, mask ? kEpiMask : kEpiNone,
-                           S(stream)));
+    TcOperand og, owt, omask;
+    N2F_TRY(make_operand(s, g, P * cout, kExpAct, &og, S(stream)));
+    N2F_TRY(make_operand(s, wt, (int64_t)cout * 9 * cin, kExpW, &owt, S(stream)));
+    const void* mk = nullptr;
+    if (mask) {  // the epilogue tests the sign of the fp16 hi tensor of the layer input
+      N2F_TRY(make_operand(s, mask, P * cin, kExpAct, &omask, S(stream)));
+      mk = omask.hi;
     }
+    ConvTcPlan pl;
+    N2F_TRY(conv_tc_plan(&pl, og, owt, h, wd, cout, cin));
+    N2F_TRY(conv_tc_plan_out(&pl, dx, nullptr, nullptr, 1.f));
+    N2F_TRY(conv_tc_launch(pl, nullptr, mk, nullptr, mask ? kEpiMask : kEpiNone, S(stream)));
   }
   N2F_CUDA(cudaStreamSynchronize(S(stream)));
   return N2F_OK;
@@ -331,7 +322,7 @@ int n2f_stop_replay(const double* scores, int n, int patience, int* stop_epoch) 
   *stop_epoch = -1;
   for (int e = 0; e < n; ++e) {
     // max_epochs beyond the sequence so only the patience rule can stop it
-    N2F_TRY(launch_stop(st, se + e, 1, 1.0, loss, 1, pt, vh, lh, th, patience, n + 1, 0, 0, 0));
+    N2F_TRY(launch_stop(st, se + e, 1, 1.0, loss, 1, pt, vh, lh, th, patience, n + 1, nullptr, nullptr, 0, 0, 0));
     DevState h;
     N2F_CUDA(cudaMemcpy(&h, st, sizeof h, cudaMemcpyDeviceToHost));
     if (h.stopped) {

@@ -1,26 +1,21 @@
 // tcgen05 (5th-gen tensor core) kernels for the 3x3 convolutions in split
-// precision.  Every operand x is held as a pair hi + lo and a product as
-// A.B ~= Ah.Bh + Ah.Bl + Al.Bh (3 MMAs), in one of two precisions:
-//
-//   TF32 (F16 = false, kind::tf32): the tensor core truncates fp32 operands
-//     to tf32, so the raw fp32 tensor IS hi and only lo = round_tf32(x - hi)
-//     is stored beside it (fp32).  ~22 significant bits per operand.
-//   FP16 (F16 = true,  kind::f16): hi = fp16(x * 2^e), lo = fp16(x * 2^e - hi)
-//     with a per-tensor power-of-two scale e (activations/weights 2^8,
-//     gradients 2^(ceil(log2 P) + 8)) keeping both parts in fp16's normal
-//     range; ~22 significant bits, 2x the MMA rate and half the bytes of TF32.
-//     The epilogue removes 2^-(eA + eB) exactly.
+// precision ("FP16x3").  Every operand x is held as an fp16 pair of the scaled
+// value, hi = fp16(x * 2^e), lo = fp16(x * 2^e - hi), with a per-tensor
+// power-of-two scale e (activations/weights 2^8, gradients 2^(ceil(log2 P) +
+// 8)) keeping both parts in fp16's normal range (~22 significant bits), and a
+// product as A.B ~= Ah.Bh + Ah.Bl + Al.Bh (3 kind::f16 MMAs).  The epilogue
+// removes 2^-(eA + eB) exactly.  Every epilogue that writes an operand pair
+// also folds max |x * 2^e| into the range-guard slot of its (tensor class,
+// layer) (tc::range_note), which the stop kernel checks once per epoch.
 //
 // Accumulation: the tensor core's fp32 accumulation truncates (measured bias
 // -4.9e-6 relative at K = 2304 when one TMEM accumulator takes the whole K
 // loop, tests/test_gpu_kernels.py::test_conv_accuracy_vs_f64), and that
 // systematic shrink compounds through the 7-layer dgrad chain.  The K loop is
-// cut into groups (K = 32 for TF32, 64 for FP16); each group accumulates into
-// a fresh TMEM buffer (ping-pong, 2 x BN columns), the small cross-term MMAs
-// of a group are issued before its hi*hi MMAs (so only 4 truncating adds act
-// on a large accumulator value), and the accumulate warps add the group
-// results into fp32 registers with round-to-nearest while the tensor core
-// runs the next group.
+// cut into groups; each group accumulates into a fresh TMEM buffer, the
+// small cross-term MMAs of a group are issued before its hi*hi MMAs, and the
+// accumulate warps add the group results into fp32 registers with
+// round-to-nearest while the tensor core runs the next group.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 #include <stdlib.h>
@@ -30,23 +25,11 @@
 #include "tc_common.cuh"
 #include "train.cuh"
 
-// Build with -DN2F_TC_TRACE=1 for per-warp cycle accounting (N2F_TC_DEBUG=64).
-// -DN2F_DY256_EC32=0: 16-channel staging for N = 256 (3 dy stages instead of 2)
-#ifndef N2F_DY256_EC32
-#define N2F_DY256_EC32 1
-#endif
-// dy kernels with N <= N2F_DY_2SM_MAXN run two CTAs per SM (0 disables)
-#ifndef N2F_DY_2SM_MAXN
-#define N2F_DY_2SM_MAXN 32
-#endif
-// -DN2F_DY_KC16=1: 16-channel K chunks for N = 256 (experiment)
-#ifndef N2F_DY_KC16
-#define N2F_DY_KC16 0
-#endif
-// stages (32 pixels each) per accumulation group of the FP16 pair wgrad
-#ifndef N2F_WG_GROUP_PAIR
-#define N2F_WG_GROUP_PAIR 4
-#endif
+// Build with -DN2F_TC_TRACE=1 for per-warp cycle accounting (profiling builds only).
+// dy kernels with N <= kDy2SmMaxN run two CTAs per SM
+constexpr int kDy2SmMaxN = 32;
+// stages (32 pixels each) per accumulation group of the wgrad CTA pairs
+constexpr int kWgGroupPair = 4;
 #ifndef N2F_TC_TRACE
 #define N2F_TC_TRACE 0
 #endif
@@ -63,40 +46,23 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
-// Precision traits.  A pipeline stage carries K = 32 elements per operand row
-// (128 B tf32 / 64 B fp16).  One MMA consumes 32 bytes of K (8 tf32 / 16 fp16),
-// so a K-major operand advances 32 B per MMA and an MN-major one 1 KB (8 rows
-// of 128 B / 16 rows of 64 B).
-template <bool F16>
+// Operand traits (fp16 parts).  A pipeline stage row carries 32 elements
+// (64 B); one MMA consumes 32 bytes of K (16 fp16), so a K-major operand
+// advances 32 B per MMA and an MN-major one 1 KB (16 rows of 64 B).
 struct Prec {
-  static constexpr int kES = F16 ? 2 : 4;           // bytes per element
-  static constexpr int kRow = 32 * kES;             // bytes per 32-element row
-  static constexpr int kKSteps = F16 ? 2 : 4;       // MMAs per 32-element stage row
-  static constexpr uint32_t kLayK = F16 ? 4 : 2;    // SWIZZLE_64B / SWIZZLE_128B (K-major)
-  static constexpr uint32_t kSboK = 8 * kRow;       // 8-row swizzle atom stride
-  static constexpr uint32_t kLayMN = F16 ? 4 : 1;   // SWIZZLE_64B / SWIZZLE_128B_BASE32B (MN-major)
-  static constexpr int kGroup = F16 ? 2 : 1;        // stages per TMEM accumulation group
-  __device__ static uint64_t kdesc(uint32_t addr) { return sw128_desc(addr, 16, kSboK, kLayK); }
+  static constexpr int kES = 2;                  // bytes per element
+  static constexpr int kRow = 32 * kES;          // bytes per 32-element row
+  static constexpr uint32_t kLayMN = 4;          // SWIZZLE_64B (MN-major)
   // MN-major blocks of 32 channels x 32 pixel rows: LBO = block stride
-  __device__ static uint64_t mndesc(uint32_t addr) {
-    return sw128_desc(addr, 32 * kRow, 512, kLayMN);
-  }
   template <int CS = 1>
   __device__ static void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    if (CS == 2) {
-      if (F16)
-        mma_f16_2sm(d, a, b, idesc, acc);
-      else
-        mma_tf32_2sm(d, a, b, idesc, acc);
-    } else {
-      if (F16)
-        mma_f16(d, a, b, idesc, acc);
-      else
-        mma_tf32(d, a, b, idesc, acc);
-    }
+    if (CS == 2)
+      mma_f16_2sm(d, a, b, idesc, acc);
+    else
+      mma_f16(d, a, b, idesc, acc);
   }
   static constexpr uint32_t idesc(int M, int N, bool amn, bool bmn) {
-    return F16 ? idesc_f16(M, N, amn, bmn) : idesc_tf32(M, N, amn, bmn);
+    return idesc_f16(M, N, amn, bmn);
   }
 };
 
@@ -165,97 +131,21 @@ __device__ __forceinline__ void tmem_load_all(uint32_t taddr, float (&acc)[HALF]
   }
 }
 
-// ---------------------------------------------------------------------------
-// 3x3 conv forward / dgrad as a persistent, TMA-fed tcgen05 implicit GEMM.
-//   M = 128 pixels (a 32 x 4 spatial tile), N = all output channels (BN),
-//   K = 9 taps x C in stages of 32 channels.
-// Per stage, TMA loads the tap-shifted input tile (out-of-bounds coordinates
-// zero-fill = the reference's zero padding, tensor.py:231-238) and its lo
-// part, plus the weight slice and its lo part.  Warp roles (320 threads):
-// w0.lane0 TMA producer; w1.lane0 MMA issuer (w1 owns TMEM); w2..w9
-// accumulate + epilogue: warp w reads TMEM lane quarter (w % 4) and column
-// half (w - 2) / 4.  Epilogue: scale removal, fused bias+ReLU (forward) or
-// ReLU-mask of the layer input (dgrad), optional per-tile column sums (the
-// bias gradient of the produced tensor), fp32 output and/or the operand pair
-// for the next tensor-core consumer.
-// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the producer
-// streams stages across tile boundaries and the epilogue of tile t overlaps
-// the first groups of tile t+1.
-// ---------------------------------------------------------------------------
-constexpr int kTW = 32, kTH = 4;
+// Warp roles of every tcgen05 kernel here (320 threads): warp 0 TMA
+// producer, warp 1 MMA issuer (owns TMEM; whole warps walk the schedule and
+// wait on mbarriers, elect.sync picks the issuing lane), warps 2..9
+// accumulate + epilogue (warp w reads TMEM lane quarter w % 4 and column half
+// (w - 2) / 4).
 constexpr int kThreadsTc = 320;
 
-template <int BN, bool F16, int CS = 1>
-struct FwdCfg {
-  using P = Prec<F16>;
-  static constexpr int kStageA = 128 * P::kRow;
-  static constexpr int kStageB = (BN / CS) * P::kRow;  // this CTA's share of the weight rows
-  static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
-  // epilogue staging (TMA-store source), per accumulate warp 32 pixels x kEpiCols
-  // channels: FP16 the fp32 output OR the fp16 (hi, lo) pair (never both);
-  // TF32 the fp32 output AND its tf32 residual
-  // (wide layers; the narrow ones keep direct transposed stores through a
-  // 32 x kEpiCols fp32 scratch: at 2 CTAs per SM their smem has no room for
-  // double-buffered staging and single-buffered TMA stores measured slower)
-  static constexpr bool kTmaEpi = BN >= 128;
-  static constexpr int kEpiCols = BN >= 128 ? 16 : 8;
-  static constexpr int kEpiWarpBytes = 32 * kEpiCols * ((F16 || !kTmaEpi) ? 4 : 8);
-  static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
-  static constexpr int kMaxStages = (220 * 1024 - kEpiBytes - 1024) / kStageBytes;
-  // narrow layers run 2 CTAs per SM (their smem, registers and TMEM allow it)
-  // with 2 groups' worth of stages; the others take as many stages as fit
-  static constexpr bool kTwoPerSm = CS == 1 && BN <= 64;
-  static constexpr int kStages = kTwoPerSm ? 2 * P::kGroup : (kMaxStages > 8 ? 8 : kMaxStages);
-  // stages per TMEM accumulation group (K = 64 FP16, 32 TF32; measured: a
-  // 3-stage FP16 group for BN 256 was slower and doubled the truncation bias)
-  static constexpr int kGroup = P::kGroup;
-  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
-  // TMEM group buffers: as many as the CTA's column budget holds (<= 4)
-  static constexpr int kTmemBudget = kTwoPerSm ? 256 : 512;
-  static constexpr int kBufs = kTmemBudget / BN > 4 ? 4 : kTmemBudget / BN;
-  static constexpr int kTmemCols = kBufs * BN < 32 ? 32 : kBufs * BN;
-  static constexpr int kHalf = BN / 2;  // columns per epilogue warp
-};
-
-// Raw output pointers for the direct-store epilogue.  y: fp32 values (may be
-// null).  F16: yhi/ylo fp16 pair of y * oscale.  TF32: ylo fp32 residual.
+// Raw output pointers of a conv plan.  y: fp32 values (may be null);
+// yhi/ylo: fp16 pair of y * oscale.
 struct ConvOut {
   float* y;
   void* yhi;
   void* ylo;
   float oscale;
 };
-
-template <bool F16>
-__device__ __forceinline__ void store_pair4(const ConvOut& o, int64_t idx, float4 v) {
-  if (F16) {
-    const float s = o.oscale;
-    const float a[4] = {v.x * s, v.y * s, v.z * s, v.w * s};
-    __half h[4], l[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      h[i] = __float2half_rn(a[i]);
-      l[i] = __float2half_rn(__fsub_rn(a[i], __half2float(h[i])));
-    }
-    auto pack = [](__half a, __half b) {
-      return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
-    };
-    if (o.yhi)
-      *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(o.yhi) + idx) =
-          make_uint2(pack(h[0], h[1]), pack(h[2], h[3]));
-    if (o.ylo)
-      *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(o.ylo) + idx) =
-          make_uint2(pack(l[0], l[1]), pack(l[2], l[3]));
-  } else if (o.ylo) {
-    float4 r;
-    float h;
-    split_tf32(v.x, h, r.x);
-    split_tf32(v.y, h, r.y);
-    split_tf32(v.z, h, r.z);
-    split_tf32(v.w, h, r.w);
-    *reinterpret_cast<float4*>(reinterpret_cast<float*>(o.ylo) + idx) = r;
-  }
-}
 
 // Programmatic dependent launch: let the next kernel of the stream launch (its
 // prologue overlaps this kernel's tail), and wait for the previous one's
@@ -278,479 +168,13 @@ __device__ __forceinline__ int swz_chunk(int row, int k) {
 // Epilogue output selection (bit mask of ConvTcPlan output maps).
 enum { kOutY = 1, kOutHi = 2, kOutLo = 4 };
 
-template <bool F16>
+// Four fp16 values of a stored activation (the ReLU mask of a dgrad).
 __device__ __forceinline__ float4 load_mask4(const void* mask, int64_t idx) {
-  if (F16) {
-    const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(mask) + idx));
-    return make_float4(__half2float(__ushort_as_half((unsigned short)(u.x & 0xFFFFu))),
-                       __half2float(__ushort_as_half((unsigned short)(u.x >> 16))),
-                       __half2float(__ushort_as_half((unsigned short)(u.y & 0xFFFFu))),
-                       __half2float(__ushort_as_half((unsigned short)(u.y >> 16))));
-  }
-  return __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(mask) + idx));
-}
-
-template <int BN, bool F16, int CS>
-__global__ void __launch_bounds__(kThreadsTc, 1)
-    k_conv3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
-                 const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
-                 const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
-                 const __grid_constant__ CUtensorMap myl, int omask, float oscale, ConvOut out,
-                 const float* __restrict__ bias, const void* __restrict__ mask, int mask_bits,
-                 uint32_t* __restrict__ mbits_out, float* __restrict__ colsum, float unscale, int H,
-                 int W, int C, int epi, int dbg) {
-  using Cfg = FwdCfg<BN, F16, CS>;
-  using P = Prec<F16>;
-  constexpr int S = Cfg::kStages;
-  constexpr int HALF = Cfg::kHalf;
-  constexpr int G = Cfg::kGroup;
-  constexpr int NB = Cfg::kBufs;
-  constexpr int UH = kTH * CS;  // rows of a cluster tile (CTA r owns rows [kTH r, kTH r + kTH))
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ uint64_t full[S], empty[S], tfull[NB], tempty[NB];
-  __shared__ uint32_t tslot;
-  __shared__ __align__(16) float csum[4][BN];
-  uint8_t* base = align1024(smem_raw);
-  pdl_trigger();
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t rank = CS > 1 ? cluster_ctarank() : 0;
-  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
-  const int tiles_x = (W + kTW - 1) / kTW;
-  const int nunits = tiles_x * ((H + UH - 1) / UH);
-  const int cpt = C / 32, KB = 9 * cpt;  // stages per tile
-  const int NG = (KB + G - 1) / G;       // groups per tile (the last may be short)
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < NB; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8 * CS);  // one arrive per accumulate warp of the cluster
-    }
-    fence_barrier_init();
-    tma_prefetch(&mx);
-    tma_prefetch(&mxl);
-    tma_prefetch(&mw);
-    tma_prefetch(&mwl);
-    if (omask & kOutY) tma_prefetch(&my);
-    if (omask & kOutHi) tma_prefetch(&myh);
-    if (omask & kOutLo) tma_prefetch(&myl);
-  }
-  if (warp == 1) {
-    if (CS == 2)
-      tmem_alloc_2sm<Cfg::kTmemCols>(&tslot);
-    else
-      tmem_alloc<Cfg::kTmemCols>(&tslot);
-  }
-  tc_fence_before();
-  if (CS == 2)
-    cluster_sync();
-  else
-    __syncthreads();
-  tc_fence_after();
-  const uint32_t taddr = tslot;
-  pdl_wait();  // everything above overlaps the previous kernel's tail (PDL)
-
-  if (warp == 0) {
-    // ---- TMA producer (stage index `it` runs across tiles).  The whole warp
-    // walks the schedule; one elected lane issues.  In a CTA pair both CTAs
-    // load their own pixel rows and their half of the weight rows, and the
-    // bytes complete on the leader's full barrier.
-    const uint32_t full0 = CS == 2 ? mapa_shared(smem_u32(&full[0]), 0) : smem_u32(&full[0]);
-    int it = 0;
-    for (int ut = cid; ut < nunits; ut += ncl) {
-      const int x0 = (ut % tiles_x) * kTW, y0 = (ut / tiles_x) * UH + kTH * (int)rank;
-      for (int kb = 0; kb < KB; ++kb, ++it) {
-        const int s = it % S, round = it / S;
-        if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-        const int tap = kb / cpt, c0 = (kb - tap * cpt) * 32;
-        const int ky = tap / 3, kx = tap - 3 * ky;
-        uint8_t* st = base + s * Cfg::kStageBytes;
-        if (elect_one_sync()) {
-          if (dbg & 4) {  // profiling experiment: no operand traffic
-            if (rank == 0) mbar_arrive(&full[s]);
-          } else if (CS == 1) {
-            mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
-            tma_load_3d(st, &mx, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
-            tma_load_3d(st + Cfg::kStageA, &mxl, &full[s], c0, x0 + kx - 1, y0 + ky - 1);
-            tma_load_2d(st + 2 * Cfg::kStageA, &mw, &full[s], tap * C + c0, 0);
-            tma_load_2d(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, &full[s], tap * C + c0, 0);
-          } else {
-            const uint32_t fb = full0 + 8u * s;
-            const int n0 = (int)rank * (BN / CS);
-            if (rank == 0) mbar_arrive_expect_tx(&full[s], CS * Cfg::kStageBytes);
-            tma_load_3d_2sm(st, &mx, fb, c0, x0 + kx - 1, y0 + ky - 1);
-            tma_load_3d_2sm(st + Cfg::kStageA, &mxl, fb, c0, x0 + kx - 1, y0 + ky - 1);
-            tma_load_2d_2sm(st + 2 * Cfg::kStageA, &mw, fb, tap * C + c0, n0);
-            tma_load_2d_2sm(st + 2 * Cfg::kStageA + Cfg::kStageB, &mwl, fb, tap * C + c0, n0);
-          }
-        }
-        __syncwarp();
-      }
-    }
-  } else if (warp == 1) {
-    // ---- MMA issuer (the leader CTA of a pair issues for both): one group =
-    // G stages into a fresh TMEM buffer.  The whole warp walks the schedule
-    // and waits; one elected lane issues.
-    if (rank == 0) {
-      constexpr uint32_t idesc = P::idesc(128 * CS, BN, false, false);
-      // descriptor offsets (16-byte units) inside a stage: A-lo, B-hi, B-lo
-      constexpr uint32_t kAl = Cfg::kStageA >> 4, kBh = (2 * Cfg::kStageA) >> 4,
-                         kBl = (2 * Cfg::kStageA + Cfg::kStageB) >> 4;
-      const uint64_t desc0 = P::kdesc(smem_u32(base));
-      int it = 0, gg = 0;  // stage and group counters across tiles
-      long long tw_e = 0, tw_f = 0, t_is = 0, t_0 = clock64();  // dbg 64: cycle accounting
-      for (int ut = cid; ut < nunits; ut += ncl) {
-        for (int g = 0; g < NG; ++g, ++gg) {
-          const int b = gg % NB;
-          const long long c0 = clock64();
-          if (gg >= NB && !(dbg & 16)) mbar_wait(&tempty[b], ((gg / NB) - 1) & 1);
-          const long long c1 = clock64();
-          const int ng = (g + 1) * G <= KB ? G : KB - g * G;
-          for (int j = 0; j < ng; ++j) mbar_wait(&full[(it + j) % S], ((it + j) / S) & 1);
-          const long long c2 = clock64();
-          tw_e += c1 - c0;
-          tw_f += c2 - c1;
-          tc_fence_after();
-          if (elect_one_sync()) {
-            const uint32_t d = taddr + b * BN;
-            uint64_t ah[G];  // A-hi descriptor of the group's stages
-#pragma unroll
-            for (int j = 0; j < G; ++j)
-              ah[j] = desc0 + (uint64_t)(((it + j) % S) * (Cfg::kStageBytes >> 4));
-            if (!(dbg & 2)) {
-              // the small cross terms of the whole group first, then hi*hi;
-              // one K step = 32 bytes = 2 descriptor units
-#pragma unroll
-              for (int j = 0; j < G; ++j) {
-                if (j < ng) {
-#pragma unroll
-                  for (int k = 0; k < P::kKSteps; ++k) {
-                    const uint64_t a = ah[j] + 2 * k;
-                    P::template mma<CS>(d, a, a + kBl, idesc, (j | k) != 0);
-                    P::template mma<CS>(d, a + kAl, a + kBh, idesc, 1);
-                  }
-                }
-              }
-#pragma unroll
-              for (int j = 0; j < G; ++j) {
-                if (j < ng) {
-#pragma unroll
-                  for (int k = 0; k < P::kKSteps; ++k) {
-                    const uint64_t a = ah[j] + 2 * k;
-                    P::template mma<CS>(d, a, a + kBh, idesc, 1);
-                  }
-                }
-              }
-            }
-            for (int j = 0; j < ng; ++j) {
-              if (CS == 2)
-                mma_commit_2sm(&empty[(it + j) % S]);
-              else
-                mma_commit(&empty[(it + j) % S]);
-            }
-            if (CS == 2)
-              mma_commit_2sm(&tfull[b]);
-            else
-              mma_commit(&tfull[b]);
-          }
-          __syncwarp();
-          t_is += clock64() - c2;
-          it += ng;
-        }
-      }
-      if ((dbg & 64) && lane == 0 && (blockIdx.x == 0 || blockIdx.x == 100))
-        printf("[mma cta %d] C %d BN %d CS %d HxW %dx%d groups %d total %lld wait_tempty %lld "
-               "wait_full %lld issue %lld\n",
-               blockIdx.x, C, BN, CS, H, W, gg, clock64() - t_0, tw_e, tw_f, t_is);
-    }
-  } else {
-    // ---- group accumulation in registers (round-to-nearest fp32 adds)
-    const int q = warp & 3;            // TMEM lane quarter
-    const int half = (warp - 2) >> 2;  // column half
-    const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * HALF;
-    // the leader's tempty barriers (shared::cluster addresses)
-    const uint32_t tempty0 = CS == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : smem_u32(&tempty[0]);
-    int gg = 0;
-#if N2F_TC_TRACE
-    long long tw = 0, td = 0, te = 0, t_0 = clock64();  // cycle accounting
-#endif
-    for (int ut = cid; ut < nunits; ut += ncl) {
-      const int x0 = (ut % tiles_x) * kTW, y0 = (ut / tiles_x) * UH + kTH * (int)rank;
-      const int tile = ut * CS + (int)rank;  // this CTA's 128-pixel tile (colsum row)
-      float acc[HALF];
-#pragma unroll
-      for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
-      for (int g = 0; g < NG; ++g, ++gg) {
-        const int b = gg % NB;
-        if (dbg & 16) continue;  // profiling experiment: no accumulator handoff
-#if N2F_TC_TRACE
-        const long long c0 = clock64();
-#endif
-        mbar_wait(&tfull[b], (gg / NB) & 1);
-#if N2F_TC_TRACE
-        const long long c1 = clock64();
-        tw += c1 - c0;
-#endif
-        tc_fence_after();
-        if (!(dbg & 1)) drain_add<HALF>(lane_base + b * BN, acc);  // dbg 1: experiment, no drain
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (CS == 2)
-            mbar_arrive_cluster(tempty0 + 8u * b);
-          else
-            mbar_arrive(&tempty[b]);
-        }
-#if N2F_TC_TRACE
-        td += clock64() - c1;
-#endif
-      }
-#if N2F_TC_TRACE
-      const long long ce = clock64();
-#endif
-
-      if constexpr (Cfg::kTmaEpi) {
-      // ---- epilogue: lane = pixel (row q of the tile, column x0 + lane),
-      // registers = channels.  Per EC-channel slice: scale removal, bias+ReLU
-      // or the ReLU mask, column sums, then the outputs are staged in smem in
-      // the TMA swizzle layout and written by TMA tensor stores (out-of-image
-      // pixels are clipped by the TMA unit), so the warp never waits on
-      // global stores.
-      constexpr int EC = Cfg::kEpiCols, CH = EC / 4;
-      constexpr int RBY = EC * 4;              // fp32 staging row bytes
-      constexpr int RBH = EC * (F16 ? 2 : 4);  // pair staging row bytes (fp16 / tf32 residual)
-      uint8_t* stg = base + S * Cfg::kStageBytes + (warp - 2) * Cfg::kEpiWarpBytes;
-      uint8_t* stg_h = stg;                                    // F16: hi (union with y)
-      uint8_t* stg_l = F16 ? stg + 32 * EC * 2 : stg + 32 * RBY;  // lo / tf32 residual
-      const int py = y0 + q, px = x0 + lane;
-      const bool valid = py < H && px < W;
-      const int n0 = half * HALF;
-      // ReLU masks as bits: [pixel][BN / 32] words, bit = channel > 0 (the
-      // forward writes them, the dgrad of the next layer reads them: 1/16 of
-      // the fp16 mask bytes, one load per thread per tile)
-      constexpr int WPP = BN / 32, MW = HALF / 32 > 0 ? HALF / 32 : 1;
-      const int64_t pix = (int64_t)py * W + px;
-      uint32_t mw[MW];
-      if (epi == kEpiMask && mask_bits) {
-#pragma unroll
-        for (int k = 0; k < MW; ++k)
-          mw[k] = valid ? __ldg(reinterpret_cast<const uint32_t*>(mask) + pix * WPP + n0 / 32 + k) : 0u;
-      }
-      uint32_t ob = 0;
-#pragma unroll
-      for (int c0 = 0; c0 < HALF; c0 += EC) {
-        const int n = n0 + c0;
-        float v[EC];
-#pragma unroll
-        for (int i = 0; i < EC; ++i) v[i] = acc[c0 + i] * unscale;
-        if (epi == kEpiBiasRelu || epi == kEpiBias) {
-#pragma unroll
-          for (int k = 0; k < CH; ++k) {
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(bias + n) + k);
-            v[4 * k] += bb.x; v[4 * k + 1] += bb.y; v[4 * k + 2] += bb.z; v[4 * k + 3] += bb.w;
-          }
-          if (epi == kEpiBiasRelu) {
-#pragma unroll
-            for (int i = 0; i < EC; ++i) v[i] = fmaxf(v[i], 0.f);
-          }
-        } else if (epi == kEpiMask && mask_bits) {
-          const uint32_t bits = mw[c0 / 32] >> (c0 % 32);
-#pragma unroll
-          for (int i = 0; i < EC; ++i) v[i] = ((bits >> i) & 1u) ? v[i] : 0.f;
-        } else if (epi == kEpiMask) {
-          const int64_t idx = pix * BN + n;
-#pragma unroll
-          for (int k = 0; k < CH; ++k) {
-            float4 mk = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid) mk = load_mask4<F16>(mask, idx + 4 * k);
-            v[4 * k] = mk.x > 0.f ? v[4 * k] : 0.f;
-            v[4 * k + 1] = mk.y > 0.f ? v[4 * k + 1] : 0.f;
-            v[4 * k + 2] = mk.z > 0.f ? v[4 * k + 2] : 0.f;
-            v[4 * k + 3] = mk.w > 0.f ? v[4 * k + 3] : 0.f;
-          }
-        }
-        if (mbits_out) {  // this layer's ReLU mask for the next layer's dgrad
-          uint32_t sb = 0;
-#pragma unroll
-          for (int i = 0; i < EC; ++i) sb |= (v[i] > 0.f ? 1u : 0u) << i;
-          ob |= sb << (c0 % 32);
-          if ((c0 + EC) % 32 == 0) {
-            if (valid) mbits_out[pix * WPP + n / 32] = ob;
-            ob = 0;
-          }
-        }
-        if (colsum) {  // deterministic per-tile column sums (bias gradient of this tensor)
-          // transpose-reduce: each level halves the channels a lane carries
-          float r[EC];
-#pragma unroll
-          for (int i = 0; i < EC; ++i) r[i] = valid ? v[i] : 0.f;
-          int ch = 0;
-#pragma unroll
-          for (int o = 16, cnt = EC; o >= 1; o >>= 1) {
-            if (cnt > 1) {
-              const int hcnt = cnt / 2;
-              const bool up = (lane & o) != 0;
-#pragma unroll
-              for (int i = 0; i < EC / 2; ++i) {
-                if (i < hcnt) {
-                  const float send = up ? r[i] : r[i + hcnt];
-                  const float keep = up ? r[i + hcnt] : r[i];
-                  r[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                }
-              }
-              ch += up ? hcnt : 0;
-              cnt = hcnt;
-            } else {
-              r[0] += __shfl_xor_sync(0xffffffffu, r[0], o);
-            }
-          }
-          if ((lane & (32 / EC - 1)) == 0) csum[q][n + ch] = r[0];
-        }
-        // the previous slice's TMA stores must have finished reading the staging
-        if (lane == 0) bulk_wait_read0();
-        __syncwarp();
-        if (omask & kOutY) {
-#pragma unroll
-          for (int k = 0; k < CH; ++k)
-            *reinterpret_cast<float4*>(stg + lane * RBY + 16 * swz_chunk<RBY>(lane, k)) =
-                make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-        }
-        if (F16 && (omask & (kOutHi | kOutLo))) {
-          uint32_t hw[EC / 2], lw[EC / 2];
-#pragma unroll
-          for (int i = 0; i < EC; i += 2) {
-            __half h0, l0, h1, l1;
-            split_f16(v[i] * oscale, h0, l0);
-            split_f16(v[i + 1] * oscale, h1, l1);
-            hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-            lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-          }
-#pragma unroll
-          for (int k = 0; k < EC / 8; ++k) {
-            const int off = lane * RBH + 16 * swz_chunk<RBH>(lane, k);
-            *reinterpret_cast<uint4*>(stg_h + off) =
-                make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
-            *reinterpret_cast<uint4*>(stg_l + off) =
-                make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
-          }
-        }
-        if (!F16 && (omask & kOutLo)) {  // tf32 residual of the fp32 output
-#pragma unroll
-          for (int k = 0; k < CH; ++k) {
-            float4 r4;
-            float hh;
-            split_tf32(v[4 * k], hh, r4.x);
-            split_tf32(v[4 * k + 1], hh, r4.y);
-            split_tf32(v[4 * k + 2], hh, r4.z);
-            split_tf32(v[4 * k + 3], hh, r4.w);
-            *reinterpret_cast<float4*>(stg_l + lane * RBH + 16 * swz_chunk<RBH>(lane, k)) = r4;
-          }
-        }
-        fence_proxy_async();  // generic-proxy staging writes -> TMA (async proxy)
-        __syncwarp();
-        if (lane == 0) {
-          if (omask & kOutY) tma_store_3d(&my, stg, n, x0, py);
-          if (F16 && (omask & kOutHi)) tma_store_3d(&myh, stg_h, n, x0, py);
-          if (omask & kOutLo) tma_store_3d(&myl, stg_l, n, x0, py);
-          bulk_commit_group();
-        }
-      }
-      } else {
-      // ---- epilogue.  The drain leaves lane = pixel, registers = channels;
-      // global rows are pixel-major, so EC-column slices are transposed
-      // through a per-warp smem scratch (16-byte chunks XOR-swizzled:
-      // conflict-free both ways) and re-read as (pixel, 4-channel chunk)
-      // pairs: CPR lanes cover EC contiguous channels of one pixel.
-      constexpr int EC = Cfg::kEpiCols, CPR = EC / 4, RPL = 32 / EC;  // rows per 128 B bank line
-      float* scr = reinterpret_cast<float*>(base + S * Cfg::kStageBytes + (warp - 2) * Cfg::kEpiWarpBytes);
-      const int n0 = half * HALF;
-      const int kk = lane % CPR;  // this lane's 4-channel chunk after the transpose
-#pragma unroll
-      for (int c0 = 0; c0 < HALF; c0 += EC) {
-#pragma unroll
-        for (int k = 0; k < CPR; ++k) {
-          const int pos = k ^ ((lane / RPL) % CPR);
-          *reinterpret_cast<float4*>(scr + lane * EC + pos * 4) =
-              make_float4(acc[c0 + 4 * k] * unscale, acc[c0 + 4 * k + 1] * unscale,
-                          acc[c0 + 4 * k + 2] * unscale, acc[c0 + 4 * k + 3] * unscale);
-        }
-        __syncwarp();
-        const int n = n0 + c0 + 4 * kk;  // first channel of this lane's chunk
-        float4 bb = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (epi == kEpiBiasRelu || epi == kEpiBias) bb = __ldg(reinterpret_cast<const float4*>(bias + n));
-        float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
-        for (int rr = 0; rr < CPR; ++rr) {  // 32 / CPR pixels per pass
-          const int pr = lane / CPR + rr * (32 / CPR);  // pixel row in the warp's 32
-          float4 v = *reinterpret_cast<const float4*>(scr + pr * EC + (kk ^ ((pr / RPL) % CPR)) * 4);
-          const int m = q * 32 + pr;
-          const int py = y0 + m / kTW, px = x0 + m % kTW;
-          const bool valid = py < H && px < W;
-          const int64_t idx = ((int64_t)py * W + px) * BN + n;
-          if (epi == kEpiBiasRelu || epi == kEpiBias) {
-            v.x += bb.x; v.y += bb.y; v.z += bb.z; v.w += bb.w;
-            if (epi == kEpiBiasRelu) {
-              v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
-            }
-          } else if (epi == kEpiMask) {
-            float4 mk = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid) mk = load_mask4<F16>(mask, idx);
-            v.x = mk.x > 0.f ? v.x : 0.f;
-            v.y = mk.y > 0.f ? v.y : 0.f;
-            v.z = mk.z > 0.f ? v.z : 0.f;
-            v.w = mk.w > 0.f ? v.w : 0.f;
-          }
-          if (valid) {
-            cs.x += v.x; cs.y += v.y; cs.z += v.z; cs.w += v.w;
-            if (out.y) *reinterpret_cast<float4*>(out.y + idx) = v;
-            store_pair4<F16>(out, idx, v);
-          }
-        }
-        if (colsum) {  // deterministic per-tile column sums (bias gradient of this tensor)
-#pragma unroll
-          for (int o = CPR; o < 32; o <<= 1) {
-            cs.x += __shfl_xor_sync(0xffffffffu, cs.x, o);
-            cs.y += __shfl_xor_sync(0xffffffffu, cs.y, o);
-            cs.z += __shfl_xor_sync(0xffffffffu, cs.z, o);
-            cs.w += __shfl_xor_sync(0xffffffffu, cs.w, o);
-          }
-          if (lane < CPR) *reinterpret_cast<float4*>(&csum[q][n]) = cs;
-        }
-        __syncwarp();  // scratch reused by the next slice
-      }
-      }
-      if (colsum) {  // the 8 accumulate warps only (named barrier 1)
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        for (int n = tid - 64; n < BN; n += 256)
-          colsum[(int64_t)tile * BN + n] = (csum[0][n] + csum[1][n]) + (csum[2][n] + csum[3][n]);
-        asm volatile("bar.sync 1, 256;" ::: "memory");  // csum reusable for the next tile
-      }
-#if N2F_TC_TRACE
-      te += clock64() - ce;
-#endif
-    }
-#if N2F_TC_TRACE
-    if ((dbg & 64) && lane == 0 && (warp == 2 || warp == 9) && (blockIdx.x == 0 || blockIdx.x == 100))
-      printf("[acc cta %d warp %d] C %d BN %d CS %d HxW %dx%d groups %d total %lld wait_tfull %lld "
-             "drain %lld epilogue %lld\n",
-             blockIdx.x, warp, C, BN, CS, H, W, gg, clock64() - t_0, tw, td, te);
-#endif
-    if (lane == 0) bulk_wait0();  // all output stores complete before the CTA retires
-  }
-  tc_fence_before();
-  if (CS == 2)
-    cluster_sync();  // the peer's TMEM / smem / barriers stay live until the pair is done
-  else
-    __syncthreads();
-  if (warp == 1) {
-    if (CS == 2)
-      tmem_dealloc_2sm<Cfg::kTmemCols>(taddr);
-    else
-      tmem_dealloc<Cfg::kTmemCols>(taddr);
-  }
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __half*>(mask) + idx));
+  return make_float4(__half2float(__ushort_as_half((unsigned short)(u.x & 0xFFFFu))),
+                     __half2float(__ushort_as_half((unsigned short)(u.x >> 16))),
+                     __half2float(__ushort_as_half((unsigned short)(u.y & 0xFFFFu))),
+                     __half2float(__ushort_as_half((unsigned short)(u.y >> 16))));
 }
 
 // ---------------------------------------------------------------------------
@@ -766,44 +190,33 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
 //   TMA instruction count by 3x.  A stage is one TMEM accumulation group
 //   (K = 96: 18 MMAs, 6 of them hi*hi).  Epilogue: TMA tensor stores.
 // ---------------------------------------------------------------------------
-template <int BN, bool DX3 = false>
+template <int BN>
 struct DyCfg {
-  // K chunk of a stage: 32 channels (SWIZZLE_64B rows); 16 (SWIZZLE_32B, five
-  // stages for N = 256) measured no faster.  A group spans K = 96 either way.
-  static constexpr int kKC = N2F_DY_KC16 && BN == 256 ? 16 : 32;
+  // K chunk of a stage: 32 channels (SWIZZLE_64B rows; 16-channel chunks with
+  // five stages for N = 256 measured no faster).  A stage spans K = 96.
+  static constexpr int kKC = 32;
   static constexpr int kRow = kKC * 2;                // bytes per GEMM row (fp16)
   static constexpr int kKSteps = kKC / 16;            // MMA K steps per tap and stage
-  static constexpr uint32_t kLayout = kKC == 32 ? 4 : 6;  // UMMA SWIZZLE_64B / _32B
-  static constexpr int kDxUnits = DX3 ? 0 : (8 * kRow) >> 4;  // a dx shift: 8 rows, descriptor units
-  // DX3 (narrow layers): the three dx taps are stacked into one N = 3 BN MMA
-  // on an unshifted 16 x 8 activation box (3x fewer activation-operand smem
-  // reads, which bound these narrow MMAs); the epilogue adds the taps of the
-  // neighbouring columns (lane shuffles by 8, a cross-warp exchange at the
-  // quarter edges) and a CTA tile keeps the 14 centre columns
-  static constexpr int kRowsA = (DX3 ? 16 : 18) * 8;  // halo columns x rows
+  static constexpr uint32_t kLayout = 4;              // UMMA SWIZZLE_64B
+  static constexpr int kDxUnits = (8 * kRow) >> 4;    // a dx shift: 8 rows, descriptor units
+  static constexpr int kRowsA = 18 * 8;               // halo columns x rows
   static constexpr int kStageA = kRowsA * kRow;       // one fp16 part (hi or lo)
   static constexpr int kTapB = (BN / 2) * kRow;       // this CTA's weight rows of one tap
   static constexpr int kStageB = 3 * kTapB;           // the three dx taps
   static constexpr int kStageBytes = 2 * kStageA + 2 * kStageB;
-  static constexpr int kCols = DX3 ? 3 * BN : BN;     // TMEM columns of one accumulator
-  static constexpr int kTileW = DX3 ? 14 : 16;        // output columns per CTA
-  // staging slices: 32 channels (one fence + TMA issue per 32) where smem
-  // allows, 16 for BN = 256 (whose three 66 KB dy stages fill the rest)
-  // narrow layers (N <= N2F_DY_2SM_MAXN) run two CTAs per SM: their short
+  static constexpr int kCols = BN;                    // TMEM columns of one accumulator
+  static constexpr int kTileW = 16;                   // output columns per CTA
+  // narrow layers (N <= kDy2SmMaxN) run two CTAs per SM: their short
   // launches are bound by per-tile latency (TMA round trips, epilogue), which
   // a second co-resident CTA pair hides; they take half the smem budget
-  static constexpr int kPerSm = BN <= N2F_DY_2SM_MAXN ? 2 : 1;
-  static constexpr int kEpiCols = (BN == 256 && !N2F_DY256_EC32) ? 16
-                                  : kPerSm == 2 ? (BN / 2 < 16 ? BN / 2 : 16)
-                                                : (BN / 2 < 32 ? BN / 2 : 32);
+  static constexpr int kPerSm = BN <= kDy2SmMaxN ? 2 : 1;
+  // staging slices: 32 channels (one fence + TMA issue per 32) where smem
+  // allows, 16 at two CTAs per SM
+  static constexpr int kEpiCols = kPerSm == 2 ? (BN / 2 < 16 ? BN / 2 : 16)
+                                              : (BN / 2 < 32 ? BN / 2 : 32);
   static constexpr int kEpiBuf = 32 * kEpiCols * 4;  // one staging buffer (fp32 y, or the fp16 pair)
-  static constexpr int kEpiNBuf = 1;
-  static constexpr int kEpiWarpBytes = kEpiNBuf * kEpiBuf;
-  // DX3 stores directly (its 4-column warp boxes would overlap the neighbour
-  // tiles) and instead needs the tap-exchange buffer: [tile parity][half][q]
-  // [side][8 lanes][BN / 2] floats
-  static constexpr int kXchBytes = DX3 ? 2 * 2 * 4 * 2 * 8 * (BN / 2) * 4 : 0;
-  static constexpr int kEpiBytes = DX3 ? kXchBytes : 8 * kEpiWarpBytes;
+  static constexpr int kEpiWarpBytes = kEpiBuf;
+  static constexpr int kEpiBytes = 8 * kEpiWarpBytes;
   static constexpr int kMaxStages = ((kPerSm == 2 ? 108 : 218) * 1024 - kEpiBytes - 1024) / kStageBytes;
   static constexpr int kStages = kMaxStages > 8 ? 8 : kMaxStages;
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024;
@@ -815,7 +228,7 @@ struct DyCfg {
   // K / kGroupsPerTile.  The MMAs run kBufs groups ahead of the accumulate
   // warps, so (kBufs / kGroupsPerTile) of a tile's MMA time hides that tile's
   // predecessor's epilogue: 2/3 of a tile for N = 256, a whole tile below.
-  static constexpr int kGroupsPerTile = BN >= 256 ? 3 : DX3 ? 2 : 4;
+  static constexpr int kGroupsPerTile = BN >= 256 ? 3 : 4;
   static constexpr int kTmemCols = kBufs * kCols <= 32 ? 32 : kBufs * kCols <= 64 ? 64
                                    : kBufs * kCols <= 128 ? 128 : kBufs * kCols <= 256 ? 256 : 512;
   static constexpr int kHalf = BN / 2;
@@ -823,20 +236,18 @@ struct DyCfg {
 
 // HEAD: 0 plain conv; 1 / 2 (BN = 256 only) = the L9 training / validation
 // head fused into the epilogue (see HeadTrainArgs / HeadValArgs).
-template <int BN, int HEAD, bool DX3 = false>
-__global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 registers at 1 CTA/SM
+// amax: range-guard slot of the operand pair this launch writes (or null).
+template <int BN, int HEAD>
+__global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registers at 1 CTA/SM
     k_conv3x3_dy(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                  const __grid_constant__ CUtensorMap mw, const __grid_constant__ CUtensorMap mwl,
                  const __grid_constant__ CUtensorMap my, const __grid_constant__ CUtensorMap myh,
                  const __grid_constant__ CUtensorMap myl, int omask, float oscale, ConvOut out,
-                 int flags, const float* __restrict__ bias, const void* __restrict__ mask,
-                 int mask_bits, uint32_t* __restrict__ mbits_out, float* __restrict__ colsum,
+                 const float* __restrict__ bias, const void* __restrict__ mask, int mask_bits,
+                 uint32_t* __restrict__ mbits_out, float* __restrict__ colsum, unsigned* __restrict__ amax,
                  float unscale, int H, int W, int C, int epi, HeadTrainArgs ht, HeadValArgs hv) {
-  using Cfg = DyCfg<BN, DX3>;
-  static_assert(!DX3 || (HEAD == 0 && BN <= 64), "dx-stacked tiles: narrow plain convolutions");
-  // flags: bits 8.. accumulation groups per tile (experiment override, 0 =
-  // DyCfg::kGroupsPerTile)
-  using P = Prec<true>;
+  using Cfg = DyCfg<BN>;
+  using P = Prec;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
   constexpr int NB = Cfg::kBufs;
@@ -857,8 +268,7 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
   const int tiles_x = (W + 2 * Cfg::kTileW - 1) / (2 * Cfg::kTileW);
   const int nunits = tiles_x * ((H + 7) / 8);
   const int KB = 3 * (C / Cfg::kKC);  // stages per tile
-  const int gpt_req = (flags >> 8) ? (flags >> 8) : Cfg::kGroupsPerTile;
-  const int NG = KB < gpt_req ? KB : gpt_req;  // accumulation groups per tile
+  const int NG = KB < Cfg::kGroupsPerTile ? KB : Cfg::kGroupsPerTile;  // accumulation groups per tile
 
   if (tid == 0) {
     if (HEAD == 1 && blockIdx.x == 0 && ht.step_counter) *ht.step_counter += 1;  // Adam t
@@ -949,33 +359,22 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
             tc_fence_after();
             if (elect_one_sync()) {
               const uint64_t a0 = desc0 + (uint64_t)(st * (Cfg::kStageBytes >> 4));
-              if constexpr (DX3) {  // one MMA covers the three taps (B rows = [tap][n])
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
                 for (int k = 0; k < Cfg::kKSteps; ++k) {
-                  const uint64_t a = a0 + 2 * k, bh = a0 + kBh + 2 * k;
-                  mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | k) != 0);
+                  const uint64_t a = a0 + Cfg::kDxUnits * dx + 2 * k;
+                  const uint64_t bh = a0 + kBh + kTap * dx + 2 * k;
+                  mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | dx | k) != 0);
                   mma_f16_2sm(d, a + kAl, bh, idesc, 1);
                 }
+              }
 #pragma unroll
-                for (int k = 0; k < Cfg::kKSteps; ++k) mma_f16_2sm(d, a0 + 2 * k, a0 + kBh + 2 * k, idesc, 1);
-              } else {
+              for (int dx = 0; dx < 3; ++dx) {
 #pragma unroll
-                for (int dx = 0; dx < 3; ++dx) {
-#pragma unroll
-                  for (int k = 0; k < Cfg::kKSteps; ++k) {
-                    const uint64_t a = a0 + Cfg::kDxUnits * dx + 2 * k;
-                    const uint64_t bh = a0 + kBh + kTap * dx + 2 * k;
-                    mma_f16_2sm(d, a, bh + (kBl - kBh), idesc, ((kb - s0) | dx | k) != 0);
-                    mma_f16_2sm(d, a + kAl, bh, idesc, 1);
-                  }
-                }
-#pragma unroll
-                for (int dx = 0; dx < 3; ++dx) {
-#pragma unroll
-                  for (int k = 0; k < Cfg::kKSteps; ++k)
-                    mma_f16_2sm(d, a0 + Cfg::kDxUnits * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k,
-                                idesc, 1);
-                }
+                for (int k = 0; k < Cfg::kKSteps; ++k)
+                  mma_f16_2sm(d, a0 + Cfg::kDxUnits * dx + 2 * k, a0 + kBh + kTap * dx + 2 * k,
+                              idesc, 1);
               }
               mma_commit_2sm(&empty[st]);
             }
@@ -995,8 +394,7 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
     // ---- group accumulation in registers (round-to-nearest fp32 adds)
     const int q = warp & 3;            // TMEM lane quarter
     const int half = (warp - 2) >> 2;  // column half
-    // DX3: this warp's columns are its channel half's three tap blocks
-    constexpr int ACOLS = DX3 ? 3 * HALF : HALF;
+    constexpr int ACOLS = HALF;
     const uint32_t lane_base = taddr + ((uint32_t)(q * 32) << 16) + half * ACOLS;
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
 #if N2F_TC_TRACE
@@ -1015,8 +413,8 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
     constexpr int RBY = EC * 4, RBH = EC * 2;  // staging row bytes: fp32 / fp16
     const int srow = lane;  // staging row: box {EC ch, 8 y, 4 x} staged [x][y][ch]
     uint8_t* stg0 = base + S * Cfg::kStageBytes + (warp - 2) * Cfg::kEpiWarpBytes;
-    int gg = 0, sb = 0;
-    int tpar = 0;  // DX3 exchange buffer parity
+    int gg = 0;
+    unsigned rmax = 0;  // max |x * 2^e| of the pair values this thread wrote (range guard)
     for (int ut = cid; ut < nunits; ut += ncl) {
       const int x0 = (ut % tiles_x) * 2 * Cfg::kTileW + Cfg::kTileW * (int)rank, y0 = (ut / tiles_x) * 8;
       const int tile = ut * 2 + (int)rank;  // colsum row
@@ -1049,37 +447,12 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
       const long long ce = clock64();
 #endif
 
-      if constexpr (DX3) {
-        // out(column xl - 1) = tap0(xl - 1) + tap1(xl) + tap2(xl + 1): the
-        // neighbouring columns are 8 lanes away; at the quarter edges they
-        // come from the adjacent warp of this channel half through smem
-        float* xch = reinterpret_cast<float*>(base + S * Cfg::kStageBytes) +
-                     (size_t)((tpar * 2 + half) * 4) * 2 * 8 * HALF;
-        if (lane >= 24) {  // tap0 of this warp's last column, for warp q + 1
-#pragma unroll
-          for (int j = 0; j < HALF; ++j) xch[((q * 2 + 0) * 8 + (lane - 24)) * HALF + j] = acc[j];
-        }
-        if (lane < 8) {  // tap2 of this warp's first column, for warp q - 1
-#pragma unroll
-          for (int j = 0; j < HALF; ++j) xch[((q * 2 + 1) * 8 + lane) * HALF + j] = acc[2 * HALF + j];
-        }
-        asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
-#pragma unroll
-        for (int j = 0; j < HALF; ++j) {
-          float left = __shfl_up_sync(0xffffffffu, acc[j], 8);
-          float right = __shfl_down_sync(0xffffffffu, acc[2 * HALF + j], 8);
-          if (lane < 8) left = q > 0 ? xch[(((q - 1) * 2 + 0) * 8 + lane) * HALF + j] : 0.f;
-          if (lane >= 24) right = q < 3 ? xch[(((q + 1) * 2 + 1) * 8 + (lane - 24)) * HALF + j] : 0.f;
-          acc[j] = __fadd_rn(__fadd_rn(left, acc[HALF + j]), right);
-        }
-        tpar ^= 1;
-      }
 
       // ---- epilogue (see k_conv3x3_tc): scale removal, bias+ReLU or the ReLU
       // mask, column sums, bit masks, staging in the TMA swizzle layout and
-      // TMA tensor stores of {EC channels, 4 x, 8 y} boxes (DX3: direct stores)
-      const int px = x0 + xl - (DX3 ? 1 : 0), py = y0 + yl;
-      const bool valid = py < H && px < W && (!DX3 || (xl >= 1 && xl <= 14));
+      // TMA tensor stores of {EC channels, 4 x, 8 y} boxes
+      const int px = x0 + xl, py = y0 + yl;
+      const bool valid = py < H && px < W;
       const int n0 = half * HALF;
       constexpr int WPP = BN / 32, MW = HALF / 32 > 0 ? HALF / 32 : 1;
       const int64_t pix = (int64_t)py * W + px;
@@ -1168,8 +541,10 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
 #pragma unroll
             for (int i = 0; i < EC; i += 2) {
               __half h0, l0, h1, l1;
-              split_f16(__fmul_rn(gk[i], oscale), h0, l0);
-              split_f16(__fmul_rn(gk[i + 1], oscale), h1, l1);
+              const float a0 = __fmul_rn(gk[i], oscale), a1 = __fmul_rn(gk[i + 1], oscale);
+              if (valid) rmax = max(rmax, max(range_bits(a0), range_bits(a1)));
+              split_f16(a0, h0, l0);
+              split_f16(a1, h1, l1);
               hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
               lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
             }
@@ -1242,7 +617,7 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
 #pragma unroll
           for (int k = 0; k < CH; ++k) {
             float4 mk = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid) mk = load_mask4<true>(mask, idx + 4 * k);
+            if (valid) mk = load_mask4(mask, idx + 4 * k);
             v[4 * k] = mk.x > 0.f ? v[4 * k] : 0.f;
             v[4 * k + 1] = mk.y > 0.f ? v[4 * k + 1] : 0.f;
             v[4 * k + 2] = mk.z > 0.f ? v[4 * k + 2] : 0.f;
@@ -1285,50 +660,13 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
           }
           if ((lane & (32 / EC - 1)) == 0) csum[q][n + ch] = r[0];
         }
-        if constexpr (DX3) {  // direct stores of this lane's pixel (EC channels)
-          if (valid) {
-            const int64_t idx = pix * BN + n;
-            if (omask & kOutY) {
-#pragma unroll
-              for (int k = 0; k < CH; ++k)
-                *reinterpret_cast<float4*>(out.y + idx + 4 * k) =
-                    make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-            }
-            if (omask & (kOutHi | kOutLo)) {
-              uint32_t hw[EC / 2], lw[EC / 2];
-#pragma unroll
-              for (int i = 0; i < EC; i += 2) {
-                __half h0, l0, h1, l1;
-                split_f16(v[i] * oscale, h0, l0);
-                split_f16(v[i + 1] * oscale, h1, l1);
-                hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-                lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-              }
-#pragma unroll
-              for (int k = 0; k < EC / 8; ++k) {
-                if (omask & kOutHi)
-                  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out.yhi) + idx + 8 * k) =
-                      make_uint4(hw[4 * k], hw[4 * k + 1], hw[4 * k + 2], hw[4 * k + 3]);
-                if (omask & kOutLo)
-                  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(out.ylo) + idx + 8 * k) =
-                      make_uint4(lw[4 * k], lw[4 * k + 1], lw[4 * k + 2], lw[4 * k + 3]);
-              }
-            }
-          }
-          continue;
-        }
-        // staging buffer sb: its previous TMA stores (two slices ago) must be done reading
-        uint8_t* stg = stg0 + sb * Cfg::kEpiBuf;
+        // the staging buffer's previous TMA stores must be done reading it
+        uint8_t* stg = stg0;
 #if N2F_TC_TRACE
         const long long cw = clock64();
         tcomp += cw - cs0;
 #endif
-        if (lane == 0) {
-          if (Cfg::kEpiNBuf == 2)
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          else
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
 #if N2F_TC_TRACE
         twr += clock64() - cw;
@@ -1344,8 +682,10 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
 #pragma unroll
           for (int i = 0; i < EC; i += 2) {
             __half h0, l0, h1, l1;
-            split_f16(v[i] * oscale, h0, l0);
-            split_f16(v[i + 1] * oscale, h1, l1);
+            const float a0 = v[i] * oscale, a1 = v[i + 1] * oscale;
+            if (valid) rmax = max(rmax, max(range_bits(a0), range_bits(a1)));
+            split_f16(a0, h0, l0);
+            split_f16(a1, h1, l1);
             hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
             lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
           }
@@ -1371,7 +711,6 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
           if (omask & kOutLo) tma_store_3d(&myl, stg + 32 * RBH, n, y0, bx);
           bulk_commit_group();
         }
-        if (Cfg::kEpiNBuf == 2) sb ^= 1;
 #if N2F_TC_TRACE
         __syncwarp();
         tiss += clock64() - cf;
@@ -1394,6 +733,7 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN, DX3>::kPerSm)  // 168 re
              "wait_read %lld stage+fence %lld issue %lld)\n",
              warp, C, BN, clock64() - t_0, tw, td, te, tcomp, twr, tstg - twr, tiss);
 #endif
+    if (amax) range_note(amax, rmax);
     if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
@@ -1419,9 +759,9 @@ constexpr int kSegW = 32;  // default pixels per stage (one image-row segment)
 // (tap, channel) rows, B = BN / CS / 32 blocks of gradient channels.  Narrow
 // layers take 64-pixel stages (twice the MMA work per TMA instruction) with
 // one stage per accumulation group (K = 64, as the 2 x 32 grouping).
-template <int BN, bool F16, int CS, int SEG>
+template <int BN, int CS, int SEG>
 struct WgCfg {
-  using P = Prec<F16>;
+  using P = Prec;
   static constexpr int kBlk = SEG * P::kRow;  // bytes of one 32-channel MN block
   static constexpr int kStageA = 4 * kBlk;
   static constexpr int kStageB = (BN / CS / 32) * kBlk;
@@ -1430,27 +770,27 @@ struct WgCfg {
   // stages per TMEM accumulation group.  A group's drain reads BN fp32
   // columns x 128 lanes from TMEM (~64 B/clk): the pair kernels (N >= 128)
   // take 4 stages (128 pixels) so the MMAs of a group outlast its drain
-  static constexpr int kGroup = SEG == 64 ? 1 : (F16 && CS == 2 ? N2F_WG_GROUP_PAIR : P::kGroup);
+  static constexpr int kGroup = SEG == 64 ? 1 : (CS == 2 ? kWgGroupPair : 2);
   static constexpr int kMaxStages = (200 * 1024) / kStageBytes;
-  static constexpr int kStages = kTwoPerSm ? 2 * P::kGroup : (kMaxStages > 8 ? 8 : kMaxStages);
+  static constexpr int kStages = kTwoPerSm ? 4 : (kMaxStages > 8 ? 8 : kMaxStages);
   static constexpr int kSmem = kStages * kStageBytes + 1024;
   static constexpr int kTmemBudget = kTwoPerSm ? 256 : 512;
   static constexpr int kBufs = kTmemBudget / BN > 4 ? 4 : kTmemBudget / BN;
   static constexpr int kTmemCols = kBufs * BN;
   static constexpr int kHalf = BN / 2;
-  static constexpr int kKSteps = SEG / (F16 ? 16 : 8);  // MMA K steps per stage
+  static constexpr int kKSteps = SEG / 16;  // MMA K steps per stage
 };
 
 // CTA pairs (CS = 2, used when C % 128 == 0 and N >= 128): a cluster owns
 // two consecutive M blocks (cta_group::2 MMA, M = 256); each CTA stages its
 // own activation blocks and half of the gradient channels.
-template <int BN, bool F16, int CS, int SEG>
+template <int BN, int CS, int SEG>
 __global__ void __launch_bounds__(kThreadsTc, 1)
     k_wgrad3x3_tc(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mxl,
                   const __grid_constant__ CUtensorMap mg, const __grid_constant__ CUtensorMap mgl,
                   float* __restrict__ part, float unscale, int H, int W, int C, int nsplit, int xblk) {
-  using Cfg = WgCfg<BN, F16, CS, SEG>;
-  using P = Prec<F16>;
+  using Cfg = WgCfg<BN, CS, SEG>;
+  using P = Prec;
   constexpr int kBlk = Cfg::kBlk;
   constexpr int S = Cfg::kStages;
   constexpr int HALF = Cfg::kHalf;
@@ -1692,23 +1032,18 @@ __global__ void __launch_bounds__(kThreadsTc, 1)
   }
 }
 
-__global__ void k_split_lo(const float* __restrict__ x, float* __restrict__ lo, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float h;
-    split_tf32(x[i], h, lo[i]);
-  }
-}
-
 __global__ void k_split_f16(const float* __restrict__ x, __half* __restrict__ hi,
-                            __half* __restrict__ lo, float scale, int64_t n) {
+                            __half* __restrict__ lo, float scale, int64_t n, unsigned* __restrict__ amax) {
+  unsigned mx = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float a = x[i] * scale;
+    mx = max(mx, range_bits(a));
     const __half h = __float2half_rn(a);
     hi[i] = h;
     lo[i] = __float2half_rn(__fsub_rn(a, __half2float(h)));
   }
+  if (amax) range_note(amax, mx);
 }
 
 // ---------------------------------------------------------------------------
@@ -1727,36 +1062,18 @@ int encoder() {
   return N2F_OK;
 }
 
-// NHWC activation [H][W][C] viewed as 3-D (C, W, H).
-int map_act(CUtensorMap* m, const void* p, bool f16, int C, int W, int H, int bc, int bw, int bh,
-            CUtensorMapSwizzle sw) {
-  N2F_TRY(encoder());
-  const cuuint64_t es = f16 ? 2 : 4;
-  const cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H};
-  const cuuint64_t strides[2] = {(cuuint64_t)C * es, (cuuint64_t)W * C * es};
-  const cuuint32_t box[3] = {(cuuint32_t)bc, (cuuint32_t)bw, (cuuint32_t)bh};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = g_encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                        3, const_cast<void*>(p), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(act) failed: %d", (int)r);
-  return N2F_OK;
-}
-
 // NHWC activation viewed as 4-D (32 channels, W, C / 32 blocks, H): a box
 // {32, bw, nblk, 1} lands as [block][pixel][32 channels], i.e. nblk MN-major
 // operand blocks of bw pixel rows in one TMA.
-int map_act_blk(CUtensorMap* m, const void* p, bool f16, int C, int W, int H, int bw, int nblk,
-                CUtensorMapSwizzle sw) {
+int map_act_blk(CUtensorMap* m, const void* p, int C, int W, int H, int bw, int nblk) {
   N2F_TRY(encoder());
-  const cuuint64_t es = f16 ? 2 : 4;
+  const cuuint64_t es = 2;
+  const CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_64B;
   const cuuint64_t dims[4] = {32, (cuuint64_t)W, (cuuint64_t)(C / 32), (cuuint64_t)H};
   const cuuint64_t strides[3] = {(cuuint64_t)C * es, 32 * es, (cuuint64_t)W * C * es};
   const cuuint32_t box[4] = {32, (cuuint32_t)bw, (cuuint32_t)nblk, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = g_encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                        4, const_cast<void*>(p), dims, strides, box, estr,
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(p), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(act4) failed: %d", (int)r);
@@ -1812,219 +1129,72 @@ int map_w_taps(CUtensorMap* m, const void* p, int C, int N, int bc, int rows) {
   return N2F_OK;
 }
 
-// Row-major matrix [rows][cols] viewed as 2-D (cols, rows).
-int map_mat(CUtensorMap* m, const void* p, bool f16, int cols, int rows, int bc, int br,
-            CUtensorMapSwizzle sw) {
-  N2F_TRY(encoder());
-  const cuuint64_t es = f16 ? 2 : 4;
-  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)cols * es};
-  const cuuint32_t box[2] = {(cuuint32_t)bc, (cuuint32_t)br};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                        2, const_cast<void*>(p), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(N2F_ERR_CUDA, "cuTensorMapEncodeTiled(mat) failed: %d", (int)r);
-  return N2F_OK;
-}
-
-// N2F_PDL=0 disables programmatic dependent launch (A/B experiments)
-int pdl_enabled() {
-  static const int on = [] {
-    const char* e = getenv("N2F_PDL");
-    return e ? atoi(e) : 1;
-  }();
-  return on;
-}
-
-template <int BN, bool F16>
-int set_attr_one() {
-  N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, F16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                FwdCfg<BN, F16, 1>::kSmem));
-  if (BN >= 128) {
-    N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_tc<BN, F16, 2>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  FwdCfg<BN, F16, 2>::kSmem));
-  }
-  if (F16) {
-    N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<BN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  DyCfg<BN>::kSmem));
-    if constexpr (BN <= 64)
-      N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<BN, 0, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, DyCfg<BN, true>::kSmem));
-    if (BN == 256) {
-      N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<256, 1>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, DyCfg<256>::kSmem));
-      N2F_CUDA(cudaFuncSetAttribute(k_conv3x3_dy<256, 2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, DyCfg<256>::kSmem));
-    }
-  }
-  N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1, 32>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                WgCfg<BN, F16, 1, 32>::kSmem));
-  if (F16) {
-    N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1, 64>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  WgCfg<BN, F16, 1, 64>::kSmem));
-    if constexpr (BN <= 64)
-      N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 1, 128>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    WgCfg<BN, F16, 1, 128>::kSmem));
-  }
-  if (BN >= 128) {
-    N2F_CUDA(cudaFuncSetAttribute(k_wgrad3x3_tc<BN, F16, 2, 32>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  WgCfg<BN, F16, 2, 32>::kSmem));
-  }
-  return N2F_OK;
-}
-
 int set_attrs_once() {
   static bool done = false;
   if (done) return N2F_OK;
-  N2F_TRY((set_attr_one<32, false>()));
-  N2F_TRY((set_attr_one<64, false>()));
-  N2F_TRY((set_attr_one<128, false>()));
-  N2F_TRY((set_attr_one<256, false>()));
-  N2F_TRY((set_attr_one<32, true>()));
-  N2F_TRY((set_attr_one<64, true>()));
-  N2F_TRY((set_attr_one<128, true>()));
-  N2F_TRY((set_attr_one<256, true>()));
+#define N2F_SMEM(kern, bytes) \
+  N2F_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))
+  N2F_SMEM((k_conv3x3_dy<32, 0>), DyCfg<32>::kSmem);
+  N2F_SMEM((k_conv3x3_dy<64, 0>), DyCfg<64>::kSmem);
+  N2F_SMEM((k_conv3x3_dy<128, 0>), DyCfg<128>::kSmem);
+  N2F_SMEM((k_conv3x3_dy<256, 0>), DyCfg<256>::kSmem);
+  N2F_SMEM((k_conv3x3_dy<256, 1>), DyCfg<256>::kSmem);
+  N2F_SMEM((k_conv3x3_dy<256, 2>), DyCfg<256>::kSmem);
+  N2F_SMEM((k_wgrad3x3_tc<32, 1, 64>), (WgCfg<32, 1, 64>::kSmem));
+  N2F_SMEM((k_wgrad3x3_tc<32, 1, 128>), (WgCfg<32, 1, 128>::kSmem));
+  N2F_SMEM((k_wgrad3x3_tc<64, 1, 64>), (WgCfg<64, 1, 64>::kSmem));
+  N2F_SMEM((k_wgrad3x3_tc<64, 1, 128>), (WgCfg<64, 1, 128>::kSmem));
+  N2F_SMEM((k_wgrad3x3_tc<128, 1, 64>), (WgCfg<128, 1, 64>::kSmem));
+  N2F_SMEM((k_wgrad3x3_tc<128, 2, 32>), (WgCfg<128, 2, 32>::kSmem));
+  N2F_SMEM((k_wgrad3x3_tc<256, 1, 64>), (WgCfg<256, 1, 64>::kSmem));
+  N2F_SMEM((k_wgrad3x3_tc<256, 2, 32>), (WgCfg<256, 2, 32>::kSmem));
+#undef N2F_SMEM
   done = true;
   return N2F_OK;
 }
 
-template <int BN, bool F16, int CS>
-int launch_conv_tc_bn(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum,
-                      int epi, cudaStream_t st) {
+// Launch attributes of every tcgen05 kernel: a cluster of cs CTAs, and
+// programmatic dependent launch (the prologue -- barrier init, TMEM alloc,
+// descriptor prefetch -- overlaps the previous kernel's tail; measured 0.7 %
+// faster per epoch).
+struct LaunchCfg {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.grid);
-  cfg.blockDim = dim3(kThreadsTc);
-  cfg.dynamicSmemBytes = FwdCfg<BN, F16, CS>::kSmem;
-  cfg.stream = st;
   cudaLaunchAttribute attr[2];
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_tc<BN, F16, CS>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
-                              pl.myh, pl.myl, pl.omask, pl.oscale,
-                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, bias, mask, pl.mask_bits,
-                              pl.mbits_out, colsum, pl.unscale,
-                              pl.H, pl.W, pl.C, epi, pl.dbg));
-  N2F_LAUNCH_CHECK();
-  return N2F_OK;
-}
+  LaunchCfg(dim3 grid, int smem, int cs, cudaStream_t st) {
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreadsTc);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+  }
+};
 
-template <int BN, int HEAD, bool DX3 = false>
+template <int BN, int HEAD>
 int launch_conv_dy(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
                    const HeadTrainArgs& ht, const HeadValArgs& hv, cudaStream_t st) {
-  if constexpr (HEAD == 0 && !DX3 && BN <= 64) {
-    if (pl.dx3) return launch_conv_dy<BN, 0, true>(pl, bias, mask, colsum, epi, ht, hv, st);
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.grid);
-  cfg.blockDim = dim3(kThreadsTc);
-  cfg.dynamicSmemBytes = DyCfg<BN, DX3>::kSmem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  static const int flags = [] {
-    const char* g = getenv("N2F_DY_GROUPS");  // accumulation groups per tile (experiment)
-    return (g ? atoi(g) : 0) << 8;
-  }();
-  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_conv3x3_dy<BN, HEAD, DX3>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
+  LaunchCfg lc(dim3(pl.grid), DyCfg<BN>::kSmem, 2, st);
+  N2F_CUDA(cudaLaunchKernelEx(&lc.cfg, k_conv3x3_dy<BN, HEAD>, pl.mx, pl.mxl, pl.mw, pl.mwl, pl.my,
                               pl.myh, pl.myl, pl.omask, pl.oscale,
-                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, flags, bias, mask,
-                              pl.mask_bits, pl.mbits_out, colsum, pl.unscale, pl.H, pl.W, pl.C, epi,
-                              ht, hv));
+                              ConvOut{pl.y, pl.yhi, pl.ylo, pl.oscale}, bias, mask, pl.mask_bits,
+                              pl.mbits_out, colsum, pl.amax, pl.unscale, pl.H, pl.W, pl.C, epi, ht, hv));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }
 
-template <bool F16>
-int launch_conv_tc_p(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum,
-                     int epi, cudaStream_t st) {
-  if (F16 && pl.dy) {
-    const HeadTrainArgs ht{};
-    const HeadValArgs hv{};
-    switch (pl.N) {
-      case 32: return launch_conv_dy<32, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
-      case 64: return launch_conv_dy<64, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
-      case 128: return launch_conv_dy<128, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
-      case 256: return launch_conv_dy<256, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
-    }
-  }
-  const bool two = pl.cs == 2;
-  switch (pl.N) {
-    case 32: return launch_conv_tc_bn<32, F16, 1>(pl, bias, mask, colsum, epi, st);
-    case 64: return launch_conv_tc_bn<64, F16, 1>(pl, bias, mask, colsum, epi, st);
-    case 128:
-      return two ? launch_conv_tc_bn<128, F16, 2>(pl, bias, mask, colsum, epi, st)
-                 : launch_conv_tc_bn<128, F16, 1>(pl, bias, mask, colsum, epi, st);
-    case 256:
-      return two ? launch_conv_tc_bn<256, F16, 2>(pl, bias, mask, colsum, epi, st)
-                 : launch_conv_tc_bn<256, F16, 1>(pl, bias, mask, colsum, epi, st);
-  }
-  return fail(N2F_ERR_ARG, "conv_tc_launch: N=%d", pl.N);
-}
-
-template <int BN, bool F16, int CS, int SEG>
+template <int BN, int CS, int SEG>
 int launch_wgrad_tc_bn(const WgradTcPlan& pl, float* part, cudaStream_t st) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.gridx, pl.nsplit);
-  cfg.blockDim = dim3(kThreadsTc);
-  cfg.dynamicSmemBytes = WgCfg<BN, F16, CS, SEG>::kSmem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  N2F_CUDA(cudaLaunchKernelEx(&cfg, k_wgrad3x3_tc<BN, F16, CS, SEG>, pl.mx, pl.mxl, pl.mg, pl.mgl,
+  LaunchCfg lc(dim3(pl.gridx, pl.nsplit), WgCfg<BN, CS, SEG>::kSmem, CS, st);
+  N2F_CUDA(cudaLaunchKernelEx(&lc.cfg, k_wgrad3x3_tc<BN, CS, SEG>, pl.mx, pl.mxl, pl.mg, pl.mgl,
                               part, pl.unscale, pl.H, pl.W, pl.C, pl.nsplit, pl.xblk));
   N2F_LAUNCH_CHECK();
   return N2F_OK;
-}
-
-template <int BN, bool F16>
-int launch_wgrad_tc_n(const WgradTcPlan& pl, float* part, cudaStream_t st) {
-  if (pl.cs == 2) {
-    if constexpr (BN >= 128) return launch_wgrad_tc_bn<BN, F16, 2, 32>(pl, part, st);
-    return fail(N2F_ERR_ARG, "wgrad pair with N=%d", BN);
-  }
-  if (F16 && pl.seg == 128) {
-    if constexpr (BN <= 64) return launch_wgrad_tc_bn<BN, F16, 1, F16 ? 128 : 32>(pl, part, st);
-  }
-  if (F16 && pl.seg >= 64) return launch_wgrad_tc_bn<BN, F16, 1, F16 ? 64 : 32>(pl, part, st);
-  return launch_wgrad_tc_bn<BN, F16, 1, 32>(pl, part, st);
-}
-
-template <bool F16>
-int launch_wgrad_tc_p(const WgradTcPlan& pl, float* part, cudaStream_t st) {
-  switch (pl.N) {
-    case 32: return launch_wgrad_tc_n<32, F16>(pl, part, st);
-    case 64: return launch_wgrad_tc_n<64, F16>(pl, part, st);
-    case 128: return launch_wgrad_tc_n<128, F16>(pl, part, st);
-    case 256: return launch_wgrad_tc_n<256, F16>(pl, part, st);
-  }
-  return fail(N2F_ERR_ARG, "wgrad_tc_launch: N=%d", pl.N);
 }
 
 int sm_count() {
@@ -2038,70 +1208,9 @@ int sm_count() {
   return n;
 }
 
-}  // namespace
-
-bool tc_supported(int cin, int cout) {
-  return cin % 32 == 0 && (cout == 32 || cout == 64 || cout == 128 || cout == 256);
-}
-
-int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, int W, int C, int N,
-                 bool f16) {
-  if (!tc_supported(C, N)) return fail(N2F_ERR_ARG, "conv_tc_plan: C=%d N=%d", C, N);
-  N2F_TRY(set_attrs_once());  // outside any stream capture
-  pl->H = H;
-  pl->W = W;
-  pl->C = C;
-  pl->N = N;
-  pl->f16 = f16;
-  pl->unscale = ldexpf(1.f, -(x.exp + w.exp));
-  // N2F_TC_DEBUG: kernel-structure experiments for profiling only (results
-  // are wrong when set): 1 skip the TMEM drain, 2 skip the MMAs, 4 skip TMA
-  const char* dbg = getenv("N2F_TC_DEBUG");
-  pl->dbg = dbg ? atoi(dbg) : 0;
-  // FP16: the dy-stage CTA-pair kernel (N2F_CONV_DY=0 selects the per-tap
-  // kernel below, 1 uses dy only for N <= 128)
-  const char* dyenv = getenv("N2F_CONV_DY");
-  const int dymode = dyenv ? atoi(dyenv) : 2;
-  pl->dy = f16 && (dymode == 2 || (dymode == 1 && N <= 128));
-  // N2F_DY_DX3=1: narrow layers stack the dx taps in N (experiment: correct,
-  // but measured 1.5-2.4x slower than the per-tap MMAs)
-  const char* dx3env = getenv("N2F_DY_DX3");
-  pl->dx3 = pl->dy && N <= 64 && dx3env && atoi(dx3env) == 1;
-  if (pl->dy) {
-    pl->cs = 2;
-    const int pairw = pl->dx3 ? 28 : 32;  // 2 x DyCfg::kTileW output columns per pair tile
-    const int units = ((W + pairw - 1) / pairw) * ((H + 7) / 8);
-    const int max_units = (N <= N2F_DY_2SM_MAXN ? 2 : 1) * sm_count() / 2;  // DyCfg<N>::kPerSm
-    pl->grid = 2 * (units < max_units ? units : max_units);
-    pl->tiles = 2 * units;
-    const int kc = N2F_DY_KC16 && N == 256 ? 16 : 32;  // DyCfg<N>::kKC
-    const int boxw = pl->dx3 ? 16 : 18;  // DyCfg::kRowsA / 8 activation columns
-    N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, kc, 8, boxw));
-    N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, kc, 8, boxw));
-    N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, kc, N / 2));
-    N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, kc, N / 2));
-    return N2F_OK;
-  }
-  // wide layers (N >= 128) run as CTA pairs (cta_group::2, M = 256: each CTA
-  // stages its own 128 pixels and half of the weight rows); N2F_TC_CLUSTER=1
-  // forces single CTAs
-  const char* cl = getenv("N2F_TC_CLUSTER");
-  pl->cs = (N >= 128 && !(cl && atoi(cl) == 1)) ? 2 : 1;
-  // persistent grid: one CTA per SM (two for the narrow layers, whose smem
-  // and register footprints allow it), each walking cluster tiles with a
-  // fixed stride
-  const int units = ((W + kTW - 1) / kTW) * ((H + kTH * pl->cs - 1) / (kTH * pl->cs));
-  const int per_sm = N <= 64 ? 2 : 1;
-  const int max_units = per_sm * sm_count() / pl->cs;
-  pl->grid = pl->cs * (units < max_units ? units : max_units);
-  pl->tiles = units * pl->cs;
-  const CUtensorMapSwizzle sw = f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
-  N2F_TRY(map_act(&pl->mx, x.hi, f16, C, W, H, 32, kTW, kTH, sw));
-  N2F_TRY(map_act(&pl->mxl, x.lo, f16, C, W, H, 32, kTW, kTH, sw));
-  N2F_TRY(map_mat(&pl->mw, w.hi, f16, 9 * C, N, 32, N / pl->cs, sw));
-  N2F_TRY(map_mat(&pl->mwl, w.lo, f16, 9 * C, N, 32, N / pl->cs, sw));
-  return N2F_OK;
-}
+// CTA pairs for the wide wgrads (one 4-D activation box per stage and an even
+// split of the gradient channels)
+int wgrad_cs(int cin, int cout) { return (cin % 128 == 0 && cout >= 128) ? 2 : 1; }
 
 // DyCfg<N>::kEpiCols on the host (the TMA-store box must match the staging slice)
 int dy_epi_cols(int N) {
@@ -2113,19 +1222,40 @@ int dy_epi_cols(int N) {
   }
 }
 
-int conv_tc_tiles(int H, int W) {  // upper bound of ConvTcPlan::tiles for any plan
-  const int per_tap = ((W + kTW - 1) / kTW) * 2 * ((H + 2 * kTH - 1) / (2 * kTH));
-  const int dx3 = 2 * ((W + 27) / 28) * ((H + 7) / 8);  // 14 x 8 tiles of the dx-stacked dy kernel
-  return per_tap > dx3 ? per_tap : dx3;
+}  // namespace
+
+bool tc_supported(int cin, int cout) {
+  return cin % 32 == 0 && (cout == 32 || cout == 64 || cout == 128 || cout == 256);
 }
 
-// Output tensor maps of a conv plan: NHWC [H][W][N] viewed as (N, W, H), box
-// {EC channels, 32 pixels, 1 row} = one accumulate warp's staging slice.
+// A conv plan: the dy-stage CTA-pair kernel over 32 x 8 pixel pair tiles,
+// persistent grid (one CTA pair per SM, two for N <= kDy2SmMaxN).
+int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, int W, int C, int N) {
+  if (!tc_supported(C, N)) return fail(N2F_ERR_ARG, "conv_tc_plan: C=%d N=%d", C, N);
+  N2F_TRY(set_attrs_once());  // outside any stream capture
+  pl->H = H;
+  pl->W = W;
+  pl->C = C;
+  pl->N = N;
+  pl->unscale = ldexpf(1.f, -(x.exp + w.exp));
+  pl->amax = nullptr;
+  const int units = ((W + 31) / 32) * ((H + 7) / 8);
+  const int max_units = (N <= kDy2SmMaxN ? 2 : 1) * sm_count() / 2;  // DyCfg<N>::kPerSm
+  pl->grid = 2 * (units < max_units ? units : max_units);
+  pl->tiles = 2 * units;
+  N2F_TRY(map_act_yx(&pl->mx, x.hi, C, W, H, 32, 8, 18));
+  N2F_TRY(map_act_yx(&pl->mxl, x.lo, C, W, H, 32, 8, 18));
+  N2F_TRY(map_w_taps(&pl->mw, w.hi, C, N, 32, N / 2));
+  N2F_TRY(map_w_taps(&pl->mwl, w.lo, C, N, 32, N / 2));
+  return N2F_OK;
+}
+
+int conv_tc_tiles(int H, int W) { return 2 * ((W + 31) / 32) * ((H + 7) / 8); }
+
+// Output tensor maps of a conv plan: NHWC [H][W][N] viewed as (N, H, W), box
+// {EC channels, 8 y, 4 x} = one accumulate warp's staging slice.
 int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale) {
-  if (!pl->f16 && ylo && !y) return fail(N2F_ERR_ARG, "tf32 pair output needs the fp32 tensor");
-  // staging slice geometry: dy kernel {EC channels, 4 x, 8 y}, else {EC, 32 x, 1 y}
-  const int ec = pl->dy ? dy_epi_cols(pl->N) : (pl->N >= 128 ? 16 : (pl->f16 ? 8 : 4));
-  const int bw = pl->dy ? 4 : kTW, bh = pl->dy ? 8 : 1;
+  const int ec = dy_epi_cols(pl->N);
   auto sw_for = [](int row_bytes) {
     return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
            : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
@@ -2138,67 +1268,63 @@ int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscal
   pl->y = y;
   pl->yhi = yhi;
   pl->ylo = ylo;
-  // the dy kernel stages [x][y][channels] (row = lane: conflict-free swizzle)
+  // staged [x][y][channels] (row = lane: conflict-free swizzle)
   auto omap = [&](CUtensorMap* m, void* p, bool half) -> int {
-    const CUtensorMapSwizzle sw = sw_for(ec * (half ? 2 : 4));
-    return pl->dy ? map_out_yx(m, p, half, pl->N, pl->W, pl->H, ec, sw)
-                  : map_act(m, p, half, pl->N, pl->W, pl->H, ec, bw, bh, sw);
+    return map_out_yx(m, p, half, pl->N, pl->W, pl->H, ec, sw_for(ec * (half ? 2 : 4)));
   };
   if (y) {
     N2F_TRY(omap(&pl->my, y, false));
     pl->omask |= kOutY;
   }
-  if (pl->f16) {
-    if (yhi) {
-      N2F_TRY(omap(&pl->myh, yhi, true));
-      pl->omask |= kOutHi;
-    }
-    if (ylo) {
-      N2F_TRY(omap(&pl->myl, ylo, true));
-      pl->omask |= kOutLo;
-    }
-  } else if (ylo) {
-    N2F_TRY(omap(&pl->myl, ylo, false));
+  if (yhi) {
+    N2F_TRY(omap(&pl->myh, yhi, true));
+    pl->omask |= kOutHi;
+  }
+  if (ylo) {
+    N2F_TRY(omap(&pl->myl, ylo, true));
     pl->omask |= kOutLo;
   }
   return N2F_OK;
 }
 
 int conv_tc_plan_maskbits(ConvTcPlan* pl, uint32_t* mbits_out, int mask_bits_in) {
-  if ((mbits_out || mask_bits_in) && pl->N < (pl->dy ? 64 : 128))
-    return fail(N2F_ERR_ARG, "bit-packed ReLU masks need N >= 128 (TMA epilogue), N=%d", pl->N);
+  if ((mbits_out || mask_bits_in) && pl->N < 64)
+    return fail(N2F_ERR_ARG, "bit-packed ReLU masks need N >= 64, N=%d", pl->N);
   pl->mbits_out = mbits_out;
   pl->mask_bits = mask_bits_in;
   return N2F_OK;
 }
 
+int conv_tc_plan_range(ConvTcPlan* pl, unsigned* amax) {
+  pl->amax = amax;
+  return N2F_OK;
+}
+
 int conv_tc_launch_head_train(const ConvTcPlan& pl, const float* bias, float* colsum,
                               const HeadTrainArgs& ht, cudaStream_t st) {
-  if (!pl.dy || pl.N != 256 || !(pl.omask & kOutHi) || !(pl.omask & kOutLo))
-    return fail(N2F_ERR_ARG, "fused training head needs the FP16 dy plan of L8 with a pair output");
+  if (pl.N != 256 || !(pl.omask & kOutHi) || !(pl.omask & kOutLo))
+    return fail(N2F_ERR_ARG, "fused training head needs the plan of L8 with a pair output");
   return launch_conv_dy<256, 1>(pl, bias, nullptr, colsum, kEpiBiasRelu, ht, HeadValArgs{}, st);
 }
 
 int conv_tc_launch_head_val(const ConvTcPlan& pl, const float* bias, const HeadValArgs& hv,
                             cudaStream_t st) {
-  if (!pl.dy || pl.N != 256) return fail(N2F_ERR_ARG, "fused validation head needs the FP16 dy plan of L8");
+  if (pl.N != 256) return fail(N2F_ERR_ARG, "fused validation head needs the plan of L8");
   return launch_conv_dy<256, 2>(pl, bias, nullptr, nullptr, kEpiBiasRelu, HeadTrainArgs{}, hv, st);
 }
 
 int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
                    cudaStream_t st) {
-  return pl.f16 ? launch_conv_tc_p<true>(pl, bias, mask, colsum, epi, st)
-                : launch_conv_tc_p<false>(pl, bias, mask, colsum, epi, st);
+  const HeadTrainArgs ht{};
+  const HeadValArgs hv{};
+  switch (pl.N) {
+    case 32: return launch_conv_dy<32, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
+    case 64: return launch_conv_dy<64, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
+    case 128: return launch_conv_dy<128, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
+    case 256: return launch_conv_dy<256, 0>(pl, bias, mask, colsum, epi, ht, hv, st);
+  }
+  return fail(N2F_ERR_ARG, "conv_tc_launch: N=%d", pl.N);
 }
-
-namespace {
-// CTA pairs for the wide wgrads (one 4-D activation box per stage and an even
-// split of the gradient channels); N2F_TC_CLUSTER=1 forces single CTAs
-int wgrad_cs(int cin, int cout) {
-  const char* cl = getenv("N2F_TC_CLUSTER");
-  return (cin % 128 == 0 && cout >= 128 && !(cl && atoi(cl) == 1)) ? 2 : 1;
-}
-}  // namespace
 
 int wgrad_tc_nsplit(int cin, int cout, int H, int W) {
   const int cs = wgrad_cs(cin, cout);
@@ -2207,8 +1333,7 @@ int wgrad_tc_nsplit(int cin, int cout, int H, int W) {
   const int nseg = ((W + kSegW - 1) / kSegW) * H;
   // narrow layers (N <= 64) fit two CTAs per SM: twice the splits keeps two
   // TMA pipelines in flight per SM (their short MMA stages are latency-bound)
-  const char* ws = getenv("N2F_WGRAD_PER_SM");
-  const int per_sm = ws ? atoi(ws) : (cout <= 64 ? 2 : 1);
+  const int per_sm = cout <= 64 ? 2 : 1;
   int n = per_sm * sm_count() / gridx;
   if (n < 1) n = 1;
   if (n > nseg) n = nseg;
@@ -2216,7 +1341,7 @@ int wgrad_tc_nsplit(int cin, int cout, int H, int W) {
 }
 
 int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H, int W, int C,
-                  int N, int nsplit, bool f16) {
+                  int N, int nsplit) {
   if (!tc_supported(C, N)) return fail(N2F_ERR_ARG, "wgrad_tc_plan: C=%d N=%d", C, N);
   N2F_TRY(set_attrs_once());
   pl->H = H;
@@ -2227,46 +1352,54 @@ int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H
   pl->cs = wgrad_cs(C, N);
   pl->gridx = pl->cs * ((pl->mblocks + pl->cs - 1) / pl->cs);
   pl->nsplit = nsplit;
-  pl->f16 = f16;
   pl->unscale = ldexpf(1.f, -(x.exp + g.exp));
-  const CUtensorMapSwizzle sw = f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
   // one TMA per operand part and stage: the 4 activation blocks of an M block
   // share a tap when C % 128 == 0 (else one box per block), the gradient's
   // N / 32 blocks always come as one box
   pl->xblk = C % 128 == 0;
-  // FP16 single-CTA wgrads take 64-pixel stages, 128 for C = 32 (N2F_WGRAD_SEG overrides)
-  const char* segenv = getenv("N2F_WGRAD_SEG");
-  // (C = 32 layers: 128-pixel stages halve the TMA instructions per pixel --
-  // their 4 per-tap activation boxes per part make them TMA-issue bound)
-  const int seg_default = (C == 32 && N <= 64) ? 128 : 64;
-  pl->seg = (f16 && pl->cs == 1) ? (segenv ? atoi(segenv) : seg_default) : kSegW;
-  if (pl->seg == 128 && N > 64) pl->seg = 64;
-  if (pl->seg != 32 && pl->seg != 64 && pl->seg != 128) pl->seg = kSegW;
+  // pixels per K stage: CTA pairs 32; single CTAs 64, or 128 for C = 32 with
+  // N <= 64 (their 4 per-tap activation boxes per part make them TMA-issue
+  // bound: 128-pixel stages halve the TMA instructions per pixel)
+  pl->seg = pl->cs == 2 ? kSegW : (C == 32 && N <= 64) ? 128 : 64;
   const int bpt = pl->xblk ? 4 : C / 32;  // activation blocks per box (one tap)
-  N2F_TRY(map_act_blk(&pl->mx, x.hi, f16, C, W, H, pl->seg, bpt, sw));
-  N2F_TRY(map_act_blk(&pl->mxl, x.lo, f16, C, W, H, pl->seg, bpt, sw));
-  N2F_TRY(map_act_blk(&pl->mg, g.hi, f16, N, W, H, pl->seg, N / 32 / pl->cs, sw));
-  N2F_TRY(map_act_blk(&pl->mgl, g.lo, f16, N, W, H, pl->seg, N / 32 / pl->cs, sw));
+  N2F_TRY(map_act_blk(&pl->mx, x.hi, C, W, H, pl->seg, bpt));
+  N2F_TRY(map_act_blk(&pl->mxl, x.lo, C, W, H, pl->seg, bpt));
+  N2F_TRY(map_act_blk(&pl->mg, g.hi, N, W, H, pl->seg, N / 32 / pl->cs));
+  N2F_TRY(map_act_blk(&pl->mgl, g.lo, N, W, H, pl->seg, N / 32 / pl->cs));
   return N2F_OK;
 }
 
 int wgrad_tc_launch(const WgradTcPlan& pl, float* part, cudaStream_t st) {
-  return pl.f16 ? launch_wgrad_tc_p<true>(pl, part, st) : launch_wgrad_tc_p<false>(pl, part, st);
+  if (pl.cs == 2) {
+    switch (pl.N) {
+      case 128: return launch_wgrad_tc_bn<128, 2, 32>(pl, part, st);
+      case 256: return launch_wgrad_tc_bn<256, 2, 32>(pl, part, st);
+    }
+  } else if (pl.seg == 128) {
+    switch (pl.N) {
+      case 32: return launch_wgrad_tc_bn<32, 1, 128>(pl, part, st);
+      case 64: return launch_wgrad_tc_bn<64, 1, 128>(pl, part, st);
+    }
+  } else {
+    switch (pl.N) {
+      case 32: return launch_wgrad_tc_bn<32, 1, 64>(pl, part, st);
+      case 64: return launch_wgrad_tc_bn<64, 1, 64>(pl, part, st);
+      case 128: return launch_wgrad_tc_bn<128, 1, 64>(pl, part, st);
+      case 256: return launch_wgrad_tc_bn<256, 1, 64>(pl, part, st);
+    }
+  }
+  return fail(N2F_ERR_ARG, "wgrad_tc_launch: N=%d cs=%d seg=%d", pl.N, pl.cs, pl.seg);
 }
 
-int split_lo(const float* x, float* lo, int64_t n, cudaStream_t st) {
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > 4096) blocks = 4096;
-  k_split_lo<<<(unsigned)blocks, 256, 0, st>>>(x, lo, n);
-  N2F_LAUNCH_CHECK();
-  return N2F_OK;
-}
-
-int split_f16(const float* x, void* hi, void* lo, int exp2, int64_t n, cudaStream_t st) {
+// fp16 operand pair of an fp32 tensor (init / set_params refresh of the
+// weights; parity entry points); folds max |x * 2^exp2| into amax (or null).
+int split_f16(const float* x, void* hi, void* lo, int exp2, int64_t n, cudaStream_t st,
+              unsigned* amax) {
   int64_t blocks = (n + 255) / 256;
   if (blocks > 4096) blocks = 4096;
   k_split_f16<<<(unsigned)blocks, 256, 0, st>>>(x, reinterpret_cast<__half*>(hi),
-                                                reinterpret_cast<__half*>(lo), ldexpf(1.f, exp2), n);
+                                                reinterpret_cast<__half*>(lo), ldexpf(1.f, exp2), n,
+                                                amax);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

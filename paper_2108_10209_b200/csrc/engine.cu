@@ -24,7 +24,6 @@ struct n2f_ctx {
   int H = 0, W = 0;
   n2f_config cfg{};
   cudaStream_t stream = nullptr;
-  int impl = kImplSimt;
 
   // geometry
   int ph[4]{}, pw[4]{};
@@ -48,15 +47,11 @@ struct n2f_ctx {
   int64_t poff[2 * kLayers]{};  // tensor offsets in the arena (w0,b0,w1,b1,...)
   int64_t pnum[2 * kLayers]{};
   int64_t ptotal = 0;
-  float* wt[kLayers]{};  // dgrad-transposed weights (layers 1..7)
-  float* act[kLayers]{};  // outputs of layers 0..7 for the training pass
+  float* wt[kLayers]{};  // dgrad-transposed weights (layers 1..7), fp32 master copy
   float* z = nullptr;     // logits of the last training step
-  float* gA = nullptr;
-  float* gB = nullptr;
-  float* vA = nullptr;
-  float* vB = nullptr;
+  float* gB = nullptr;    // L1 dgrad output (fp32: the first-layer wgrad input)
   float* ring = nullptr;
-  int nsplit[kLayers]{};
+  int nsplit0 = 0;  // pixel splits of the first-layer wgrad
   float* part_w[kLayers]{};
   float* part_b[kLayers]{};
   int nblk_head = 0, nblk_val = 0;
@@ -71,6 +66,8 @@ struct n2f_ctx {
   float* bc2 = nullptr;
   int table_len = 0;
   double* out_stage = nullptr;  // H*W f64 for the host API
+  unsigned* range_cur = nullptr;  // [kRangeSlots] this epoch's max |x * 2^e| (float bits)
+  float* range_hist = nullptr;    // [max_epochs][kRangeSlots]
 
   // host pinned mirrors
   double* h_mm = nullptr;
@@ -81,23 +78,11 @@ struct n2f_ctx {
   cudaGraphExec_t exec = nullptr;
   cudaGraphConditionalHandle handle = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  AdamArgs adam{};
   int64_t epoch_launches = 0;  // kernels in one captured epoch body
 
-  // tcgen05 path: tf32 residual companions of every tensor-core operand,
-  // TMA plans per (shape class, layer), Adam descriptors per shape class
-  bool tc = false;
-  float* params_lo = nullptr;
-  float* wt_lo[kLayers]{};
-  float* act_lo[kLayers]{};
-  float* gA_lo = nullptr;
-  float* gB_lo = nullptr;
-  float* vA_lo = nullptr;
-  float* vB_lo = nullptr;
-  // FP16 tensor-core mode (conv_impl 3): fp16 (hi, lo) pairs of the scaled
-  // operands replace the tf32 residuals; activations and weights carry
-  // 2^kExpAct / 2^kExpW, gradients 2^exp_g (see setup)
-  bool f16 = false;
+  // tcgen05 FP16x3 operands: fp16 (hi, lo) pairs of the scaled tensors;
+  // activations and weights carry 2^kExpAct / 2^kExpW, gradients 2^exp_g
+  // (see setup)
   int exp_g = 0;
   __half* w16[2] = {};            // hi, lo arenas (same layout as params)
   __half* wt16[2][kLayers] = {};  // dgrad-transposed pairs
@@ -109,7 +94,7 @@ struct n2f_ctx {
   ConvTcPlan dgrad_plan[2][kLayers]{};
   ConvTcPlan val_plan[kLayers]{};
   WgradTcPlan wgrad_plan[2][kLayers]{};
-  AdamArgs adam_sc[2]{};
+  AdamArgs adam_sc[2]{};  // per training-plane shape class
   // profiling
   struct Mark {
     int cls, li;
@@ -120,7 +105,6 @@ struct n2f_ctx {
   std::vector<Mark> marks;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
-  int bias_tiles[2]{};
   int wsplit[2][kLayers]{};
   int last_sc = 0;  // shape class of the last enqueued step (parity readback)
 };
@@ -138,20 +122,9 @@ int dalloc(n2f_ctx* c, T** p, size_t count) {
   return N2F_OK;
 }
 
-int nblocks_for(int64_t pixels, int per_block) {
-  int64_t n = (pixels + per_block - 1) / per_block;
-  if (n > 148 * 8) n = 148 * 8;
-  if (n < 1) n = 1;
-  return (int)n;
-}
-
 const float* W_(n2f_ctx* c, int li) { return c->params + c->poff[2 * li]; }
 const float* B_(n2f_ctx* c, int li) { return c->params + c->poff[2 * li + 1]; }
-
-int conv3x3(n2f_ctx* c, const float* x, const float* wk, const float* bias, const float* mask,
-            float* y, int h, int w, int cin, int cout, int epi) {
-  return conv3x3_simt(x, wk, bias, mask, y, h, w, cin, cout, epi, c->stream);
-}
+unsigned* RS_(n2f_ctx* c, int cls, int li) { return c->range_cur + cls * kLayers + li; }
 
 // training-plane shape class of pair k (checkerboard: up pairs 0,1 vs left 2,3)
 int shape_class(const n2f_ctx* c, int k) {
@@ -192,10 +165,13 @@ cudaEvent_t prof_event(n2f_ctx* c) {
 
 double conv_flop(int64_t P, int li) { return 2.0 * P * kCout[li] * kKsz[li] * kKsz[li] * kCin[li]; }
 
-// tcgen05 variant of a training step: L2..L8 forward and dgrad on the tensor
-// cores (3xTF32), bias gradients as fused column sums of each layer's
-// pre-activation gradient, wgrad still on the SIMT kernels.
-int enqueue_step_tc(n2f_ctx* c, int k) {
+// One training step on pair k (model.forward / _loss_and_grad / backward /
+// apply_gradients, model.py:72-120, trainer.py:184-190): L1 forward, L2..L8
+// forward on the tensor cores (L8 with the L9 head, loss and head backward
+// fused), then per layer L8..L2 the wgrad (split-K partials) and the masked
+// dgrad (whose epilogue also writes the bias-gradient column sums of the
+// layer below), the L1 wgrad, and Adam (reducing every partial in fixed order).
+int enqueue_step(n2f_ctx* c, int k) {
   cudaStream_t st = c->stream;
   const int sc = shape_class(c, k);
   c->last_sc = sc;
@@ -203,126 +179,44 @@ int enqueue_step_tc(n2f_ctx* c, int k) {
   const int64_t P = (int64_t)h * w;
   const float* x0 = c->pin + k * c->plane;
   const float* tgt = c->ptgt + k * c->plane;
-  const bool f16 = c->f16;
-  const float sg = ldexpf(1.f, c->exp_g);
-  if (f16) {
-    PROF(kPFirst, 0, conv_flop(P, 0),
-         conv_first_simt(x0, W_(c, 0), B_(c, 0), nullptr, h, w, kCout[0], st, 1, nullptr,
-                         c->act16[0][0], c->act16[1][0], ldexpf(1.f, kExpAct)));
-  } else {
-    PROF(kPFirst, 0, conv_flop(P, 0),
-         conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st, 1, c->act_lo[0]));
-  }
-  for (int li = 1; li < (f16 ? 7 : 8); ++li)
+  PROF(kPFirst, 0, conv_flop(P, 0),
+       conv_first_simt(x0, W_(c, 0), B_(c, 0), nullptr, h, w, kCout[0], st, 1, c->act16[0][0],
+                       c->act16[1][0], ldexpf(1.f, kExpAct), RS_(c, kRangeAct, 0)));
+  for (int li = 1; li < 7; ++li)
     PROF(kPFwd, li, conv_flop(P, li),
          conv_tc_launch(c->fwd_plan[sc][li], B_(c, li), nullptr, nullptr, kEpiBiasRelu, st));
-  if (f16) {  // L8 forward with the L9 head, loss and head backward fused
-    HeadTrainArgs ht{W_(c, 8), B_(c, 8), tgt, c->z, c->part_w[8], c->part_b[8],
-                     c->part_loss + (int64_t)k * c->nblk_head, c->step_counter, c->cfg.loss,
-                     (float)P, (float)(2.0 / (double)P)};
-    PROF(kPFwd, 7, conv_flop(P, 7) + 6.0 * P * kMaxC,
-         conv_tc_launch_head_train(c->fwd_plan[sc][7], B_(c, 7), c->part_b[7], ht, st));
-  } else {
-    PROF(kPHead, 8, 6.0 * P * kMaxC,
-         launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, c->gA, c->part_w[8], c->part_b[8],
-                           c->part_loss + (int64_t)k * c->nblk_head, c->z, P, c->nblk_head,
-                           c->cfg.loss, c->step_counter, st, c->gA_lo, c->part_b[7]));
-  }
-  float* g = c->gA;
-  float* gn = c->gB;
+  HeadTrainArgs ht{W_(c, 8), B_(c, 8), tgt, c->z, c->part_w[8], c->part_b[8],
+                   c->part_loss + (int64_t)k * c->nblk_head, c->step_counter, c->cfg.loss,
+                   (float)P, (float)(2.0 / (double)P)};
+  PROF(kPFwd, 7, conv_flop(P, 7) + 6.0 * P * kMaxC,
+       conv_tc_launch_head_train(c->fwd_plan[sc][7], B_(c, 7), c->part_b[7], ht, st));
   for (int li = 7; li >= 1; --li) {
     PROF(kPWgrad, li, conv_flop(P, li), wgrad_tc_launch(c->wgrad_plan[sc][li], c->part_w[li], st));
-    const void* mask = c->mbits[li - 1] ? (const void*)c->mbits[li - 1]
-                       : f16 ? (const void*)c->act16[0][li - 1] : (const void*)c->act[li - 1];
+    const void* mask = c->mbits[li - 1] ? (const void*)c->mbits[li - 1] : (const void*)c->act16[0][li - 1];
     PROF(kPDgrad, li, conv_flop(P, li),
          conv_tc_launch(c->dgrad_plan[sc][li], nullptr, mask, li > 1 ? c->part_b[li - 1] : nullptr,
                         kEpiMask, st));
-    float* t = g;
-    g = gn;
-    gn = t;
   }
   PROF(kPWgradFirst, 0, conv_flop(P, 0),
-       wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
+       wgrad_first_simt(c->gB, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit0, st));
   PROF(kPAdam, 0, 0.0, launch_adam(c->adam_sc[sc], c->step_counter, 0, st));
   return N2F_OK;
 }
 
-int enqueue_validate_tc(n2f_ctx* c) {
+// Full-resolution validation (trainer.validate -> model.predict, trainer.py:97-101,
+// model.py:123-140): forward with the head fused into L8 (sigmoid, clip, ring
+// slot, squared-error partials).
+int enqueue_validate(n2f_ctx* c) {
   cudaStream_t st = c->stream;
-  const bool f16 = c->f16;
-  if (f16) {
-    PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
-         conv_first_simt(c->norm, W_(c, 0), B_(c, 0), nullptr, c->H, c->W, kCout[0], st, 1, nullptr,
-                         c->v16[0][0], c->v16[0][1], ldexpf(1.f, kExpAct)));
-  } else {
-    PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
-         conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, c->H, c->W, kCout[0], st, 1,
-                         c->vA_lo));
-  }
-  for (int li = 1; li < (f16 ? 7 : 8); ++li)
+  PROF(kPValFirst, 0, conv_flop(c->Pv, 0),
+       conv_first_simt(c->norm, W_(c, 0), B_(c, 0), nullptr, c->H, c->W, kCout[0], st, 1,
+                       c->v16[0][0], c->v16[0][1], ldexpf(1.f, kExpAct), RS_(c, kRangeValAct, 0)));
+  for (int li = 1; li < 7; ++li)
     PROF(kPValConv, li, conv_flop(c->Pv, li),
          conv_tc_launch(c->val_plan[li], B_(c, li), nullptr, nullptr, kEpiBiasRelu, st));
-  if (f16) {  // L8 with the validation head fused
-    HeadValArgs hv{W_(c, 8), B_(c, 8), c->norm, c->ring, c->dstate, c->cfg.avg_window, c->part_se};
-    PROF(kPValConv, 7, conv_flop(c->Pv, 7) + 2.0 * c->Pv * kMaxC,
-         conv_tc_launch_head_val(c->val_plan[7], B_(c, 7), hv, st));
-  } else {
-    // layer 7 (odd) wrote vB
-    PROF(kPHeadVal, 8, 2.0 * c->Pv * kMaxC,
-         launch_head_val(c->vB, W_(c, 8), B_(c, 8), c->norm, c->ring, c->Pv, c->nblk_val, c->dstate,
-                         c->cfg.avg_window, c->part_se, st));
-  }
-  return N2F_OK;
-}
-
-// One training step on pair k: forward, fused head/loss/head-backward,
-// backward through L8..L1 (wgrad partials + masked dgrad), Adam.
-int enqueue_step(n2f_ctx* c, int k) {
-  if (c->tc) return enqueue_step_tc(c, k);
-  cudaStream_t st = c->stream;
-  const int h = c->ph[k], w = c->pw[k];
-  const int64_t P = (int64_t)h * w;
-  const float* x0 = c->pin + k * c->plane;
-  const float* tgt = c->ptgt + k * c->plane;
-  N2F_TRY(conv_first_simt(x0, W_(c, 0), B_(c, 0), c->act[0], h, w, kCout[0], st));
-  for (int li = 1; li < 8; ++li)
-    N2F_TRY(conv3x3(c, c->act[li - 1], W_(c, li), B_(c, li), nullptr, c->act[li], h, w, kCin[li],
-                    kCout[li], kEpiBiasRelu));
-  N2F_TRY(launch_head_train(c->act[7], W_(c, 8), B_(c, 8), tgt, c->gA, c->part_w[8], c->part_b[8],
-                            c->part_loss + (int64_t)k * c->nblk_head, c->z, P, c->nblk_head,
-                            c->cfg.loss, c->step_counter, st));
-  float* g = c->gA;
-  float* gn = c->gB;
-  for (int li = 7; li >= 1; --li) {
-    N2F_TRY(wgrad3x3_simt(g, c->act[li - 1], c->part_w[li], c->part_b[li], h, w, kCin[li],
-                          kCout[li], c->nsplit[li], st));
-    N2F_TRY(conv3x3(c, g, c->wt[li], nullptr, c->act[li - 1], gn, h, w, kCout[li], kCin[li],
-                    kEpiMask));
-    float* t = g;
-    g = gn;
-    gn = t;
-  }
-  N2F_TRY(wgrad_first_simt(g, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit[0], st));
-  N2F_TRY(launch_adam(c->adam, c->step_counter, 0, st));
-  return N2F_OK;
-}
-
-// Full-resolution validation forward + head (writes the ring slot + se partials).
-int enqueue_validate(n2f_ctx* c) {
-  if (c->tc) return enqueue_validate_tc(c);
-  cudaStream_t st = c->stream;
-  const int h = c->H, w = c->W;
-  N2F_TRY(conv_first_simt(c->norm, W_(c, 0), B_(c, 0), c->vA, h, w, kCout[0], st));
-  float* a = c->vA;
-  float* b = c->vB;
-  for (int li = 1; li < 8; ++li) {
-    N2F_TRY(conv3x3(c, a, W_(c, li), B_(c, li), nullptr, b, h, w, kCin[li], kCout[li], kEpiBiasRelu));
-    float* t = a;
-    a = b;
-    b = t;
-  }
-  N2F_TRY(launch_head_val(a, W_(c, 8), B_(c, 8), c->norm, c->ring, c->Pv, c->nblk_val, c->dstate,
-                          c->cfg.avg_window, c->part_se, st));
+  HeadValArgs hv{W_(c, 8), B_(c, 8), c->norm, c->ring, c->dstate, c->cfg.avg_window, c->part_se};
+  PROF(kPValConv, 7, conv_flop(c->Pv, 7) + 2.0 * c->Pv * kMaxC,
+       conv_tc_launch_head_val(c->val_plan[7], B_(c, 7), hv, st));
   return N2F_OK;
 }
 
@@ -333,7 +227,8 @@ int enqueue_epoch(n2f_ctx* c, int use_handle) {
   PROF(kPStop, 0, 0.0,
        launch_stop(c->dstate, c->part_se, c->nblk_val, (double)c->Pv, c->part_loss, c->nblk_head,
                    pt, c->val_hist, c->loss_hist, c->time_hist, c->cfg.patience_epochs,
-                   c->cfg.max_epochs, c->handle, use_handle, c->stream));
+                   c->cfg.max_epochs, c->range_cur, c->range_hist, c->handle, use_handle,
+                   c->stream));
   return N2F_OK;
 }
 
@@ -420,158 +315,113 @@ int setup(n2f_ctx* c) {
   N2F_TRY(dalloc(c, &c->m, off));
   N2F_TRY(dalloc(c, &c->v, off));
   for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt[li], c->pnum[2 * li]));
-  // FP16x3 keeps layer outputs as fp16 operand pairs (allocated below) and
-  // fuses the L9 head into L8's epilogue; the only fp32 layer buffer left is
-  // the L1 dgrad output (the SIMT first-layer wgrad)
-  const bool f16 = c->f16;
-  if (!f16)
-    for (int li = 0; li < 8; ++li) N2F_TRY(dalloc(c, &c->act[li], c->Pt * kCout[li]));
+  // layer outputs live as fp16 operand pairs (below) and the L9 head is fused
+  // into L8's epilogue; the only fp32 layer buffer is the L1 dgrad output
   N2F_TRY(dalloc(c, &c->z, c->Pt));
-  if (!f16) N2F_TRY(dalloc(c, &c->gA, c->Pt * kMaxC));
-  N2F_TRY(dalloc(c, &c->gB, c->Pt * (f16 ? kCout[0] : kMaxC)));
-  if (!f16) N2F_TRY(dalloc(c, &c->vA, c->Pv * kMaxC));
-  if (!f16) N2F_TRY(dalloc(c, &c->vB, c->Pv * kMaxC));
+  N2F_TRY(dalloc(c, &c->gB, c->Pt * kCout[0]));
   N2F_TRY(dalloc(c, &c->ring, (int64_t)c->cfg.avg_window * c->Pv));
+  N2F_TRY(dalloc(c, &c->range_cur, kRangeSlots));
+  N2F_CUDA(cudaMemset(c->range_cur, 0, kRangeSlots * sizeof(unsigned)));
+  N2F_TRY(dalloc(c, &c->range_hist, (int64_t)c->cfg.max_epochs * kRangeSlots));
 
-  c->nblk_head = nblocks_for(c->Pt, 64);
-  c->nblk_val = nblocks_for(c->Pv, 64);
-  for (int li = 0; li < 8; ++li) c->nsplit[li] = wgrad_nsplit(c->Pt, kCin[li], kCout[li]);
-  c->nsplit[8] = c->nblk_head;
-  // TC mode: the bias gradient of layer li (1..6) is a per-tile column sum
-  // written by the dgrad of layer li+1, L8's by the fused head
-  int tiles[2] = {conv_tc_tiles(c->ph[0], c->pw[0]), conv_tc_tiles(c->ph[2], c->pw[2])};
+  // split-K partial buffers: the bias gradient of layer li (1..6) is a
+  // per-tile column sum written by the dgrad of layer li+1, L8's by the fused
+  // head; weight gradients use the tcgen05 wgrad's split count
+  c->nsplit0 = wgrad_first_nsplit(c->Pt);
+  const int tiles[2] = {conv_tc_tiles(c->ph[0], c->pw[0]), conv_tc_tiles(c->ph[2], c->pw[2])};
   const int max_tiles = tiles[0] > tiles[1] ? tiles[0] : tiles[1];
-  int wsplit[2][kLayers] = {};  // tcgen05 wgrad split-K per shape class
   for (int sc = 0; sc < 2; ++sc)
-    for (int li = 1; li < 8; ++li) wsplit[sc][li] = wgrad_tc_nsplit(kCin[li], kCout[li], c->ph[2 * sc], c->pw[2 * sc]);
+    for (int li = 1; li < 8; ++li)
+      c->wsplit[sc][li] = wgrad_tc_nsplit(kCin[li], kCout[li], c->ph[2 * sc], c->pw[2 * sc]);
   for (int li = 0; li < kLayers; ++li) {
-    int64_t nb = c->nsplit[li], nw = c->nsplit[li];
-    if (c->tc && li >= 1 && li <= 7 && max_tiles > nb) nb = max_tiles;
-    if (c->tc && li == 7 && c->nblk_head > nb) nb = c->nblk_head;
-    if (f16 && li == 8) {  // fused head: per-tile db9, per-(tile, warp group) dW9
+    int64_t nb, nw;
+    if (li == 0) {
+      nb = nw = c->nsplit0;
+    } else if (li == 8) {  // fused head: per-tile db9, per-(tile, warp group) dW9
       nb = max_tiles;
       nw = 4 * (int64_t)max_tiles;
-    }
-    if (c->tc && li >= 1 && li <= 7) {
-      nw = wsplit[0][li] > wsplit[1][li] ? wsplit[0][li] : wsplit[1][li];
-      if (c->nsplit[li] > nw) nw = c->nsplit[li];
+    } else {
+      nb = max_tiles;
+      nw = c->wsplit[0][li] > c->wsplit[1][li] ? c->wsplit[0][li] : c->wsplit[1][li];
     }
     N2F_TRY(dalloc(c, &c->part_w[li], nw * c->pnum[2 * li]));
     N2F_TRY(dalloc(c, &c->part_b[li], nb * c->pnum[2 * li + 1]));
   }
-  if (c->tc && !c->f16) {
-    N2F_TRY(dalloc(c, &c->params_lo, c->ptotal));
-    for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt_lo[li], c->pnum[2 * li]));
-    for (int li = 0; li < 7; ++li) N2F_TRY(dalloc(c, &c->act_lo[li], c->Pt * kCout[li]));
-    N2F_TRY(dalloc(c, &c->gA_lo, c->Pt * kMaxC));
-    N2F_TRY(dalloc(c, &c->gB_lo, c->Pt * kMaxC));
-    N2F_TRY(dalloc(c, &c->vA_lo, c->Pv * kMaxC));
-    N2F_TRY(dalloc(c, &c->vB_lo, c->Pv * kMaxC));
-  }
-  if (c->f16) {
-    // gradient scale: |dL/dz| <= 1/P per pixel, so 2^ceil(log2 P) lifts the
-    // head gradient to O(1); kExpAct more keeps small entries out of the
-    // fp16 subnormal range
-    int lg = 0;
-    while ((int64_t(1) << lg) < c->Pt) ++lg;
-    c->exp_g = lg + kExpAct;
-    for (int q = 0; q < 2; ++q) {
-      N2F_TRY(dalloc(c, &c->w16[q], c->ptotal));
-      for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt16[q][li], c->pnum[2 * li]));
-      for (int li = 0; li < 7; ++li) N2F_TRY(dalloc(c, &c->act16[q][li], c->Pt * kCout[li]));
-      for (int ab = 0; ab < 2; ++ab) {
-        N2F_TRY(dalloc(c, &c->g16[ab][q], c->Pt * kMaxC));
-        N2F_TRY(dalloc(c, &c->v16[ab][q], c->Pv * kMaxC));
-      }
+  // gradient scale: |dL/dz| <= 1/P per pixel, so 2^ceil(log2 P) lifts the
+  // head gradient to O(1); kExpAct more keeps small entries out of the
+  // fp16 subnormal range
+  int lg = 0;
+  while ((int64_t(1) << lg) < c->Pt) ++lg;
+  c->exp_g = lg + kExpAct;
+  for (int q = 0; q < 2; ++q) {
+    N2F_TRY(dalloc(c, &c->w16[q], c->ptotal));
+    for (int li = 1; li < 8; ++li) N2F_TRY(dalloc(c, &c->wt16[q][li], c->pnum[2 * li]));
+    for (int li = 0; li < 7; ++li) N2F_TRY(dalloc(c, &c->act16[q][li], c->Pt * kCout[li]));
+    for (int ab = 0; ab < 2; ++ab) {
+      N2F_TRY(dalloc(c, &c->g16[ab][q], c->Pt * kMaxC));
+      N2F_TRY(dalloc(c, &c->v16[ab][q], c->Pv * kMaxC));
     }
   }
-  if (c->tc) {
-    const bool f16 = c->f16;
-    // operand pairs of layer li's input activation, its weights (forward and
-    // dgrad-transposed) and the gradient buffer A (ab 0) or B (ab 1)
-    auto act_op = [&](int li) -> TcOperand {
-      return f16 ? TcOperand{c->act16[0][li], c->act16[1][li], kExpAct}
-                 : TcOperand{c->act[li], c->act_lo[li], 0};
-    };
-    auto w_op = [&](int li) -> TcOperand {
-      const int64_t o = c->poff[2 * li];
-      return f16 ? TcOperand{c->w16[0] + o, c->w16[1] + o, kExpW}
-                 : TcOperand{c->params + o, c->params_lo + o, 0};
-    };
-    auto wt_op = [&](int li) -> TcOperand {
-      return f16 ? TcOperand{c->wt16[0][li], c->wt16[1][li], kExpW}
-                 : TcOperand{c->wt[li], c->wt_lo[li], 0};
-    };
-    auto g_op = [&](int ab) -> TcOperand {
-      if (f16) return TcOperand{c->g16[ab][0], c->g16[ab][1], c->exp_g};
-      return ab ? TcOperand{c->gB, c->gB_lo, 0} : TcOperand{c->gA, c->gA_lo, 0};
-    };
-    auto v_op = [&](int ab) -> TcOperand {
-      if (f16) return TcOperand{c->v16[ab][0], c->v16[ab][1], kExpAct};
-      return ab ? TcOperand{c->vB, c->vB_lo, 0} : TcOperand{c->vA, c->vA_lo, 0};
-    };
-    const float sa = ldexpf(1.f, kExpAct), sg = ldexpf(1.f, c->exp_g);
-    // wide forward outputs feeding a wide dgrad also emit bit-packed ReLU masks
-    for (int li = 1; li < 7; ++li)
-      if (kCout[li] >= 128) N2F_TRY(dalloc(c, &c->mbits[li], c->Pt * (kCout[li] / 32)));
-    for (int sc = 0; sc < 2; ++sc) {
-      const int h = c->ph[2 * sc], w = c->pw[2 * sc];
-      for (int li = 1; li < 8; ++li) {
-        ConvTcPlan& fp = c->fwd_plan[sc][li];
-        N2F_TRY(conv_tc_plan(&fp, act_op(li - 1), w_op(li), h, w, kCin[li], kCout[li], f16));
-        // forward outputs: the operand pair of the next layer; L8: fp32 for the
-        // head (TF32) or, with the head fused (FP16), the L8 gradient pair
-        if (li == 7 && f16)
-          N2F_TRY(conv_tc_plan_out(&fp, nullptr, c->g16[0][0], c->g16[0][1], sg));
-        else if (li == 7)
-          N2F_TRY(conv_tc_plan_out(&fp, c->act[7], nullptr, nullptr, sa));
-        else if (f16)
-          N2F_TRY(conv_tc_plan_out(&fp, nullptr, c->act16[0][li], c->act16[1][li], sa));
-        else
-          N2F_TRY(conv_tc_plan_out(&fp, c->act[li], nullptr, c->act_lo[li], sa));
-        if (c->mbits[li]) N2F_TRY(conv_tc_plan_maskbits(&fp, c->mbits[li], 0));
-        const int ab = (li & 1) ? 0 : 1;  // L8 (li 7) reads gA (head output), then alternate
-        N2F_TRY(conv_tc_plan(&c->dgrad_plan[sc][li], g_op(ab), wt_op(li), h, w, kCout[li],
-                             kCin[li], f16));
-        // dgrad output: the buffer this layer does not read (B when li is odd);
-        // L1's feeds the SIMT first-layer wgrad in fp32
-        const int nb = 1 - ab;
-        float* gf = nb ? c->gB : c->gA;
-        if (li == 1)
-          N2F_TRY(conv_tc_plan_out(&c->dgrad_plan[sc][li], gf, nullptr, nullptr, sg));
-        else if (f16)
-          N2F_TRY(conv_tc_plan_out(&c->dgrad_plan[sc][li], nullptr, c->g16[nb][0], c->g16[nb][1], sg));
-        else
-          N2F_TRY(conv_tc_plan_out(&c->dgrad_plan[sc][li], gf, nullptr, nb ? c->gB_lo : c->gA_lo, sg));
-        if (c->mbits[li - 1]) N2F_TRY(conv_tc_plan_maskbits(&c->dgrad_plan[sc][li], nullptr, 1));
-        N2F_TRY(wgrad_tc_plan(&c->wgrad_plan[sc][li], act_op(li - 1), g_op(ab), h, w, kCin[li],
-                              kCout[li], wsplit[sc][li], f16));
-      }
-    }
-    for (int sc = 0; sc < 2; ++sc)
-      for (int li = 1; li < 8; ++li) c->wsplit[sc][li] = wsplit[sc][li];
+  // operand pairs of layer li's input activation, its weights (forward and
+  // dgrad-transposed) and the gradient buffer A (ab 0) or B (ab 1)
+  auto act_op = [&](int li) { return TcOperand{c->act16[0][li], c->act16[1][li], kExpAct}; };
+  auto w_op = [&](int li) {
+    const int64_t o = c->poff[2 * li];
+    return TcOperand{c->w16[0] + o, c->w16[1] + o, kExpW};
+  };
+  auto wt_op = [&](int li) { return TcOperand{c->wt16[0][li], c->wt16[1][li], kExpW}; };
+  auto g_op = [&](int ab) { return TcOperand{c->g16[ab][0], c->g16[ab][1], c->exp_g}; };
+  auto v_op = [&](int ab) { return TcOperand{c->v16[ab][0], c->v16[ab][1], kExpAct}; };
+  const float sa = ldexpf(1.f, kExpAct), sg = ldexpf(1.f, c->exp_g);
+  // wide forward outputs feeding a wide dgrad also emit bit-packed ReLU masks
+  for (int li = 1; li < 7; ++li)
+    if (kCout[li] >= 128) N2F_TRY(dalloc(c, &c->mbits[li], c->Pt * (kCout[li] / 32)));
+  for (int sc = 0; sc < 2; ++sc) {
+    const int h = c->ph[2 * sc], w = c->pw[2 * sc];
     for (int li = 1; li < 8; ++li) {
-      const int ab = (li & 1) ? 0 : 1;  // L1 writes vA; layer li reads vA when li is odd
-      N2F_TRY(conv_tc_plan(&c->val_plan[li], v_op(ab), w_op(li), c->H, c->W, kCin[li], kCout[li],
-                           f16));
-      const int ob = 1 - ab;  // layer li writes vB when odd
-      float* vf = ob ? c->vB : c->vA;
-      if (li == 7 && f16)
-        N2F_TRY(conv_tc_plan_out(&c->val_plan[li], nullptr, nullptr, nullptr, sa));  // fused head
-      else if (li == 7)
-        N2F_TRY(conv_tc_plan_out(&c->val_plan[li], vf, nullptr, nullptr, sa));
-      else if (f16)
-        N2F_TRY(conv_tc_plan_out(&c->val_plan[li], nullptr, c->v16[ob][0], c->v16[ob][1], sa));
-      else
-        N2F_TRY(conv_tc_plan_out(&c->val_plan[li], vf, nullptr, ob ? c->vB_lo : c->vA_lo, sa));
+      // forward: outputs are the next layer's operand pair; L8 (head fused)
+      // writes the L8 gradient pair (the dgrad/wgrad input)
+      ConvTcPlan& fp = c->fwd_plan[sc][li];
+      N2F_TRY(conv_tc_plan(&fp, act_op(li - 1), w_op(li), h, w, kCin[li], kCout[li]));
+      if (li == 7) {
+        N2F_TRY(conv_tc_plan_out(&fp, nullptr, c->g16[0][0], c->g16[0][1], sg));
+        N2F_TRY(conv_tc_plan_range(&fp, RS_(c, kRangeGrad, 7)));
+      } else {
+        N2F_TRY(conv_tc_plan_out(&fp, nullptr, c->act16[0][li], c->act16[1][li], sa));
+        N2F_TRY(conv_tc_plan_range(&fp, RS_(c, kRangeAct, li)));
+      }
+      if (c->mbits[li]) N2F_TRY(conv_tc_plan_maskbits(&fp, c->mbits[li], 0));
+      // dgrad: reads gradient buffer ab (L8's is A, the head output), writes
+      // the other; L1's output feeds the first-layer wgrad in fp32
+      const int ab = (li & 1) ? 0 : 1;
+      ConvTcPlan& dp = c->dgrad_plan[sc][li];
+      N2F_TRY(conv_tc_plan(&dp, g_op(ab), wt_op(li), h, w, kCout[li], kCin[li]));
+      const int nb = 1 - ab;
+      if (li == 1) {
+        N2F_TRY(conv_tc_plan_out(&dp, c->gB, nullptr, nullptr, sg));
+      } else {
+        N2F_TRY(conv_tc_plan_out(&dp, nullptr, c->g16[nb][0], c->g16[nb][1], sg));
+        N2F_TRY(conv_tc_plan_range(&dp, RS_(c, kRangeGrad, li - 1)));
+      }
+      if (c->mbits[li - 1]) N2F_TRY(conv_tc_plan_maskbits(&dp, nullptr, 1));
+      N2F_TRY(wgrad_tc_plan(&c->wgrad_plan[sc][li], act_op(li - 1), g_op(ab), h, w, kCin[li],
+                            kCout[li], c->wsplit[sc][li]));
     }
-    c->bias_tiles[0] = tiles[0];
-    c->bias_tiles[1] = tiles[1];
   }
-  if (f16) {  // fused heads write one loss / squared-error partial per tile
-    c->nblk_head = max_tiles;
-    c->nblk_val = c->val_plan[7].tiles;
+  for (int li = 1; li < 8; ++li) {
+    const int ab = (li & 1) ? 0 : 1;  // L1 writes vA; layer li reads vA when li is odd
+    ConvTcPlan& vp = c->val_plan[li];
+    N2F_TRY(conv_tc_plan(&vp, v_op(ab), w_op(li), c->H, c->W, kCin[li], kCout[li]));
+    if (li == 7) {
+      N2F_TRY(conv_tc_plan_out(&vp, nullptr, nullptr, nullptr, sa));  // fused head
+    } else {
+      N2F_TRY(conv_tc_plan_out(&vp, nullptr, c->v16[1 - ab][0], c->v16[1 - ab][1], sa));
+      N2F_TRY(conv_tc_plan_range(&vp, RS_(c, kRangeValAct, li)));
+    }
   }
+  // the fused heads write one loss / squared-error partial per tile
+  c->nblk_head = max_tiles;
+  c->nblk_val = c->val_plan[7].tiles;
   N2F_TRY(dalloc(c, &c->part_loss, 4 * (int64_t)c->nblk_head));
   N2F_TRY(dalloc(c, &c->part_se, c->nblk_val));
   // a shape class with fewer tiles leaves its tail of the loss partials at 0
@@ -599,7 +449,7 @@ int setup(n2f_ctx* c) {
   N2F_CUDA(cudaMemcpy(c->bc1, t1.data(), t1.size() * 4, cudaMemcpyHostToDevice));
   N2F_CUDA(cudaMemcpy(c->bc2, t2.data(), t2.size() * 4, cudaMemcpyHostToDevice));
 
-  AdamArgs& a = c->adam;
+  AdamArgs a{};
   a.ntensors = 2 * kLayers;
   a.total = c->ptotal;
   a.p = c->params;
@@ -614,53 +464,43 @@ int setup(n2f_ctx* c) {
   a.one_minus_beta2 = (float)(1.0 - 0.999);
   a.lr = (float)c->cfg.lr;
   a.eps = 1e-8f;
+  a.phi16 = c->w16[0];
+  a.plo16 = c->w16[1];
+  a.wscale = ldexpf(1.f, kExpW);
   for (int li = 0; li < kLayers; ++li) {
     for (int q = 0; q < 2; ++q) {
       AdamTensor& T = a.t[2 * li + q];
       T.off = c->poff[2 * li + q];
       T.n = c->pnum[2 * li + q];
       T.part = q == 0 ? c->part_w[li] : c->part_b[li];
-      T.nsplit = c->nsplit[li];
-      T.wt = (q == 0 && li >= 1 && li <= 7) ? c->wt[li] : nullptr;
+      T.wt = nullptr;
       T.cin = kCin[li];
       T.cout = kCout[li];
     }
   }
-  if (c->tc) {
-    a.plo = c->params_lo;
-    a.phi16 = c->w16[0];
-    a.plo16 = c->w16[1];
-    a.wscale = ldexpf(1.f, kExpW);
-    for (int li = 1; li < 8; ++li) {
-      AdamTensor& T = a.t[2 * li];
-      if (c->f16) {
-        T.want16 = 1;
-        T.wt = nullptr;  // the FP16 path reads only the fp16 pair of wt
-        T.wth16 = c->wt16[0][li];
-        T.wtl16 = c->wt16[1][li];
-      } else {
-        T.want_lo = 1;
-        T.wtlo = c->wt_lo[li];
-      }
-    }
-    // bias gradients of layers 1..7 are per-tile column sums (dgrad epilogue,
-    // head); weights use the tcgen05 wgrad's split count
-    for (int sc = 0; sc < 2; ++sc) {
-      c->adam_sc[sc] = a;
-      for (int li = 1; li <= 7; ++li) {
-        c->adam_sc[sc].t[2 * li + 1].nsplit =
-            li == 7 ? (f16 ? c->fwd_plan[sc][7].tiles : c->nblk_head) : c->dgrad_plan[sc][li + 1].tiles;
-        c->adam_sc[sc].t[2 * li].nsplit = c->wsplit[sc][li];
-      }
-      if (f16) {  // the head's partials come from the fused L8 epilogue
-        c->adam_sc[sc].t[16].nsplit = 4 * c->fwd_plan[sc][7].tiles;
-        c->adam_sc[sc].t[17].nsplit = c->fwd_plan[sc][7].tiles;
-      }
-    }
+  // tcgen05 weights (layers 1..7): Adam also writes their fp16 pairs (the
+  // forward operand and the dgrad-transposed one) from the same registers
+  for (int li = 1; li < 8; ++li) {
+    AdamTensor& T = a.t[2 * li];
+    T.want16 = 1;
+    T.amax = RS_(c, kRangeWeight, li);
+    T.wth16 = c->wt16[0][li];
+    T.wtl16 = c->wt16[1][li];
   }
-  N2F_TRY(plan_adam(c, c->adam));
-  if (c->tc) {
-    for (int sc = 0; sc < 2; ++sc) N2F_TRY(plan_adam(c, c->adam_sc[sc]));
+  // split counts per shape class: bias gradients of layers 1..7 are per-tile
+  // column sums (dgrad epilogue of the layer above; L8's from the head), the
+  // head's partials come from the fused L8 epilogue
+  for (int sc = 0; sc < 2; ++sc) {
+    AdamArgs& as = c->adam_sc[sc];
+    as = a;
+    as.t[0].nsplit = as.t[1].nsplit = c->nsplit0;
+    for (int li = 1; li <= 7; ++li) {
+      as.t[2 * li].nsplit = c->wsplit[sc][li];
+      as.t[2 * li + 1].nsplit = li == 7 ? c->fwd_plan[sc][7].tiles : c->dgrad_plan[sc][li + 1].tiles;
+    }
+    as.t[16].nsplit = 4 * c->fwd_plan[sc][7].tiles;
+    as.t[17].nsplit = c->fwd_plan[sc][7].tiles;
+    N2F_TRY(plan_adam(c, as));
   }
 
   N2F_CUDA(cudaMallocHost(&c->h_mm, 4 * sizeof(double)));
@@ -683,21 +523,18 @@ int prepare_input(n2f_ctx* c, const void* image, int dtype, const void* clean, i
   return N2F_OK;
 }
 
-// Derived operand copies of the weights (dgrad-transposed layouts).  Adam
-// keeps them current after every step; this refreshes them after init/set.
+// Derived operand copies of the weights (dgrad-transposed fp32 copy and the
+// fp16 pairs of both layouts).  Adam keeps them current after every step;
+// this refreshes them after init / set_params, and resets the range slots so
+// the first epoch's record starts with these weights.
 int refresh_derived(n2f_ctx* c) {
-  for (int li = 1; li < 8; ++li)
-    N2F_TRY(transpose_dgrad_weights(c->params + c->poff[2 * li], c->wt[li], kCin[li], kCout[li],
-                                    c->stream));
-  if (c->f16) {
-    N2F_TRY(split_f16(c->params, c->w16[0], c->w16[1], kExpW, c->ptotal, c->stream));
-    for (int li = 1; li < 8; ++li)
-      N2F_TRY(split_f16(c->wt[li], c->wt16[0][li], c->wt16[1][li], kExpW, c->pnum[2 * li],
-                        c->stream));
-  } else if (c->tc) {
-    N2F_TRY(split_lo(c->params, c->params_lo, c->ptotal, c->stream));
-    for (int li = 1; li < 8; ++li)
-      N2F_TRY(split_lo(c->wt[li], c->wt_lo[li], c->pnum[2 * li], c->stream));
+  N2F_CUDA(cudaMemsetAsync(c->range_cur, 0, kRangeSlots * sizeof(unsigned), c->stream));
+  for (int li = 1; li < 8; ++li) {
+    const int64_t o = c->poff[2 * li], n = c->pnum[2 * li];
+    unsigned* slot = RS_(c, kRangeWeight, li);
+    N2F_TRY(transpose_dgrad_weights(c->params + o, c->wt[li], kCin[li], kCout[li], c->stream));
+    N2F_TRY(split_f16(c->params + o, c->w16[0] + o, c->w16[1] + o, kExpW, n, c->stream, slot));
+    N2F_TRY(split_f16(c->wt[li], c->wt16[0][li], c->wt16[1][li], kExpW, n, c->stream, slot));
   }
   return N2F_OK;
 }
@@ -744,6 +581,27 @@ int check_cfg(const n2f_config* cfg) {
   return N2F_OK;
 }
 
+const char* range_class_name(int cls) {
+  switch (cls) {
+    case kRangeAct: return "training activation";
+    case kRangeValAct: return "validation activation";
+    case kRangeGrad: return "gradient";
+    default: return "weight";
+  }
+}
+
+// The fit stopped on the range guard (k_stop): N2F_ERR_RANGE naming the slot.
+int range_error(const n2f_ctx* c, const DevState& s) {
+  if (s.range_slot < 0)
+    return fail(N2F_ERR_RANGE, "non-finite validation score %g at epoch %d (FP16x3 range guard)",
+                (double)s.range_val, s.epoch);
+  return fail(N2F_ERR_RANGE,
+              "FP16x3 range guard: %s of layer %d reached max |x * 2^e| = %g (limit %g) at epoch %d; "
+              "the fp16 operand split would overflow",
+              range_class_name(s.range_slot / kLayers), s.range_slot % kLayers + 1,
+              (double)s.range_val, (double)kRangeLimit, s.epoch);
+}
+
 int run_loop(n2f_ctx* c) {
   if (c->cfg.use_graph) {
     N2F_CUDA(cudaGraphLaunch(c->exec, c->stream));
@@ -775,12 +633,11 @@ int n2f_create(int device, int height, int width, const n2f_config* cfg, n2f_ctx
   N2F_TRY(check_cfg(cfg));
   if (height < 4 || width < 4)
     return fail(N2F_ERR_ARG, "image must be at least 4x4, got (%d, %d)", height, width);
-  if (cfg->conv_impl < kImplAuto || cfg->conv_impl > kImplTcF16)
-    return fail(N2F_ERR_ARG,
-                "conv_impl must be 0 (auto), 1 (SIMT), 2 (tcgen05 3xTF32) or 3 (tcgen05 FP16x3)");
+  if (cfg->conv_impl != kImplAuto && cfg->conv_impl != kImplTcF16)
+    return fail(N2F_ERR_UNSUPPORTED,
+                "conv_impl %d: this library implements only tcgen05 FP16x3 (0 = auto, 3)",
+                cfg->conv_impl);
   n2f_ctx* c = new n2f_ctx();
-  c->tc = cfg->conv_impl != kImplSimt;  // auto = tcgen05 FP16x3
-  c->f16 = cfg->conv_impl == kImplTcF16 || cfg->conv_impl == kImplAuto;
   c->device = device;
   c->H = height;
   c->W = width;
@@ -869,6 +726,7 @@ int n2f_fit_denoise_dev(n2f_ctx* c, const void* image, int dtype, const void* cl
   float ms = 0.f;
   N2F_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   res->gpu_ms = ms;
+  if (c->h_state->stop_reason == N2F_STOP_RANGE) return range_error(c, *c->h_state);
   return N2F_OK;
 }
 
@@ -928,7 +786,7 @@ int n2f_ctx_get_arena(n2f_ctx* c, int which, float* host) {
   }
   float* tmp = nullptr;
   N2F_CUDA(cudaMalloc(&tmp, c->ptotal * 4));
-  const AdamArgs& args = c->tc ? c->adam_sc[c->last_sc] : c->adam;
+  const AdamArgs& args = c->adam_sc[c->last_sc];
   for (int q = 0; q < 2 * kLayers; ++q) {
     const AdamTensor& T = args.t[q];
     int s = reduce_partials(T.part, tmp + T.off, T.nsplit, T.n, c->stream);
@@ -1024,6 +882,22 @@ int n2f_ctx_epoch(n2f_ctx* c, int* stopped) {
                            c->stream));
   N2F_CUDA(cudaStreamSynchronize(c->stream));
   if (stopped) *stopped = c->h_state->stopped;
+  if (c->h_state->stop_reason == N2F_STOP_RANGE) return range_error(c, *c->h_state);
+  return N2F_OK;
+}
+
+// Per-epoch range-guard maxima of the epochs run since the last reset
+// (init / set_params): [n][N2F_RANGE_SLOTS] floats.
+int n2f_ctx_range_history(n2f_ctx* c, float* host, int max_rows, int* n_rows) {
+  if (!c || !host || max_rows < 0 || !n_rows) return fail(N2F_ERR_ARG, "bad argument");
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  DevState s;
+  N2F_CUDA(cudaMemcpy(&s, c->dstate, sizeof s, cudaMemcpyDeviceToHost));
+  const int n = s.epoch < max_rows ? s.epoch : max_rows;
+  if (n > 0)
+    N2F_CUDA(cudaMemcpy(host, c->range_hist, (size_t)n * kRangeSlots * sizeof(float),
+                        cudaMemcpyDeviceToHost));
+  *n_rows = n;
   return N2F_OK;
 }
 

@@ -1,0 +1,211 @@
+// First-layer (Cin = 1) kernels on NHWC activations: the L1 forward and the
+// L1 weight gradient.  With one input channel the layer is K = 9: no GEMM
+// shape for the tensor cores, and HBM/latency bound (132 B/px written by the
+// forward), so both are direct CUDA-core kernels restating the reference's
+// fp32 conv (tensor.py:268-316) in the im2col dot order.
+//
+//   forward : y[p][n] = relu( sum_tap x[p+d(tap)] * w[n][tap] + b[n] ), written
+//             as the fp16 operand pair of y * 2^kExpAct for the L2 tcgen05
+//             kernels (or fp32 for the parity entry point)
+//   wgrad   : dw[o][tap] = sum_p g[p][o] * x[p+d(tap)], db[o] = sum_p g[p][o]
+//             (deterministic split over pixels: partial sums per split,
+//             reduced in fixed order by k_adam)
+#include "n2f_internal.cuh"
+#include "tc_common.cuh"
+
+namespace n2f {
+namespace {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// First layer (Cin = 1): direct 3x3, one thread per (pixel, 8 output
+// channels), one image row per grid row (no 64-bit index division).  The
+// 9-tap sum order (fmaf over taps, then + bias) is the reference's im2col
+// dot order (tensor.py:268-282).
+// ---------------------------------------------------------------------------
+template <int CPT>  // output channels per thread: 8 (the network, N % 8 == 0) or 1 (any N, fp32 out)
+__global__ void __launch_bounds__(kThreads)
+    k_conv_first(const float* __restrict__ x, const float* __restrict__ w,
+                 const float* __restrict__ b, float* __restrict__ y, int H, int W, int N, int relu,
+                 __half* __restrict__ yh16, __half* __restrict__ yl16, float oscale,
+                 unsigned* __restrict__ amax) {
+  // weights staged tap-major (ws[t][n]) so a thread's 8 channels of one tap
+  // are two 16-byte smem loads
+  __shared__ __align__(16) float ws[kMaxC * 9];
+  __shared__ __align__(16) float bs[kMaxC];
+  for (int i = threadIdx.x; i < N * 9; i += blockDim.x) ws[(i % 9) * N + i / 9] = w[i];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) bs[i] = b[i];
+  __syncthreads();
+  if constexpr (CPT == 1) {  // parity entry point for arbitrary N (fp32 output only)
+    const int ppb = blockDim.x / N;
+    const int n = threadIdx.x % N;
+    const int px = blockIdx.x * ppb + threadIdx.x / N, py = blockIdx.y;
+    if (px >= W || threadIdx.x >= ppb * N) return;
+    float a = 0.f;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
+      const float xv = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
+      a = fmaf(xv, ws[t * N + n], a);
+    }
+    y[((int64_t)py * W + px) * N + n] = relu ? fmaxf(a + bs[n], 0.f) : a + bs[n];
+    return;
+  }
+  const int nq = N >> 3, ppb = blockDim.x / nq;
+  const int q = threadIdx.x % nq;
+  const int px = blockIdx.x * ppb + threadIdx.x / nq, py = blockIdx.y;
+  if (px >= W) return;
+  float xv[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
+    xv[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
+  }
+  float o[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = 0.f;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {  // per channel the same fmaf order over taps as before
+    const float4 w0 = *reinterpret_cast<const float4*>(ws + t * N + 8 * q);
+    const float4 w1 = *reinterpret_cast<const float4*>(ws + t * N + 8 * q + 4);
+    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = fmaf(xv[t], wv[j], o[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = relu ? fmaxf(o[j] + bs[8 * q + j], 0.f) : o[j] + bs[8 * q + j];
+  const int64_t idx = ((int64_t)py * W + px) * N + 8 * q;
+  if (y) {
+    *reinterpret_cast<float4*>(y + idx) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(y + idx + 4) = make_float4(o[4], o[5], o[6], o[7]);
+  }
+  if (yh16) {  // fp16 pair of y * oscale for the FP16 tcgen05 consumers
+    uint32_t hw[4], lw[4];
+    unsigned mx = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      __half h0, l0, h1, l1;
+      const float a0 = o[j] * oscale, a1 = o[j + 1] * oscale;
+      mx = max(mx, max(tc::range_bits(a0), tc::range_bits(a1)));
+      tc::split_f16(a0, h0, l0);
+      tc::split_f16(a1, h1, l1);
+      hw[j / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+      lw[j / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+    }
+    *reinterpret_cast<uint4*>(yh16 + idx) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(yl16 + idx) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    if (amax) tc::range_note(amax, mx);
+  }
+}
+
+// First-layer wgrad (Cin = 1): dw[o][tap], db[o]; 8 pixel lanes x 32 channels.
+// First-layer wgrad (Cin = 1, NO = 32 output channels): warp = 32 channels,
+// each warp walks 32-pixel row segments with a sliding 3x3 window of the
+// input in registers (3 broadcast loads + one coalesced 128-byte gradient
+// load per pixel).  Block partials [nsplit][NO * 9] / [nsplit][NO], warps
+// combined in fixed order (deterministic).
+constexpr int kFirstSeg = 32;
+__global__ void __launch_bounds__(kThreads)
+    k_wgrad_first(const float* __restrict__ g, const float* __restrict__ x,
+                  float* __restrict__ dw_part, float* __restrict__ db_part, int H, int W, int upw) {
+  constexpr int NO = 32;
+  __shared__ float red[kThreads / 32][NO * 10];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int segs_x = (W + kFirstSeg - 1) / kFirstSeg;
+  const int nunits = H * segs_x;
+  const int gw = blockIdx.x * (kThreads / 32) + warp;
+  float acc[10];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) acc[t] = 0.f;
+  auto X = [&](int yy, int xx) {
+    return (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
+  };
+  const int u1 = min(nunits, (gw + 1) * upw);
+  for (int u = gw * upw; u < u1; ++u) {
+    const int py = u / segs_x, x0 = (u - py * segs_x) * kFirstSeg;
+    const int x1 = min(W, x0 + kFirstSeg);
+    float a0 = X(py - 1, x0 - 1), a1 = X(py - 1, x0);
+    float b0 = X(py, x0 - 1), b1 = X(py, x0);
+    float c0 = X(py + 1, x0 - 1), c1 = X(py + 1, x0);
+    const float* gr = g + ((int64_t)py * W) * NO + lane;
+#pragma unroll 4
+    for (int px = x0; px < x1; ++px) {
+      const float a2 = X(py - 1, px + 1), b2 = X(py, px + 1), c2 = X(py + 1, px + 1);
+      const float gv = __ldg(gr + (int64_t)px * NO);
+      acc[0] = fmaf(gv, a0, acc[0]);
+      acc[1] = fmaf(gv, a1, acc[1]);
+      acc[2] = fmaf(gv, a2, acc[2]);
+      acc[3] = fmaf(gv, b0, acc[3]);
+      acc[4] = fmaf(gv, b1, acc[4]);
+      acc[5] = fmaf(gv, b2, acc[5]);
+      acc[6] = fmaf(gv, c0, acc[6]);
+      acc[7] = fmaf(gv, c1, acc[7]);
+      acc[8] = fmaf(gv, c2, acc[8]);
+      acc[9] += gv;
+      a0 = a1; a1 = a2;
+      b0 = b1; b1 = b2;
+      c0 = c1; c1 = c2;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 10; ++t) red[warp][t * NO + lane] = acc[t];
+  __syncthreads();
+  for (int i = threadIdx.x; i < NO * 10; i += kThreads) {
+    float s = red[0][i];
+#pragma unroll
+    for (int k = 1; k < kThreads / 32; ++k) s += red[k][i];
+    const int t = i / NO, o = i - t * NO;
+    if (t < 9)
+      dw_part[(int64_t)blockIdx.x * NO * 9 + o * 9 + t] = s;
+    else
+      db_part[(int64_t)blockIdx.x * NO + o] = s;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
+                    int cout, cudaStream_t st, int relu, void* yh16, void* yl16, float oscale,
+                    unsigned* amax) {
+  if (cout < 1 || cout > kMaxC) return fail(N2F_ERR_ARG, "conv_first: cout %d", cout);
+  if (h > 65535) return fail(N2F_ERR_ARG, "conv_first: height %d", h);
+  if (cout % 8 == 0 && kThreads % (cout / 8) == 0) {
+    const int ppb = kThreads / (cout / 8);
+    k_conv_first<8><<<dim3((unsigned)((w_ + ppb - 1) / ppb), (unsigned)h), kThreads, 0, st>>>(
+        x, w, b, y, h, w_, cout, relu, reinterpret_cast<__half*>(yh16),
+        reinterpret_cast<__half*>(yl16), oscale, amax);
+  } else {
+    if (!y || yh16) return fail(N2F_ERR_ARG, "conv_first: cout %d supports fp32 output only", cout);
+    const int ppb = kThreads / cout;
+    k_conv_first<1><<<dim3((unsigned)((w_ + ppb - 1) / ppb), (unsigned)h), kThreads, 0, st>>>(
+        x, w, b, y, h, w_, cout, relu, nullptr, nullptr, 1.f, nullptr);
+  }
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+// Pixel splits of the first-layer wgrad: one block per ~256 pixels (8 warps x
+// one 32-pixel segment; the kernel is latency-bound, so many warps), <= 1024.
+int wgrad_first_nsplit(int64_t pixels) {
+  int64_t n = (pixels + 255) / 256;
+  if (n < 1) n = 1;
+  if (n > 1024) n = 1024;
+  return (int)n;
+}
+
+int wgrad_first_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
+                     int cout, int nsplit, cudaStream_t st) {
+  if (cout != 32) return fail(N2F_ERR_ARG, "wgrad_first: cout %d", cout);
+  const int64_t nunits = (int64_t)h * ((w + kFirstSeg - 1) / kFirstSeg);
+  const int64_t warps = (int64_t)nsplit * (kThreads / 32);
+  const int upw = (int)((nunits + warps - 1) / warps);
+  k_wgrad_first<<<nsplit, kThreads, 0, st>>>(g, x, dw_part, db_part, h, w, upw);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+}  // namespace n2f

@@ -52,32 +52,39 @@ constexpr int kCout[kLayers] = {32, 32, 64, 64, 128, 128, 256, 256, 1};
 constexpr int kKsz[kLayers] = {3, 3, 3, 3, 3, 3, 3, 3, 1};
 constexpr int kMaxC = 256;
 
-// ---- conv implementations ---------------------------------------------------
-enum ConvImpl { kImplAuto = 0, kImplSimt = 1, kImplTc = 2, kImplTcF16 = 3 };
+// ---- conv implementation ------------------------------------------------------
+// n2f_config::conv_impl: the product library has ONE implementation, tcgen05
+// FP16x3 (0 = auto = 3); anything else is N2F_ERR_UNSUPPORTED.
+enum ConvImpl { kImplAuto = 0, kImplTcF16 = 3 };
 // power-of-two operand scales of the FP16 split (activations, weights);
-// gradients use ceil(log2(pixels)) + kExpAct (see conv_tc.cu)
+// gradients use ceil(log2(pixels)) + kExpAct (see engine.cu setup)
 constexpr int kExpAct = 8, kExpW = 8;
+
+// ---- FP16x3 range guard (see tc_common.cuh range_note) ----------------------
+// One slot per (tensor class, layer) holds max |x * 2^e| (as ordered float
+// bits) of every operand pair written during the current epoch; the stop
+// kernel moves the slots into a per-epoch history and stops the fit with
+// N2F_STOP_RANGE when one reaches kRangeLimit (or is non-finite).
+enum RangeClass { kRangeAct = 0, kRangeValAct = 1, kRangeGrad = 2, kRangeWeight = 3, kRangeClasses = 4 };
+constexpr int kRangeSlots = kRangeClasses * kLayers;
+constexpr float kRangeLimit = 32768.f;  // 2^15: one binade of headroom below fp16's 65504
 
 // Epilogue modes of the 3x3 implicit GEMM.
 enum Epi { kEpiBiasRelu = 0, kEpiMask = 1, kEpiBias = 2, kEpiNone = 3 };
 
-// SIMT fp32 kernels (conv_simt.cu)
-int conv3x3_simt(const float* x, const float* wk, const float* bias, const float* mask, float* y,
-                 int h, int w, int cin, int cout, int epi, cudaStream_t st);
+// First-layer kernels (first_layer.cu).  conv_first: fp32 output y and/or the
+// fp16 pair of y * oscale (yh16/yl16), amax = range slot of that pair.
 int conv_first_simt(const float* x, const float* w, const float* b, float* y, int h, int w_,
-                    int cout, cudaStream_t st, int relu = 1, float* ylo = nullptr,
-                    void* yh16 = nullptr, void* yl16 = nullptr, float oscale = 1.f);
-int wgrad3x3_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
-                  int cin, int cout, int nsplit, cudaStream_t st);
+                    int cout, cudaStream_t st, int relu = 1, void* yh16 = nullptr,
+                    void* yl16 = nullptr, float oscale = 1.f, unsigned* amax = nullptr);
 int wgrad_first_simt(const float* g, const float* x, float* dw_part, float* db_part, int h, int w,
                      int cout, int nsplit, cudaStream_t st);
-int wgrad_nsplit(int64_t pixels, int cin, int cout);
+int wgrad_first_nsplit(int64_t pixels);
 
 // tcgen05 kernels (conv_tc.cu).  A plan holds the TMA descriptors of one
 // (input buffer, weight buffer, shape) combination; it is built once and
 // launched many times (graph-capturable: maps are kernel parameters).
-// A tensor-core operand: the (hi, lo) pair in TF32 mode (hi = the fp32
-// tensor, lo = fp32 residual; exp = 0) or FP16 mode (fp16 pair of x * 2^exp).
+// A tensor-core operand: the fp16 pair (hi, lo) of x * 2^exp.
 struct TcOperand {
   const void* hi;
   const void* lo;
@@ -85,53 +92,47 @@ struct TcOperand {
 };
 struct ConvTcPlan {
   CUtensorMap mx, mxl, mw, mwl;
-  CUtensorMap my, myh, myl;  // outputs (conv_tc_plan_out): fp32, fp16 hi / tf32-or-fp16 lo
+  CUtensorMap my, myh, myl;  // outputs (conv_tc_plan_out): fp32, fp16 hi / lo
   int omask;                 // which outputs exist (1 y, 2 hi, 4 lo)
   float oscale;              // FP16 pair = fp16 split of y * oscale
   uint32_t* mbits_out;       // bit-packed ReLU mask of the output ([px][N/32]), or null
-  int mask_bits;             // the launch's `mask` is such a bit mask (else fp16/fp32 values)
-  float* y;                  // the same outputs as raw pointers (narrow-layer epilogue)
+  int mask_bits;             // the launch's `mask` is such a bit mask (else fp16 values)
+  unsigned* amax;            // range-guard slot of the pair output, or null
+  float* y;                  // the same outputs as raw pointers
   void* yhi;
   void* ylo;
   int H, W, C, N, grid;
-  bool f16;
   float unscale;  // 2^-(exp_x + exp_w)
-  int dbg;        // profiling experiments only (N2F_TC_DEBUG)
-  int cs;         // CTAs per cluster (2: cta_group::2 pair, M = 256)
-  int dy;         // FP16 dy-stage halo kernel (16 x 8 pixel tiles per CTA)
-  int dx3;        // dy kernel with the dx taps stacked in N (14 x 8 output tiles, N <= 64)
-  int tiles;      // 128-pixel tiles = rows of the colsum output
+  int tiles;      // 16 x 8 pixel CTA tiles = rows of the colsum output
 };
 bool tc_supported(int cin, int cout);
-int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, int W, int C, int N,
-                 bool f16);
-// Outputs (bound once per plan): y fp32 (may be null); FP16 plans write the
-// fp16 pair of y * oscale into yhi/ylo (either may be null); TF32 plans write
-// the fp32 residual into ylo (y required).  mask at launch: layer-input tensor
-// for the ReLU mask (fp32 in TF32 mode, fp16 hi in FP16 mode).
+int conv_tc_plan(ConvTcPlan* pl, const TcOperand& x, const TcOperand& w, int H, int W, int C, int N);
+// Outputs (bound once per plan): y fp32 (may be null) and/or the fp16 pair of
+// y * oscale into yhi/ylo (either may be null).  mask at launch: the fp16 hi
+// tensor of the layer input (ReLU mask), or a bit mask (conv_tc_plan_maskbits).
 int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscale);
-// Wide layers (N >= 128): the forward can emit its ReLU mask bit-packed, the
+// Wide layers (N >= 64): the forward can emit its ReLU mask bit-packed, the
 // dgrad can consume one (call after conv_tc_plan_out).
 int conv_tc_plan_maskbits(ConvTcPlan* pl, uint32_t* mbits_out, int mask_bits_in);
+int conv_tc_plan_range(ConvTcPlan* pl, unsigned* amax);
 int conv_tc_launch(const ConvTcPlan& pl, const float* bias, const void* mask, float* colsum, int epi,
                    cudaStream_t st);
-int conv_tc_tiles(int H, int W);  // upper bound of ConvTcPlan::tiles
+int conv_tc_tiles(int H, int W);  // ConvTcPlan::tiles of an H x W plan
 struct WgradTcPlan {
   CUtensorMap mx, mxl, mg, mgl;
   int H, W, C, N, mblocks, nsplit;
-  bool f16;
   float unscale;
   int xblk;   // activation blocks of an M block loaded as one 4-D box (C % 128 == 0)
   int cs;     // CTAs per cluster (2: pairs of M blocks, cta_group::2)
   int gridx;  // CTAs along M (mblocks rounded up to a multiple of cs)
-  int seg;    // pixels per K stage (32, or 64 for the FP16 single-CTA kernels)
+  int seg;    // pixels per K stage (32 pairs; 64 or 128 single CTAs)
 };
 int wgrad_tc_nsplit(int cin, int cout, int H, int W);
 int wgrad_tc_plan(WgradTcPlan* pl, const TcOperand& x, const TcOperand& g, int H, int W, int C,
-                  int N, int nsplit, bool f16);
+                  int N, int nsplit);
 int wgrad_tc_launch(const WgradTcPlan& pl, float* part, cudaStream_t st);
-int split_lo(const float* x, float* lo, int64_t n, cudaStream_t st);
-int split_f16(const float* x, void* hi, void* lo, int exp2, int64_t n, cudaStream_t st);
+int split_f16(const float* x, void* hi, void* lo, int exp2, int64_t n, cudaStream_t st,
+              unsigned* amax = nullptr);
 
 // utility kernels (prep.cu / train.cu)
 int reduce_partials(const float* part, float* out, int nsplit, int64_t n, cudaStream_t st);

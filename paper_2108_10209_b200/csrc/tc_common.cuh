@@ -205,17 +205,6 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// D[tmem] (+)= A[smem] * B[smem], kind::tf32, one CTA.
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                        uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
 // D[tmem] (+)= A[smem] * B[smem], kind::f16 (fp16/bf16 inputs, fp32 accumulate).
 __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                        uint32_t idesc, uint32_t accumulate) {
@@ -229,15 +218,6 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64
 
 // cta_group::2 MMAs (issued by the leader CTA of a 2-CTA cluster, M = 256:
 // A rows split by CTA, B rows split into N halves by CTA, D in each CTA's TMEM).
-__device__ __forceinline__ void mma_tf32_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                            uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 __device__ __forceinline__ void mma_f16_2sm(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                            uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -315,23 +295,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uin
   d |= (uint64_t)layout << 61;
   return d;
 }
-// layout type 1: SWIZZLE_128B_BASE32B (32-byte granules XOR (row % 4)), the
-// MN-major layout for 32-bit operands.
-constexpr uint32_t kLayoutSw128 = 2, kLayoutSw128Base32 = 1;
-
-__host__ __device__ __forceinline__ uint32_t sw128b32_offset(uint32_t row, uint32_t byte_in_row) {
-  return row * 128u + ((((byte_in_row >> 5) ^ (row & 3u)) << 5) | (byte_in_row & 31u));
-}
-
-// Instruction descriptor, kind::tf32 with fp32 accumulation.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn_major, bool b_mn_major) {
-  return (1u << 4)                      // D format f32
-         | (2u << 7)                    // A format tf32
-         | (2u << 10)                   // B format tf32
-         | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
-         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
 // Instruction descriptor, kind::f16 with fp16 inputs and fp32 accumulation.
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (1u << 4)                      // D format f32
@@ -346,34 +309,24 @@ __host__ __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t
   return row * 128u + ((((byte_in_row >> 4) ^ (row & 7u)) << 4) | (byte_in_row & 15u));
 }
 
-// fp32 -> (hi, lo) split for 3xTF32.  hi = x with the low 13 mantissa bits
-// cleared: exactly what the tensor core reads from the raw fp32 x (it
-// truncates).  lo = the residual x - hi (exact in fp32), then rounded to
-// NEAREST tf32 so that the hardware's truncation of lo is exact and the
-// remaining error is unbiased (a truncated lo always errs toward zero; that
-// systematic shrink measured -7.9e-7 relative per conv).  Zero/subnormal x:
-// hi = x, lo = 0 (so sign(hi) == sign(x) always: ReLU masks can test hi).
-__device__ __forceinline__ float round_tf32(float v) {
-  const uint32_t u = __float_as_uint(v);
-  if ((u & 0x7F800000u) == 0x7F800000u) return v;
-  const uint32_t r = (u + 0x0FFFu + ((u >> 13) & 1u)) & 0xFFFFE000u;  // RN-even on bit 13
-  return __uint_as_float(r);
-}
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  const uint32_t u = __float_as_uint(x);
-  if ((u & 0x7F800000u) == 0u) {
-    hi = x;
-    lo = 0.f;
-  } else {
-    hi = __uint_as_float(u & 0xFFFFE000u);
-    lo = round_tf32(__fsub_rn(x, hi));
-  }
-}
-
 // FP16 split of an (already scaled) fp32 value: hi = fp16(x), lo = fp16(x - hi).
 __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
   hi = __float2half_rn(x);
   lo = __float2half_rn(__fsub_rn(x, __half2float(hi)));
+}
+
+// ---- FP16x3 range guard -------------------------------------------------------
+// Magnitude of a scaled operand value as ordered bits: for non-negative floats
+// the IEEE bit pattern orders like the value, and NaN (0x7FC00000+) sorts
+// above +inf, so an unsigned max catches non-finite values too.
+__device__ __forceinline__ unsigned range_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
+
+// Fold one thread's max into a per-(tensor class, layer) slot: reduce over the
+// threads of the warp that are active here, one atomicMax per group.
+__device__ __forceinline__ void range_note(unsigned* slot, unsigned v) {
+  const unsigned m = __activemask();
+  v = __reduce_max_sync(m, v);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(m) - 1)) atomicMax(slot, v);
 }
 
 }  // namespace tc

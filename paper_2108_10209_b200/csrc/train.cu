@@ -1,6 +1,8 @@
-// Training-loop kernels: fused 1x1 head + loss (+ its backward), validation
-// tail, multi-tensor Adam with fused deterministic split-K reduction, the
-// device-side early-stopping state machine and the output window mean.
+// Training-loop kernels: multi-tensor Adam with fused deterministic split-K
+// reduction, the device-side early-stopping state machine (with the FP16x3
+// range guard), the output window mean, and the standalone loss / validation
+// tail of the parity entry points (the engine fuses both into the L8
+// epilogue, conv_tc.cu).
 #include "n2f_internal.cuh"
 #include "tc_common.cuh"
 #include "loss_dev.cuh"
@@ -10,187 +12,6 @@ namespace n2f {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// ---------------------------------------------------------------------------
-// Fused head for a training step: z = b9 + a8 . w9 (1x1 conv 256->1), loss and
-// dloss/dz, then the head's backward: gp8 = dz * w9 masked by (a8 > 0), and
-// deterministic per-block partials of dw9 / db9 / loss.  Warp per pixel.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads)
-    k_head_train(const float* __restrict__ a8, const float* __restrict__ w9,
-                 const float* __restrict__ b9, const float* __restrict__ tgt,
-                 float* __restrict__ gp8, float* __restrict__ part_w, float* __restrict__ part_b,
-                 double* __restrict__ part_loss, float* __restrict__ zout, int64_t P, int chunk,
-                 int loss, int* __restrict__ step_counter, float* __restrict__ gp8lo,
-                 float* __restrict__ colsum, __half* __restrict__ gp8h, __half* __restrict__ gp8l,
-                 float gscale) {
-  __shared__ float red_w[kWarps][kMaxC];
-  __shared__ float red_c[kWarps][kMaxC];
-  float gcs[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) gcs[c] = 0.f;
-  __shared__ float red_b[kWarps];
-  __shared__ double red_l[kWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t pbeg = (int64_t)blockIdx.x * chunk;
-  const int64_t pend = min(P, pbeg + chunk);
-  float w[8], gw[8];
-  {
-    const float4 w0 = __ldg(reinterpret_cast<const float4*>(w9 + 8 * lane));
-    const float4 w1 = __ldg(reinterpret_cast<const float4*>(w9 + 8 * lane + 4));
-    w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
-    w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) gw[c] = 0.f;
-  const float bias = __ldg(b9);
-  const float nf = (float)P;
-  const float two_over_n = (float)(2.0 / (double)P);
-  float gb = 0.f;
-  double lsum = 0.0;
-  for (int64_t p = pbeg + warp; p < pend; p += kWarps) {
-    const float* row = a8 + p * kMaxC + 8 * lane;
-    const float4 x0 = __ldg(reinterpret_cast<const float4*>(row));
-    const float4 x1 = __ldg(reinterpret_cast<const float4*>(row + 4));
-    const float a[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-    float dot = 0.f;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) dot = fmaf(a[c], w[c], dot);
-    const float z = warp_sum(dot) + bias;
-    float elem;
-    const float dz = loss_grad(z, __ldg(tgt + p), loss, nf, two_over_n, &elem);
-    float g[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      g[c] = a[c] > 0.f ? __fmul_rn(w[c], dz) : 0.f;
-      gw[c] = fmaf(dz, a[c], gw[c]);
-    }
-    if (gp8) {
-      float* grow = gp8 + p * kMaxC + 8 * lane;
-      *reinterpret_cast<float4*>(grow) = make_float4(g[0], g[1], g[2], g[3]);
-      *reinterpret_cast<float4*>(grow + 4) = make_float4(g[4], g[5], g[6], g[7]);
-    }
-    if (gp8h) {  // fp16 pair of g * gscale for the FP16 tcgen05 dgrad / wgrad of L8
-      uint4 hv, lv;
-      uint32_t* hw = reinterpret_cast<uint32_t*>(&hv);
-      uint32_t* lw = reinterpret_cast<uint32_t*>(&lv);
-#pragma unroll
-      for (int c = 0; c < 8; c += 2) {
-        __half h2[2], l2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) tc::split_f16(__fmul_rn(g[c + e], gscale), h2[e], l2[e]);
-        hw[c / 2] = (uint32_t)__half_as_ushort(h2[0]) | ((uint32_t)__half_as_ushort(h2[1]) << 16);
-        lw[c / 2] = (uint32_t)__half_as_ushort(l2[0]) | ((uint32_t)__half_as_ushort(l2[1]) << 16);
-      }
-      *reinterpret_cast<uint4*>(gp8h + p * kMaxC + 8 * lane) = hv;
-      *reinterpret_cast<uint4*>(gp8l + p * kMaxC + 8 * lane) = lv;
-    }
-    if (gp8lo) {  // tf32 residuals for the tcgen05 dgrad of L8
-      float l[8], hh;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) tc::split_tf32(g[c], hh, l[c]);
-      float* lrow = gp8lo + p * kMaxC + 8 * lane;
-      *reinterpret_cast<float4*>(lrow) = make_float4(l[0], l[1], l[2], l[3]);
-      *reinterpret_cast<float4*>(lrow + 4) = make_float4(l[4], l[5], l[6], l[7]);
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c) gcs[c] += g[c];
-    if (lane == 0) {
-      gb += dz;
-      lsum += (double)elem;
-      zout[p] = z;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    red_w[warp][8 * lane + c] = gw[c];
-    red_c[warp][8 * lane + c] = gcs[c];
-  }
-  if (lane == 0) {
-    red_b[warp] = gb;
-    red_l[warp] = lsum;
-  }
-  __syncthreads();
-  {
-    const int c = threadIdx.x;  // kThreads == kMaxC
-    float s = red_w[0][c], t = red_c[0][c];
-    for (int k = 1; k < kWarps; ++k) {
-      s += red_w[k][c];
-      t += red_c[k][c];
-    }
-    part_w[(int64_t)blockIdx.x * kMaxC + c] = s;
-    if (colsum) colsum[(int64_t)blockIdx.x * kMaxC + c] = t;  // bias grad of L8
-  }
-  if (threadIdx.x == 0) {
-    float sb = red_b[0];
-    double sl = red_l[0];
-    for (int k = 1; k < kWarps; ++k) {
-      sb += red_b[k];
-      sl += red_l[k];
-    }
-    part_b[blockIdx.x] = sb;
-    part_loss[blockIdx.x] = sl;
-    if (blockIdx.x == 0 && step_counter) *step_counter += 1;  // Adam step t for this step
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Validation head: z -> sigmoid -> clip to (0,1) (model.py:136-140), write
-// into the ring slot of this epoch, f64 squared error vs the f32 normalised
-// input (trainer.py:97-101).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads)
-    k_head_val(const float* __restrict__ a8, const float* __restrict__ w9,
-               const float* __restrict__ b9, const float* __restrict__ norm,
-               float* __restrict__ ring, int64_t P, int chunk, const DevState* __restrict__ st,
-               int window, double* __restrict__ part_se) {
-  __shared__ double red[kWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t pbeg = (int64_t)blockIdx.x * chunk;
-  const int64_t pend = min(P, pbeg + chunk);
-  float* out = ring + (int64_t)(st->epoch % window) * P;
-  float w[8];
-  {
-    const float4 w0 = __ldg(reinterpret_cast<const float4*>(w9 + 8 * lane));
-    const float4 w1 = __ldg(reinterpret_cast<const float4*>(w9 + 8 * lane + 4));
-    w[0] = w0.x; w[1] = w0.y; w[2] = w0.z; w[3] = w0.w;
-    w[4] = w1.x; w[5] = w1.y; w[6] = w1.z; w[7] = w1.w;
-  }
-  const float bias = __ldg(b9);
-  const float tiny = __int_as_float(1);           // nextafter(0, 1)
-  const float top = __int_as_float(0x3f7fffff);   // nextafter(1, 0)
-  double se = 0.0;
-  for (int64_t p = pbeg + warp; p < pend; p += kWarps) {
-    const float* row = a8 + p * kMaxC + 8 * lane;
-    const float4 x0 = __ldg(reinterpret_cast<const float4*>(row));
-    const float4 x1 = __ldg(reinterpret_cast<const float4*>(row + 4));
-    float dot = x0.x * w[0];
-    dot = fmaf(x0.y, w[1], dot); dot = fmaf(x0.z, w[2], dot); dot = fmaf(x0.w, w[3], dot);
-    dot = fmaf(x1.x, w[4], dot); dot = fmaf(x1.y, w[5], dot); dot = fmaf(x1.z, w[6], dot);
-    dot = fmaf(x1.w, w[7], dot);
-    const float z = warp_sum(dot) + bias;
-    if (lane == 0) {
-      const float o = fminf(fmaxf(sigmoid_ref(z), tiny), top);
-      out[p] = o;
-      const double d = (double)o - (double)__ldg(norm + p);
-      se += d * d;
-    }
-  }
-  if (lane == 0) red[warp] = se;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = red[0];
-    for (int k = 1; k < kWarps; ++k) s += red[k];
-    part_se[blockIdx.x] = s;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Multi-tensor Adam (tensor.py:125-141) with the split-K gradient reduction
@@ -204,17 +25,13 @@ __global__ void __launch_bounds__(kThreads)
 // each operation is rounded separately (no FMA contraction).
 // ---------------------------------------------------------------------------
 constexpr int kAdamRowsPerLane = 16;
-#ifndef N2F_ADAM_NO_WT  // experiment only: skip the transposed weight copies (wrong dgrads)
-#define N2F_ADAM_NO_WT 0
-#endif
-
 // One element's Adam update (NumPy-2 fp32 semantics, tensor.py:125-141) in
-// registers, plus the scattered derived copies (tf32 residual, fp16 pair of
-// the dgrad-transposed weight); m, v, p and the forward fp16 pair are stored
-// by the caller.
+// registers, plus the scattered fp16 pair of the dgrad-transposed weight;
+// m, v, p and the forward fp16 pair are stored by the caller.  rmax: max
+// |p * 2^kExpW| of the pairs written (range guard).
 __device__ __forceinline__ void adam_elem(const AdamArgs& args, const AdamTensor& T, int64_t j,
                                           float g, float bc1, float bc2, float& m, float& v, float& p,
-                                          __half& h16, __half& l16, float& lo) {
+                                          __half& h16, __half& l16, unsigned& rmax) {
   m = __fmul_rn(m, args.beta1);
   m = __fadd_rn(m, __fmul_rn(args.one_minus_beta1, g));
   v = __fmul_rn(v, args.beta2);
@@ -222,11 +39,12 @@ __device__ __forceinline__ void adam_elem(const AdamArgs& args, const AdamTensor
   const float mh = __fdiv_rn(m, bc1);
   const float vh = __fdiv_rn(v, bc2);
   p = __fsub_rn(p, __fdiv_rn(__fmul_rn(args.lr, mh), __fadd_rn(__fsqrt_rn(vh), args.eps)));
-  float hi;
-  lo = 0.f;
-  if (T.want_lo || T.wtlo) tc::split_tf32(p, hi, lo);
-  if (T.want16) tc::split_f16(__fmul_rn(p, args.wscale), h16, l16);  // p * 2^kExpW
-  if (!N2F_ADAM_NO_WT && (T.wt || T.wth16)) {  // wt[c][8-tap][o] = w[o][tap][c]
+  if (T.want16) {  // p * 2^kExpW
+    const float a = __fmul_rn(p, args.wscale);
+    rmax = max(rmax, tc::range_bits(a));
+    tc::split_f16(a, h16, l16);
+  }
+  if (T.wt || T.wth16) {  // wt[c][8-tap][o] = w[o][tap][c]
     const int jj = (int)j;
     // cin is a power of two in the network (shift); 9 is a compile-time divisor
     const int r = T.cin_log2 >= 0 ? jj >> T.cin_log2 : jj / T.cin;
@@ -235,7 +53,6 @@ __device__ __forceinline__ void adam_elem(const AdamArgs& args, const AdamTensor
     const int tap = r - 9 * o;
     const int64_t q = ((int64_t)cc * 9 + (8 - tap)) * T.cout + o;
     if (T.wt) T.wt[q] = p;
-    if (T.wtlo) T.wtlo[q] = lo;
     if (T.wth16) {
       T.wth16[q] = h16;
       T.wtl16[q] = l16;
@@ -296,16 +113,16 @@ __global__ void __launch_bounds__(kThreads)
     float* pv = &p4.x;
     const float* gv = &g4.x;
     __half h[4], l[4];
-    float lo[4];
+    unsigned rmax = 0;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) adam_elem(args, T, j4 + e, gv[e], bc1, bc2, mv[e], vv[e], pv[e], h[e], l[e], lo[e]);
+    for (int e = 0; e < 4; ++e) adam_elem(args, T, j4 + e, gv[e], bc1, bc2, mv[e], vv[e], pv[e], h[e], l[e], rmax);
     *reinterpret_cast<float4*>(args.m + i4) = m4;
     *reinterpret_cast<float4*>(args.v + i4) = v4;
     *reinterpret_cast<float4*>(args.p + i4) = p4;
-    if (T.want_lo) *reinterpret_cast<float4*>(args.plo + i4) = make_float4(lo[0], lo[1], lo[2], lo[3]);
     if (T.want16) {
       *reinterpret_cast<uint2*>(args.phi16 + i4) = make_uint2(pack_h2(h[0], h[1]), pack_h2(h[2], h[3]));
       *reinterpret_cast<uint2*>(args.plo16 + i4) = make_uint2(pack_h2(l[0], l[1]), pack_h2(l[2], l[3]));
+      if (T.amax) tc::range_note(T.amax, rmax);
     }
     return;
   }
@@ -375,30 +192,43 @@ __global__ void __launch_bounds__(kThreads)
   const int ti = (t < args.table_len ? t : args.table_len) - 1;
   const float bc1 = args.bc1[ti], bc2 = args.bc2[ti];
   __half h16, l16;
-  float lo;
-  adam_elem(args, T, j, g, bc1, bc2, m, v, p, h16, l16, lo);
+  unsigned rmax = 0;
+  adam_elem(args, T, j, g, bc1, bc2, m, v, p, h16, l16, rmax);
   args.m[i] = m;
   args.v[i] = v;
   args.p[i] = p;
-  if (T.want_lo) args.plo[i] = lo;  // tf32 residual of the forward operand
-  if (T.want16) {                   // FP16 pair for the FP16 tensor-core path
+  if (T.want16) {  // the forward operand pair of the tcgen05 kernels
     args.phi16[i] = h16;
     args.plo16[i] = l16;
+    if (T.amax) tc::range_note(T.amax, rmax);
   }
 }
 
 // ---------------------------------------------------------------------------
 // End-of-epoch bookkeeping (trainer.py:78-94): reduce the validation and loss
 // partials in fixed order, record history, strict-improvement patience rule,
-// and drive the graph's while-condition.
+// and drive the graph's while-condition.  Range guard: the epoch's
+// per-(class, layer) max |x * 2^e| slots move into range_hist[epoch] and are
+// reset; a slot at or above kRangeLimit (or a non-finite score) stops the fit
+// with N2F_STOP_RANGE instead of training on through inf/NaN operands.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
     k_stop(DevState* __restrict__ st, const double* __restrict__ part_se, int n_se, double pv,
            const double* __restrict__ part_loss, int n_loss, Pt4 pt,
            double* __restrict__ val_hist, double* __restrict__ loss_hist,
            unsigned long long* __restrict__ time_hist, int patience, int max_epochs,
+           unsigned* __restrict__ range_cur, float* __restrict__ range_hist,
            cudaGraphConditionalHandle handle, int use_handle) {
   __shared__ double red[kThreads];
+  __shared__ int bad_slot;
+  if (threadIdx.x == 0) bad_slot = kRangeSlots;
+  __syncthreads();
+  if (range_cur && threadIdx.x < kRangeSlots) {
+    const unsigned b = range_cur[threadIdx.x];
+    range_cur[threadIdx.x] = 0u;
+    if (range_hist) range_hist[(int64_t)st->epoch * kRangeSlots + threadIdx.x] = __uint_as_float(b);
+    if (b >= __float_as_uint(kRangeLimit)) atomicMin(&bad_slot, (int)threadIdx.x);
+  }
   double s = 0.0;
   for (int i = threadIdx.x; i < n_se; i += kThreads) s += part_se[i];
   red[threadIdx.x] = s;
@@ -438,7 +268,15 @@ __global__ void __launch_bounds__(kThreads)
     st->since += 1;
   }
   int go = 1;
-  if (st->since >= patience) {
+  if (bad_slot < kRangeSlots || !isfinite(score)) {
+    st->stopped = 1;
+    st->stop_reason = N2F_STOP_RANGE;
+    st->range_slot = bad_slot < kRangeSlots ? bad_slot : -1;
+    st->range_val = bad_slot < kRangeSlots ? range_hist ? range_hist[(int64_t)e * kRangeSlots + bad_slot]
+                                                        : kRangeLimit
+                                           : (float)score;
+    go = 0;
+  } else if (st->since >= patience) {
     st->stopped = 1;
     st->stop_reason = N2F_STOP_PATIENCE;
     go = 0;
@@ -544,6 +382,8 @@ __global__ void k_reset_state(DevState* st) {
     st->stop_reason = N2F_STOP_MAX_EPOCHS;
     st->best_epoch = 0;
     st->best = INFINITY;
+    st->range_slot = -1;
+    st->range_val = 0.f;
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     st->t0 = now;
@@ -553,28 +393,6 @@ __global__ void k_reset_state(DevState* st) {
 }  // namespace
 
 // ---- launchers ---------------------------------------------------------------
-int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
-                      float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
-                      int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st,
-                      float* gp8lo, float* colsum, void* gp8h, void* gp8l, float gscale) {
-  const int chunk = (int)((P + nblk - 1) / nblk);
-  k_head_train<<<nblk, kThreads, 0, st>>>(a8, w9, b9, tgt, gp8, part_w, part_b, part_loss, zout, P,
-                                          chunk, loss, step_counter, gp8lo, colsum,
-                                          reinterpret_cast<__half*>(gp8h),
-                                          reinterpret_cast<__half*>(gp8l), gscale);
-  N2F_LAUNCH_CHECK();
-  return N2F_OK;
-}
-
-int launch_head_val(const float* a8, const float* w9, const float* b9, const float* norm,
-                    float* ring, int64_t P, int nblk, const DevState* dst, int window,
-                    double* part_se, cudaStream_t st) {
-  const int chunk = (int)((P + nblk - 1) / nblk);
-  k_head_val<<<nblk, kThreads, 0, st>>>(a8, w9, b9, norm, ring, P, chunk, dst, window, part_se);
-  N2F_LAUNCH_CHECK();
-  return N2F_OK;
-}
-
 void adam_plan(AdamArgs& a) {
   int blk = 0, cnt = 0;
   int64_t scr = 0;
@@ -618,11 +436,13 @@ int launch_adam(const AdamArgs& args, const int* step_counter, int fixed_t, cuda
 
 int launch_stop(DevState* dst, const double* part_se, int n_se, double pv, const double* part_loss,
                 int n_loss, const double pt[4], double* val_hist, double* loss_hist,
-                unsigned long long* time_hist, int patience, int max_epochs,
-                cudaGraphConditionalHandle handle, int use_handle, cudaStream_t st) {
+                unsigned long long* time_hist, int patience, int max_epochs, unsigned* range_cur,
+                float* range_hist, cudaGraphConditionalHandle handle, int use_handle,
+                cudaStream_t st) {
   Pt4 ptv{{pt[0], pt[1], pt[2], pt[3]}};
   k_stop<<<1, kThreads, 0, st>>>(dst, part_se, n_se, pv, part_loss, n_loss, ptv, val_hist, loss_hist,
-                                 time_hist, patience, max_epochs, handle, use_handle);
+                                 time_hist, patience, max_epochs, range_cur, range_hist, handle,
+                                 use_handle);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

@@ -16,6 +16,8 @@ struct DevState {
   int best_epoch;
   double best;
   unsigned long long t0;  // %globaltimer at the start of the fit
+  int range_slot;         // N2F_STOP_RANGE: class * 9 + layer of the slot over the limit (-1: score)
+  float range_val;        //   and its max |x * 2^e| (or the non-finite score)
 };
 
 // The 1x1 head (L9) fused into the epilogue of the last 3x3 convolution
@@ -62,9 +64,8 @@ struct AdamTensor {
   const float* part;  // [nsplit][n] gradient partials
   int nsplit;
   float* wt;          // optional dgrad-transposed copy (3x3 weights), else null
-  float* wtlo;        // optional tf32 residual of wt
-  int want_lo;        // write the tf32 residual of p into AdamArgs::plo
   int want16;         // write the fp16 pair of p * wscale into AdamArgs::phi16/plo16
+  unsigned* amax;     // range-guard slot of those pairs (or null)
   __half* wth16;      // optional fp16 pair of the dgrad-transposed copy (scaled)
   __half* wtl16;
   int cin, cout;
@@ -84,7 +85,6 @@ struct AdamArgs {
   int ntensors;
   int64_t total;
   float* p;
-  float* plo;  // tf32 residual arena (same layout as p), for tensors with want_lo
   __half* phi16;  // fp16 pair arenas (same layout as p), for tensors with want16
   __half* plo16;
   float wscale;   // 2^kExpW
@@ -105,19 +105,12 @@ struct AdamArgs {
 // scratch / counter sizes; the caller allocates scratch and zeroed counters.
 void adam_plan(AdamArgs& a);
 
-int launch_head_train(const float* a8, const float* w9, const float* b9, const float* tgt,
-                      float* gp8, float* part_w, float* part_b, double* part_loss, float* zout,
-                      int64_t P, int nblk, int loss, int* step_counter, cudaStream_t st,
-                      float* gp8lo = nullptr, float* colsum = nullptr, void* gp8h = nullptr,
-                      void* gp8l = nullptr, float gscale = 1.f);
-int launch_head_val(const float* a8, const float* w9, const float* b9, const float* norm,
-                    float* ring, int64_t P, int nblk, const DevState* dst, int window,
-                    double* part_se, cudaStream_t st);
 int launch_adam(const AdamArgs& args, const int* step_counter, int fixed_t, cudaStream_t st);
 int launch_stop(DevState* dst, const double* part_se, int n_se, double pv, const double* part_loss,
                 int n_loss, const double pt[4], double* val_hist, double* loss_hist,
-                unsigned long long* time_hist, int patience, int max_epochs,
-                cudaGraphConditionalHandle handle, int use_handle, cudaStream_t st);
+                unsigned long long* time_hist, int patience, int max_epochs, unsigned* range_cur,
+                float* range_hist, cudaGraphConditionalHandle handle, int use_handle,
+                cudaStream_t st);
 int launch_window_mean(const float* ring, int64_t plane, int window, const DevState* dst, int n,
                        int first, const double* mm, double vmin, double vmax, double* out,
                        cudaStream_t st);

@@ -5,8 +5,9 @@ Images share nothing, so the data path has no collective: one process per GPU
 torch.distributed key-value store (TCPStore `add` is an atomic counter): a
 dynamic queue like the reference CLI's process pool (cli.py:207-211), which
 absorbs the per-image imbalance of early stopping.  The only collectives are
-host-side bookkeeping: a barrier before/after the timed region and a MAX
-reduction of the per-rank device times.
+host-side bookkeeping over a gloo group on CPU tensors (north_star (4): no
+NCCL): a barrier before/after the timed region and a MAX reduction of the
+per-rank device times.
 """
 
 from __future__ import annotations

@@ -129,7 +129,7 @@ class Engine:
     """Owns one libn2f context: workspaces + the captured CUDA graph."""
 
     def __init__(self, height: int, width: int, config, device: int | None = None,
-                 conv_impl: int = 0, use_graph: bool = True):
+                 use_graph: bool = True):
         lib = load()
         self.height, self.width = int(height), int(width)
         self.device = _device_index() if device is None else int(device)
@@ -140,7 +140,7 @@ class Engine:
         cfg.patience_epochs = int(config.patience_epochs)
         cfg.avg_window = int(config.avg_window)
         cfg.max_epochs = int(config.max_epochs)
-        cfg.conv_impl = int(conv_impl)
+        cfg.conv_impl = 0  # tcgen05 FP16x3, the library's only implementation
         cfg.seed = int(config.seed) & _M64
         cfg.use_graph = 1 if use_graph else 0
         self.cfg = cfg
@@ -198,29 +198,51 @@ class Engine:
 
     def params(self) -> np.ndarray:
         """The parameter arena (w0, b0, ..., w8, b8; weights K-major) on the host."""
-        n = _lib.C.c_int64()
-        call("n2f_ctx_param_count", self.handle, _lib.C.byref(n))
-        out = np.empty(n.value, np.float32)
+        out = np.empty(self.param_count(), np.float32)
         call("n2f_ctx_get_arena", self.handle, 0, out.ctypes.data)
         return out
 
+    def param_count(self) -> int:
+        n = _lib.C.c_int64()
+        call("n2f_ctx_param_count", self.handle, _lib.C.byref(n))
+        return n.value
+
     def set_params(self, arena: np.ndarray) -> None:
         """Overwrite the parameters (resets Adam moments, step count and stop state)."""
-        a = np.ascontiguousarray(arena, np.float32)
+        a = np.ascontiguousarray(arena, np.float32).reshape(-1)
+        if a.size != self.param_count():
+            raise ValueError(f"parameter arena has {a.size} values, the network has {self.param_count()}")
         call("n2f_ctx_set_params", self.handle, a.ctypes.data)
 
+    def range_history(self) -> np.ndarray:
+        """FP16x3 range guard record of the epochs run since the last init /
+        set_params: [epochs, 4 classes (act, val_act, grad, weight), 9 layers]
+        max |x * 2^e| of the fp16 operand pairs written (0 = none)."""
+        buf = np.zeros((self.max_epochs, _lib.N2F_RANGE_SLOTS), np.float32)
+        n = _lib.C.c_int()
+        call("n2f_ctx_range_history", self.handle, buf.ctypes.data, self.max_epochs, _lib.C.byref(n))
+        return buf[: n.value].reshape(n.value, 4, 9).copy()
+
     def save_checkpoint(self, path) -> None:
-        """N2FW v1 checkpoint of the current parameters (model.py:143-152)."""
+        """N2FW v1 checkpoint of the current parameters (model.py:143-152).
+        The header's seed is the loaded checkpoint's, else this engine's."""
         from . import checkpoint
 
-        checkpoint.save_checkpoint(self.params(), path, self.cfg.seed)
+        seed = self.checkpoint_seed if self.checkpoint_seed is not None else self.cfg.seed
+        checkpoint.save_checkpoint(self.params(), path, seed)
+
+    checkpoint_seed = None
 
     def load_checkpoint(self, path) -> None:
         """Load an N2FW v1 checkpoint into this context (model.py:155-184)."""
         from . import checkpoint
 
-        arena, _, _ = checkpoint.load_checkpoint(path)
+        arena, seed, in_channels = checkpoint.load_checkpoint(path)
+        if in_channels != 1:
+            raise ValueError(f"checkpoint has in_channels={in_channels}; this engine fits "
+                             "single-channel planes (in_channels=1)")
         self.set_params(arena)
+        self.checkpoint_seed = int(seed)
 
     PROF_CLASSES = ("first_fwd", "conv_fwd", "head_loss", "wgrad", "dgrad", "first_wgrad", "adam",
                     "val_first", "val_conv", "val_head", "stop")
@@ -294,10 +316,12 @@ def train_single_channel(noisy, config, clean=None, telemetry=None, telemetry_ta
         raise ValueError(f"expected a 2-D image, got shape {arr.shape}")
     if arr.shape[0] < 4 or arr.shape[1] < 4:
         raise ValueError(f"image must be at least 4x4, got {arr.shape}")
+    # checked here (before any engine work: a NaN image must not evict a
+    # cached context, trainer.py:142-143); the device min/max scan re-checks
+    if not np.isfinite(arr).all():
+        raise ValueError("image contains non-finite values")
     clean_arr = None
     if config.scheme == "exact":
-        if not np.isfinite(arr).all():
-            raise ValueError("image contains non-finite values")
         if clean is None:
             raise ValueError("the exact scheme requires the clean ground-truth image")
         clean_arr = np.asarray(clean, dtype=np.float64)
@@ -317,6 +341,10 @@ def train_single_channel(noisy, config, clean=None, telemetry=None, telemetry_ta
             raise ValueError("image contains non-finite values") from None
         if e.code == _lib.N2F_ERR_ARG:
             raise ValueError(e.msg) from None
+        if e.code == _lib.N2F_ERR_RANGE:
+            # an fp16 operand pair would have overflowed: never return the NaN
+            # image the fit would otherwise produce
+            raise FloatingPointError(e.msg) from None
         raise
     reason = STOP_REASONS[r.stop_reason]
     if reason == "degenerate":

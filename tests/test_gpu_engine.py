@@ -19,13 +19,10 @@ from n2f_testutil import arena_to_layers, net_to_arena, norm_rel, psnr
 pytestmark = pytest.mark.gpu
 
 
-def _engine(h, w, impl=0, **cfg):
+def _engine(h, w, **cfg):
     from paper_2108_10209_b200 import Engine, TrainConfig
 
-    return Engine(h, w, TrainConfig(**cfg), use_graph=False, conv_impl=impl)
-
-
-IMPLS = [pytest.param(1, id="simt"), pytest.param(2, id="tf32x3"), pytest.param(3, id="f16x3")]
+    return Engine(h, w, TrainConfig(**cfg), use_graph=False)
 
 
 def _arena(eng, which):
@@ -60,14 +57,13 @@ def test_seeded_init_matches_oracle(oracle, hw):
     assert np.array_equal(got, net_to_arena(oracle.init_net(7)))
 
 
-@pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("hw", [(32, 32), (64, 48), (128, 128)])
 @pytest.mark.parametrize("loss", ["bce", "mse"])
-def test_one_step_and_one_epoch(oracle, hw, loss, impl):
+def test_one_step_and_one_epoch(oracle, hw, loss):
     from paper_2108_10209_b200 import _lib
 
     img, _ = _image(*hw)
-    eng = _engine(*hw, impl=impl, seed=7, loss=loss)
+    eng = _engine(*hw, seed=7, loss=loss)
     _prepare(eng, img)
     net = oracle.init_net(7)
     norm, lo, hi, _ = oracle.normalize(img)
@@ -118,18 +114,25 @@ def _oracle_arenas(net):
     return [np.ascontiguousarray(np.concatenate(x), dtype=np.float32) for x in (ps, ms, vs)]
 
 
-@pytest.mark.parametrize("impl", IMPLS)
-@pytest.mark.parametrize("hw", [(64, 48), (128, 128), (256, 256)])
-@pytest.mark.parametrize("loss", ["bce", "mse"])
-def test_fixed_weight_steps(oracle, hw, loss, impl):
+@pytest.mark.parametrize("hw,loss", [((64, 48), "bce"), ((64, 48), "mse"), ((128, 128), "bce"),
+                                     ((128, 128), "mse"), ((256, 256), "bce"), ((256, 256), "mse"),
+                                     ((512, 512), "bce")])
+def test_fixed_weight_steps(oracle, hw, loss):
     """Each of the 4 steps of an epoch from IDENTICAL state (weights, Adam
     moments, t) on both sides: logits, gradients and the Adam update agree
     within 1e-3 (per-layer norm-relative), isolating per-step error from the
-    chaotic drift of a free-running trajectory."""
+    chaotic drift of a free-running trajectory; then the epoch's validation
+    pass at the oracle's end-of-epoch weights.  (512, 512) is BASELINE config
+    2, the bench image's size (blob+rect, sigma 50/255)."""
     from paper_2108_10209_b200 import _lib
 
-    img, _ = _image(*hw)
-    eng = _engine(*hw, impl=impl, seed=7, loss=loss)
+    if hw == (512, 512):
+        from paper_2108_10209_b200 import synthetic as sy
+
+        img = sy.config_image(2, 0)[0].astype(np.float64)
+    else:
+        img, _ = _image(*hw)
+    eng = _engine(*hw, seed=7, loss=loss)
     _prepare(eng, img)
     net = oracle.init_net(7)
     n32 = oracle.normalize(img)[0].astype(np.float32)
@@ -155,6 +158,15 @@ def test_fixed_weight_steps(oracle, hw, loss, impl):
             err = norm_rel(np.concatenate([w.ravel(), bb]),
                            np.concatenate([net.weights[li].ravel(), net.biases[li]]))
             assert err < 1e-3, ("params", k, li, err)
+    # validation of the epoch at the oracle's weights after its 4 steps
+    p, m, v = _oracle_arenas(net)
+    _lib.call("n2f_ctx_set_arena", eng.handle, 0, p.ctypes.data, net.t)
+    out = np.empty(img.size, np.float32)
+    score = C.c_double()
+    _lib.call("n2f_ctx_validate", eng.handle, out.ctypes.data, C.byref(score))
+    ref = oracle.predict(net, n32)
+    assert norm_rel(out.reshape(img.shape), ref) < 1e-4
+    assert abs(score.value - oracle.val_score(ref, n32)) < 5e-4 * score.value
 
 
 def test_fit_api_errors_and_degenerate():
@@ -177,9 +189,8 @@ def test_fit_api_errors_and_degenerate():
     assert r.denoised.dtype == np.float64 and np.array_equal(r.denoised, const)
 
 
-@pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("use_graph", [True, False])
-def test_short_fit_matches_oracle_protocol(oracle, use_graph, impl):
+def test_short_fit_matches_oracle_protocol(oracle, use_graph):
     """max_epochs-bounded fit: epoch accounting, telemetry, histories ~ oracle."""
     from paper_2108_10209_b200 import TrainConfig, train_single_channel
     from paper_2108_10209_b200 import trainer as T
@@ -187,7 +198,7 @@ def test_short_fit_matches_oracle_protocol(oracle, use_graph, impl):
     img, clean = _image(32, 40)
     cfg = TrainConfig(seed=3, patience_epochs=50, avg_window=3, max_epochs=5)
     ref = oracle.fit_denoise(img, seed=3, patience=50, window=3, max_epochs=5)
-    eng = T.Engine(32, 40, cfg, use_graph=use_graph, conv_impl=impl)
+    eng = T.Engine(32, 40, cfg, use_graph=use_graph)
     out, r, hist, losses, _ = eng.fit_host(np.ascontiguousarray(img))
     eng.close()
     assert r.epochs_run == ref.epochs_run == 5 and r.stop_reason == 1
@@ -197,7 +208,7 @@ def test_short_fit_matches_oracle_protocol(oracle, use_graph, impl):
     np.testing.assert_allclose(hist, ref.val_history, rtol=5e-2)
     np.testing.assert_allclose(losses, ref.train_losses, rtol=5e-2)
     assert norm_rel(out, ref.denoised) < 2e-2
-    if use_graph and impl == 3:  # the public API (default impl): result types + telemetry schema
+    if use_graph:  # the public API: result types + telemetry schema
         sink = io.StringIO()
         res = train_single_channel(img, cfg, telemetry=sink, telemetry_tags={"slice": 0})
         assert res.epochs_run == 5 and res.stop_reason == "max_epochs"
@@ -308,3 +319,55 @@ def test_context_reuse_across_seeds():
     assert np.array_equal(a2.denoised, b2.denoised) and a2.val_history == b2.val_history
     assert not np.array_equal(a1.denoised, a2.denoised)
     T.release_engines()
+
+
+def test_range_guard_stops_overflowing_weights():
+    """FP16x3 range guard: weights scaled x1e3 put
+    |w * 2^8| far above 2^15, so the first epoch's stop kernel must end the
+    fit with N2F_ERR_RANGE (naming the slot) instead of training on inf/NaN
+    operands and returning a NaN image after `patience` epochs."""
+    from paper_2108_10209_b200 import _lib
+
+    img, _ = _image(64, 64)
+    eng = _engine(64, 64, seed=7, max_epochs=5)
+    _prepare(eng, img)
+    eng.set_params(eng.params() * np.float32(1e3))
+    stopped = C.c_int()
+    with pytest.raises(_lib.N2FError) as e:
+        _lib.call("n2f_ctx_epoch", eng.handle, C.byref(stopped))
+    assert e.value.code == _lib.N2F_ERR_RANGE and "range guard" in e.value.msg
+    assert stopped.value == 1
+    hist = eng.range_history()
+    assert hist.shape == (1, 4, 9)
+    assert hist[0, 3, 1:8].max() >= 2**15  # the weight pairs of L2..L8
+    eng.close()
+
+
+def test_range_guard_public_api_raises():
+    """Through train_single_channel: lr = 1e4 makes the first Adam step move
+    every weight by ~1e4 (Adam's first step is lr * sign(g)), far outside the
+    fp16 operand range: FloatingPointError, never a silent NaN image."""
+    from paper_2108_10209_b200 import TrainConfig, train_single_channel
+    from paper_2108_10209_b200 import trainer as T
+
+    img, _ = _image(48, 48)
+    with pytest.raises(FloatingPointError, match="range guard"):
+        train_single_channel(img, TrainConfig(seed=1, lr=1e4, max_epochs=4))
+    T.release_engines()
+
+
+def test_range_history_headroom_normal_fit():
+    """A normal bounded fit records every slot the engine writes each epoch
+    and stays well inside the fp16 range (the long-fit traces at configs 2, 3
+    and 5 are in profiles/r02_range_trace_*.json)."""
+    img, _ = _image(64, 64, seed=5)
+    from paper_2108_10209_b200 import Engine, TrainConfig
+
+    eng = Engine(64, 64, TrainConfig(seed=5, max_epochs=6, patience_epochs=100, avg_window=3))
+    eng.fit_host(np.ascontiguousarray(img))
+    h = eng.range_history()
+    eng.close()
+    assert h.shape == (6, 4, 9) and np.isfinite(h).all()
+    assert (h[:, 0, 0:7] > 0).all() and (h[:, 1, 0:7] > 0).all()  # activations L1..L7
+    assert (h[:, 2, 1:8] > 0).all() and (h[:, 3, 1:8] > 0).all()  # gradients, weights
+    assert h.max() < 2**15

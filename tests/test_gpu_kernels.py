@@ -85,16 +85,14 @@ CONV_SHAPES = [(1, 32, 3), (32, 32, 3), (32, 64, 3), (64, 64, 3), (64, 128, 3), 
                (128, 256, 3), (256, 256, 3), (256, 1, 1)]
 
 
-def _tc_ok(cin, cout, k):
-    return k == 3 and cin % 32 == 0 and cout in (32, 64, 128, 256)
+IMPL = 3  # tcgen05 FP16x3, the library's only conv implementation (L1 / the 1x1 head:
+          # the first-layer and head kernels)
 
 
-@pytest.mark.parametrize("impl", [1, 2, 3])
 @pytest.mark.parametrize("cin,cout,k", CONV_SHAPES)
 @pytest.mark.parametrize("hw", [(13, 17), (40, 24), (64, 96)])
-def test_conv_forward(lib, oracle, cin, cout, k, hw, impl):
-    if impl >= 2 and not _tc_ok(cin, cout, k):
-        pytest.skip("tcgen05 path covers the 3x3 layers with cin >= 32")
+def test_conv_forward(lib, oracle, cin, cout, k, hw):
+    impl = IMPL
     rng = np.random.default_rng(cin * 1000 + cout + hw[0])
     x = rng.standard_normal((cin, *hw)).astype(np.float32)
     w = (rng.standard_normal((cout, cin, k, k)) / np.sqrt(cin * k * k)).astype(np.float32)
@@ -110,12 +108,10 @@ def test_conv_forward(lib, oracle, cin, cout, k, hw, impl):
         np.testing.assert_allclose(got, ref, rtol=0, atol=1e-5 * np.abs(ref).max())
 
 
-@pytest.mark.parametrize("impl", [1, 2, 3])
 @pytest.mark.parametrize("cin,cout,k", CONV_SHAPES)
 @pytest.mark.parametrize("hw", [(13, 17), (40, 24), (64, 96)])
-def test_conv_backward(lib, oracle, cin, cout, k, hw, impl):
-    if impl >= 2 and not _tc_ok(cout, cin, k):
-        pytest.skip("tcgen05 dgrad covers 3x3 layers with cin in {32..256}")
+def test_conv_backward(lib, oracle, cin, cout, k, hw):
+    impl = IMPL
     rng = np.random.default_rng(cin * 77 + cout + hw[1])
     x = np.maximum(rng.standard_normal((cin, *hw)), 0).astype(np.float32)  # post-ReLU input
     w = (rng.standard_normal((cout, cin, k, k)) / np.sqrt(cin * k * k)).astype(np.float32)
@@ -273,13 +269,37 @@ def test_conv_accuracy_vs_f64(lib, oracle, cin, cout):
     scale = np.abs(exact).max()
     errs = {"oracle_fp32": np.abs(blas - exact).max() / scale}
     d_x, d_w, d_b = dev(chw_to_hwc(x)), dev(oihw_to_engine(wt)), dev(b)
-    for impl in (1, 2, 3):
-        y = empty(h * w * cout)
-        _call(lib, "n2f_conv_fwd", d_x.data_ptr(), d_w.data_ptr(), d_b.data_ptr(), y.data_ptr(),
-              h, w, cin, cout, 3, 0, impl, None)
-        got = hwc_to_chw(host(y).reshape(h, w, cout))
-        errs[f"impl{impl}"] = np.abs(got - exact).max() / scale
-        # signed bias: mean of (got - exact) * sign(exact), relative to mean |exact|
-        errs[f"impl{impl}_bias"] = float(np.mean((got - exact) * np.sign(exact)) / np.mean(np.abs(exact)))
+    y = empty(h * w * cout)
+    _call(lib, "n2f_conv_fwd", d_x.data_ptr(), d_w.data_ptr(), d_b.data_ptr(), y.data_ptr(),
+          h, w, cin, cout, 3, 0, IMPL, None)
+    got = hwc_to_chw(host(y).reshape(h, w, cout))
+    errs["f16x3"] = np.abs(got - exact).max() / scale
+    # signed bias: mean of (got - exact) * sign(exact), relative to mean |exact|
+    errs["f16x3_bias"] = float(np.mean((got - exact) * np.sign(exact)) / np.mean(np.abs(exact)))
     print(f"cin={cin} cout={cout} max-err/scale: {errs}")
-    assert errs["impl1"] < 1e-5 and errs["impl2"] < 3e-5 and errs["impl3"] < 3e-5
+    assert errs["f16x3"] < 3e-5 and abs(errs["f16x3_bias"]) < 1e-5
+
+
+@pytest.mark.parametrize("impl", [1, 2, 4])
+def test_other_conv_impls_unsupported(lib, impl):
+    """One implementation only (no multi-backend dispatch): any conv_impl other
+    than 0 / 3 is N2F_ERR_UNSUPPORTED, for the per-kernel entry points and for
+    a context."""
+    from paper_2108_10209_b200 import TrainConfig, _lib
+
+    d = empty(32 * 32 * 32)
+    w = empty(32 * 9 * 32)
+    b = empty(32)
+    with pytest.raises(_lib.N2FError) as e:
+        _call(lib, "n2f_conv_fwd", d.data_ptr(), w.data_ptr(), b.data_ptr(), d.data_ptr(), 32, 32,
+              32, 32, 3, 1, impl, None)
+    assert e.value.code == _lib.N2F_ERR_UNSUPPORTED
+    cfg = _lib.N2FConfig()
+    cfg.loss, cfg.scheme, cfg.lr = 0, 0, 1e-3
+    cfg.patience_epochs, cfg.avg_window, cfg.max_epochs = 100, 100, 10
+    cfg.conv_impl = impl
+    h = C.c_void_p()
+    with pytest.raises(_lib.N2FError) as e:
+        _call(lib, "n2f_create", 0, 32, 32, C.byref(cfg), C.byref(h))
+    assert e.value.code == _lib.N2F_ERR_UNSUPPORTED
+    del TrainConfig

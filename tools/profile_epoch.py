@@ -1,7 +1,7 @@
 """Per-kernel-class / per-layer timing of one training epoch at a given size
 (CUDA events around every launch), with achieved algorithmic TFLOP/s.
 
-    python tools/profile_epoch.py --size 512 [--impl 2]
+    python tools/profile_epoch.py --size 512
 """
 
 import argparse
@@ -19,13 +19,11 @@ from paper_2108_10209_b200 import Engine, TrainConfig, synthetic  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--size", type=int, default=512)
-    ap.add_argument("--impl", type=int, default=0)
     ap.add_argument("--json", default=None)
     args = ap.parse_args()
     clean = synthetic.blob_rect_image(args.size, args.size, 0)
     noisy = synthetic.gaussian_noisy(clean, 50 / 255, 1)
-    eng = Engine(args.size, args.size, TrainConfig(seed=0, max_epochs=3, patience_epochs=10**6),
-                 conv_impl=args.impl)
+    eng = Engine(args.size, args.size, TrainConfig(seed=0, max_epochs=3, patience_epochs=10**6))
     eng.fit_host(np.ascontiguousarray(noisy))  # warm up + leaves a prepared context
     print(f"context device bytes: {eng.device_bytes / 2**30:.2f} GiB")
     ms, fl, ln = eng.profile_epoch()

@@ -1,7 +1,9 @@
-"""Full-fit PSNR parity across seeds: CPU oracle vs the GPU engine (SIMT,
-tcgen05 3xTF32 and FP16x3 convs).  Prints one JSON line per (seed) and a summary.
+"""GPU side of the PSNR equivalence study: full default fits of the engine on
+the seeded images of tools/psnr_equiv_cpu.py (128^2 blob+rect, clean seed
+100+s, noise seed 200+s, sigma 25/255, TrainConfig(seed=s)), one JSON row per
+seed.  tools/psnr_equiv.py joins these rows with the CPU reference rows.
 
-    python tools/psnr_parity.py --size 64 --seeds 4
+    python tools/psnr_parity.py --size 128 --seeds 0-149 --out gpurun_out/psnr_gpu.jsonl
 """
 
 import argparse
@@ -14,45 +16,41 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import numpy as np  # noqa: E402
 
-from oracle import n2f_oracle as o  # noqa: E402
-from paper_2108_10209_b200 import Engine, TrainConfig, synthetic  # noqa: E402
+from paper_2108_10209_b200 import TrainConfig, synthetic, train_single_channel  # noqa: E402
 
 
 def psnr(a, b):
     return 10 * np.log10(1.0 / np.mean((np.asarray(a, np.float64) - b) ** 2))
 
 
+def parse_seeds(s):
+    out = []
+    for part in s.split(","):
+        a, _, b = part.partition("-")
+        out.extend(range(int(a), int(b or a) + 1))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--size", type=int, default=64)
-    ap.add_argument("--seeds", type=int, default=4)
+    ap.add_argument("--size", type=int, default=128)
+    ap.add_argument("--seeds", default="0-149")
     ap.add_argument("--sigma", type=float, default=25.0)
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-only", action="store_true")
-    ap.add_argument("--first-seed", type=int, default=0)
+    ap.add_argument("--out", default=None)
     args = ap.parse_args()
-    rows = []
-    for s in range(args.first_seed, args.first_seed + args.seeds):
+    sink = open(args.out, "a") if args.out else None
+    for s in parse_seeds(args.seeds):
         clean = synthetic.blob_rect_image(args.size, args.size, 100 + s)
         noisy = synthetic.gaussian_noisy(clean, args.sigma / 255, 200 + s).astype(np.float64)
-        row = {"seed": s, "psnr_noisy": psnr(noisy, clean)}
-        cfg = TrainConfig(seed=s)
-        for impl, name in (() if args.cpu_only else ((1, "simt"), (2, "tf32x3"), (3, "f16x3"))):
-            eng = Engine(args.size, args.size, cfg, conv_impl=impl)
-            out, r, hist, _, _ = eng.fit_host(np.ascontiguousarray(noisy))
-            eng.close()
-            row[name] = psnr(out, clean)
-            row[name + "_epochs"] = r.epochs_run
-        if not args.no_cpu:
-            t = time.time()
-            ref = o.fit_denoise(noisy, seed=s)
-            row["cpu"] = psnr(ref.denoised, clean)
-            row["cpu_epochs"] = ref.epochs_run
-            row["cpu_s"] = time.time() - t
-        rows.append(row)
+        t = time.time()
+        r = train_single_channel(noisy, TrainConfig(seed=s))
+        row = {"kind": "gpu", "seed": s, "size": args.size, "psnr": float(psnr(r.denoised, clean)),
+               "psnr_noisy": float(psnr(noisy, clean)), "epochs": r.epochs_run,
+               "stop": r.stop_reason, "s": time.time() - t}
         print(json.dumps(row), flush=True)
-    keys = ([] if args.cpu_only else ["simt", "tf32x3", "f16x3"]) + ([] if args.no_cpu else ["cpu"])
-    print(json.dumps({"mean": {k: float(np.mean([r[k] for r in rows])) for k in keys}}))
+        if sink:
+            sink.write(json.dumps(row) + "\n")
+            sink.flush()
 
 
 if __name__ == "__main__":
