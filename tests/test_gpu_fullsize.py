@@ -127,11 +127,63 @@ def _check_prep_bitwise(oracle, eng, img):
     return n32, pairs
 
 
-def test_config3_prep_step_and_validation(oracle, config3):
-    """1024^2 microscopy image: bit-exact normalise/pairs/init, then the first
-    training step (pair 0) and the validation pass after it against a float64
-    PyTorch restatement (BCE mean loss, tensor.py:164-181; Adam t=1,
-    tensor.py:125-141)."""
+def _layers_arena(layers):
+    """[(w_oihw, b)] (numpy) -> engine arena (K-major weights)."""
+    from n2f_testutil import oihw_to_engine
+
+    parts = []
+    for w, b in layers:
+        parts += [oihw_to_engine(np.asarray(w, np.float32)).ravel(), np.asarray(b, np.float32)]
+    return np.ascontiguousarray(np.concatenate(parts), dtype=np.float32)
+
+
+def _torch_grads(torch, layers, x, t, loss="bce"):
+    """Manual backprop of model.py:92-113 with torch conv kernels, one layer at
+    a time (only the post-ReLU activations are kept, so a 4096 x 2048 pair
+    fits beside the engine's context).  Returns (logits, [(dW, db)])."""
+    F = torch.nn.functional
+    acts = [x]
+    h = x
+    last = len(layers) - 1
+    with torch.no_grad():
+        for i, (w, b) in enumerate(layers):
+            h = F.conv2d(h, w, b, padding=(w.shape[-1] - 1) // 2)
+            if i != last:
+                h = torch.relu_(h)
+            acts.append(h)
+        z = acts.pop()[0, 0]
+        n = z.numel()
+        if loss == "bce":  # tensor.py:164-181: (sigmoid(z) - t) / N
+            g = ((torch.sigmoid(z) - t) / n)[None, None]
+        else:
+            raise ValueError(loss)
+        grads = [None] * len(layers)
+        for i in range(last, -1, -1):
+            w, b = layers[i]
+            inp = acts.pop()
+            pad = (w.shape[-1] - 1) // 2
+            grads[i] = (torch.nn.grad.conv2d_weight(inp, w.shape, g, padding=pad), g.sum((0, 2, 3)))
+            if i > 0:
+                g = torch.nn.grad.conv2d_input(inp.shape, w, g, padding=pad) * (inp > 0)
+            del inp
+    return z, grads
+
+
+def _adam_ref(p, g, m, v, t, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
+    """tensor.py:125-141 in float64."""
+    m = b1 * m + (1 - b1) * g
+    v = b2 * v + (1 - b2) * g * g
+    p = p - lr * (m / (1 - b1 ** t)) / (np.sqrt(v / (1 - b2 ** t)) + eps)
+    return p, m, v
+
+
+def test_config3_prep_and_all_four_steps(oracle, config3):
+    """1024^2 microscopy image: bit-exact normalise/pairs/init, then ALL FOUR
+    training steps of an epoch, each from an identical state on both sides
+    (weights, Adam moments, t), against a float64 PyTorch restatement: logits
+    < 1e-4, every layer's gradients and updated parameters < 1e-3
+    norm-relative (north_star step bar); then the validation pass at the
+    engine's end-of-epoch weights."""
     from paper_2108_10209_b200 import _lib
 
     torch = _torch()
@@ -145,46 +197,91 @@ def test_config3_prep_step_and_validation(oracle, config3):
     from n2f_testutil import net_to_arena
 
     assert np.array_equal(p0, net_to_arena(oracle.init_net(5)))
-
-    # engine step on pair 0
-    a, t = pairs[0]
-    z = np.empty(a.size, np.float32)
-    _lib.call("n2f_ctx_step", eng.handle, 0, z.ctypes.data)
-    grads = arena_to_layers(_arena(eng, 3), shapes)
-    p1 = arena_to_layers(_arena(eng, 0), shapes)
-
-    # float64 reference step
     f64 = torch.float64
-    layers = _torch_layers(torch, p0, shapes, f64)
-    for w, b in layers:
-        w.requires_grad_(True)
-        b.requires_grad_(True)
-    x = torch.tensor(a, dtype=f64, device="cuda")[None, None]
-    tt = torch.tensor(t, dtype=f64, device="cuda")
-    zr = _torch_forward(torch, layers, x)[0, 0]
-    loss = torch.nn.functional.binary_cross_entropy_with_logits(zr, tt)
-    loss.backward()
-    assert norm_rel(z, zr.detach().cpu().numpy().ravel()) < 1e-4
-    lr, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
-    for li, ((w, b), (gw, gb), (ew, eb)) in enumerate(zip(layers, grads, p1)):
-        rw, rb = w.grad.cpu().numpy(), b.grad.cpu().numpy()
-        assert norm_rel(gw, rw) < 1e-3, ("grad w", li, norm_rel(gw, rw))
-        assert norm_rel(gb, rb) < 1e-3, ("grad b", li, norm_rel(gb, rb))
-        new = []
-        for p, g in ((w, rw), (b, rb)):
-            m = (1 - b1) * g
-            v = (1 - b2) * g * g
-            new.append(p.detach().cpu().numpy() - lr * (m / (1 - b1)) / (np.sqrt(v / (1 - b2)) + eps))
-        err = norm_rel(np.concatenate([ew.ravel(), eb]), np.concatenate([new[0].ravel(), new[1]]))
-        assert err < 1e-3, ("params", li, err)
-
-    # validation pass with the engine's updated parameters
+    # reference state (fp32 values, as both sides hold them), Adam moments zero
+    P = [(w.astype(np.float64), b.astype(np.float64)) for w, b in arena_to_layers(p0, shapes)]
+    M = [(np.zeros_like(w), np.zeros_like(b)) for w, b in P]
+    V = [(np.zeros_like(w), np.zeros_like(b)) for w, b in P]
+    for k, (a, t) in enumerate(pairs):
+        r32 = lambda L: [(w.astype(np.float32), b.astype(np.float32)) for w, b in L]  # noqa: E731
+        P, M, V = r32(P), r32(M), r32(V)
+        for which, L in enumerate((P, M, V)):
+            arr = _layers_arena(L)
+            _lib.call("n2f_ctx_set_arena", eng.handle, which, arr.ctypes.data, k)
+        z = np.empty(a.size, np.float32)
+        _lib.call("n2f_ctx_step", eng.handle, k, z.ctypes.data)
+        grads = arena_to_layers(_arena(eng, 3), shapes)
+        got = arena_to_layers(_arena(eng, 0), shapes)
+        layers = [(torch.tensor(w, dtype=f64, device="cuda"), torch.tensor(b, dtype=f64, device="cuda"))
+                  for w, b in P]
+        x = torch.tensor(a, dtype=f64, device="cuda")[None, None]
+        tt = torch.tensor(t, dtype=f64, device="cuda")
+        zr, rg = _torch_grads(torch, layers, x, tt)
+        assert norm_rel(z, zr.cpu().numpy().ravel()) < 1e-4, ("logits", k)
+        nP, nM, nV = [], [], []
+        for li in range(len(shapes)):
+            rw, rb = (q.cpu().numpy() for q in rg[li])
+            gw, gb = grads[li]
+            assert norm_rel(gw, rw) < 1e-3, ("grad w", k, li, norm_rel(gw, rw))
+            assert norm_rel(gb, rb) < 1e-3, ("grad b", k, li, norm_rel(gb, rb))
+            w1, mw, vw = _adam_ref(P[li][0].astype(np.float64), rw, M[li][0], V[li][0], k + 1)
+            b1_, mb, vb = _adam_ref(P[li][1].astype(np.float64), rb, M[li][1], V[li][1], k + 1)
+            ew, eb = got[li]
+            err = norm_rel(np.concatenate([ew.ravel(), eb]), np.concatenate([w1.ravel(), b1_]))
+            assert err < 1e-3, ("params", k, li, err)
+            nP.append((w1, b1_))
+            nM.append((mw, mb))
+            nV.append((vw, vb))
+        P, M, V = nP, nM, nV
+        del layers, rg
+    # validation pass with the engine's updated parameters (after step 4)
     out = np.empty(H * W, np.float32)
     score = C.c_double()
     _lib.call("n2f_ctx_validate", eng.handle, out.ctypes.data, C.byref(score))
     ref = _predict_banded(torch, _torch_layers(torch, _arena(eng, 0), shapes, f64), n32, f64)
     assert norm_rel(out.reshape(H, W), ref) < 1e-4
     assert abs(score.value - oracle.val_score(ref, n32)) < 1e-3 * score.value
+    eng.close()
+    torch.cuda.empty_cache()
+
+
+def test_config5_training_step_4096(oracle, config5):
+    """4096^2 (config 5): one training step (pair 0, a 4096 x 2048 plane) from
+    the seeded init against a float32 (TF32 off) PyTorch restatement run beside
+    the engine's ~79 GiB context: logits < 1e-4, every layer's gradients and
+    updated parameters < 1e-3 norm-relative."""
+    from paper_2108_10209_b200 import _lib
+
+    torch = _torch()
+    img, _ = config5
+    H, W = img.shape
+    eng = _engine(H, W, seed=9)
+    _lib.call("n2f_ctx_prepare", eng.handle, img.ctypes.data, _lib.N2F_F32, None, 1)
+    shapes = oracle.layer_shapes()
+    p0 = _arena(eng, 0)
+    norm, pairs = _pairs(eng, H, W)
+    a, t = pairs[0]
+    z = np.empty(a.size, np.float32)
+    _lib.call("n2f_ctx_step", eng.handle, 0, z.ctypes.data)
+    grads = arena_to_layers(_arena(eng, 3), shapes)
+    got = arena_to_layers(_arena(eng, 0), shapes)
+    f32 = torch.float32
+    layers = _torch_layers(torch, p0, shapes, f32)
+    zr, rg = _torch_grads(torch, layers, torch.tensor(a, device="cuda")[None, None],
+                          torch.tensor(t, device="cuda"))
+    assert norm_rel(z, zr.cpu().numpy().ravel()) < 1e-4
+    for li, (w0, b0) in enumerate(arena_to_layers(p0, shapes)):
+        rw, rb = (q.double().cpu().numpy() for q in rg[li])
+        gw, gb = grads[li]
+        assert norm_rel(gw, rw) < 1e-3, ("grad w", li, norm_rel(gw, rw))
+        assert norm_rel(gb, rb) < 1e-3, ("grad b", li, norm_rel(gb, rb))
+        w1 = _adam_ref(w0.astype(np.float64), rw, 0.0, 0.0, 1)[0]
+        b1_ = _adam_ref(b0.astype(np.float64), rb, 0.0, 0.0, 1)[0]
+        ew, eb = got[li]
+        err = norm_rel(np.concatenate([ew.ravel(), eb]), np.concatenate([w1.ravel(), b1_]))
+        assert err < 1e-3, ("params", li, err)
+    del layers, rg, zr
+    torch.cuda.empty_cache()
     eng.close()
 
 

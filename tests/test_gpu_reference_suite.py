@@ -1,0 +1,58 @@
+"""The reference's OWN test suite, run against this engine.
+
+`/root/reference/pkg/tests` is copied beside the pip-installed stock package
+into `baseline/_ref/` (git-ignored; it travels to the GPU box with the
+snapshot) by `__graft_entry__.build()`.  Here the whole suite runs in a
+subprocess with `tests/refsuite/n2f_install_plugin.py` loaded first: it calls
+`install()` before any test module imports `noise2fast.trainer`, so every
+`train_single_channel` the suite reaches -- test_trainer.py:208-295, the
+`denoise_image` fan-out tests (320-360), the CLI tests (test_cli.py, incl.
+the `--threads 2` spawn pool, whose workers route through the same engine
+via the autoinstall sitecustomize hook), acceptance criteria 8 and 9 -- runs
+on the B200 engine.  matplotlib is not installed in this image, so a no-op
+stand-in (tests/refsuite/stubs) lets `noise2fast.report` and the CLI import.
+
+Deselected: the three tests that need the scikit-image sample photographs
+(absent here; their data may not be recreated): test_trainer.py::
+test_training_loss_decreases_smoke and acceptance criteria 6 and 7.
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+DESELECT = ["test_trainer.py::test_training_loss_decreases_smoke",
+            "test_acceptance.py::test_criterion_6_denoising_efficacy",
+            "test_acceptance.py::test_criterion_7_ablation_ordering"]
+
+
+def test_reference_suite_through_engine(tmp_path):
+    if not os.path.isdir(os.path.join(REF, "tests")) or not os.path.isdir(os.path.join(REF, "noise2fast")):
+        pytest.fail("baseline/_ref (stock reference + its tests) is missing: run __graft_entry__.build() "
+                    "in the container that has /root/reference")
+    report = tmp_path / "refsuite.json"
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([
+        os.path.join(ROOT, "tests", "refsuite"), os.path.join(ROOT, "tests", "refsuite", "stubs"),
+        os.path.join(ROOT, "paper_2108_10209_b200", "autoinstall"), REF, ROOT,
+        env.get("PYTHONPATH", "")])
+    env.update(N2F_B200_INSTALL="1", N2F_REFSUITE_REPORT=str(report),
+               NUMBA_CACHE_DIR=str(tmp_path / "numba"), PYTHONDONTWRITEBYTECODE="1")
+    tests = os.path.join(REF, "tests")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "n2f_install_plugin", "-p", "no:cacheprovider",
+           "--rootdir", tests, tests, *sum((["--deselect", os.path.join(tests, d)] for d in DESELECT), [])]
+    p = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=str(tmp_path), timeout=1800)
+    tail = p.stdout[-4000:] + p.stderr[-2000:]
+    print(tail)
+    assert p.returncode == 0, tail
+    rep = json.loads(report.read_text())
+    assert rep["routed"] and rep["exitstatus"] == 0
+    # the trainer/denoise_image/CLI tests ran their fits on the engine
+    assert rep["engine_fits"] >= 20, rep
