@@ -197,6 +197,10 @@ int n2f_ctx_get_pairs(n2f_ctx* ctx, float* pair_in, float* pair_tgt, float* norm
 #define N2F_RANGE_SLOTS 36
 int n2f_ctx_range_history(n2f_ctx* ctx, float* host, int max_rows, int* n_rows);
 
+/* Out-of-bounds write check: every context allocation is bracketed by 256
+ * guard bytes of a fixed pattern; *n_bad = guards that no longer hold it. */
+int n2f_ctx_check_guards(n2f_ctx* ctx, int* n_bad);
+
 /* ---- image-quality metrics (benchmark mode; imaging.psnr / imaging.ssim,
  * imaging.py:249-311), f64 device buffers of one single-channel plane ------ */
 /* sum of (a - b)^2 over n samples (host result) */

@@ -101,6 +101,7 @@ SIGNATURES = {
     "n2f_device_count": [_P],
     "n2f_ctx_set_seed": [_P, C.c_uint64],
     "n2f_ctx_range_history": [_P, _P, _I, C.POINTER(C.c_int)],
+    "n2f_ctx_check_guards": [_P, C.POINTER(C.c_int)],
 }
 _RESTYPES = {
     "n2f_last_error": C.c_char_p,

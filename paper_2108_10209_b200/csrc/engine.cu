@@ -31,8 +31,11 @@ struct n2f_ctx {
   int64_t Pt = 0;     // pixels per training pair (identical for the 4 pairs)
   int64_t Pv = 0;     // validation pixels (H*W)
 
-  // device buffers
-  std::vector<void*> allocs;
+  // device buffers: each allocation is bracketed by guard bytes (a fixed
+  // pattern checked by n2f_ctx_check_guards -- the out-of-bounds-write check
+  // that runs everywhere, compute-sanitizer being unavailable on the GPU pool)
+  std::vector<void*> allocs;     // base pointers (guard included)
+  std::vector<size_t> alloc_bytes;  // payload bytes of each
   size_t bytes = 0;
   void* img = nullptr;    // staging input (H*W f64)
   void* clean = nullptr;  // staging clean image (exact scheme)
@@ -111,14 +114,22 @@ struct n2f_ctx {
 
 namespace {
 
+constexpr size_t kGuardBytes = 256;
+constexpr int kGuardByte = 0xA5;
+
 template <typename T>
 int dalloc(n2f_ctx* c, T** p, size_t count) {
   void* q = nullptr;
   const size_t b = count * sizeof(T);
-  N2F_CUDA(cudaMalloc(&q, b < 16 ? 16 : b));
+  const size_t pb = (b + 255) / 256 * 256;  // payload rounded to the guard alignment
+  N2F_CUDA(cudaMalloc(&q, pb + 2 * kGuardBytes));
   c->allocs.push_back(q);
+  c->alloc_bytes.push_back(pb);
   c->bytes += b;
-  *p = reinterpret_cast<T*>(q);
+  uint8_t* base = reinterpret_cast<uint8_t*>(q);
+  N2F_CUDA(cudaMemset(base, kGuardByte, kGuardBytes));
+  N2F_CUDA(cudaMemset(base + kGuardBytes + pb, kGuardByte, kGuardBytes));
+  *p = reinterpret_cast<T*>(base + kGuardBytes);
   return N2F_OK;
 }
 
@@ -883,6 +894,29 @@ int n2f_ctx_epoch(n2f_ctx* c, int* stopped) {
   N2F_CUDA(cudaStreamSynchronize(c->stream));
   if (stopped) *stopped = c->h_state->stopped;
   if (c->h_state->stop_reason == N2F_STOP_RANGE) return range_error(c, *c->h_state);
+  return N2F_OK;
+}
+
+// Guard bytes around every context allocation still hold their pattern (no
+// kernel wrote past either end of a buffer); *n_bad = corrupted guards.
+int n2f_ctx_check_guards(n2f_ctx* c, int* n_bad) {
+  if (!c || !n_bad) return fail(N2F_ERR_ARG, "bad argument");
+  N2F_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<uint8_t> h(kGuardBytes);
+  int bad = 0;
+  for (size_t i = 0; i < c->allocs.size(); ++i) {
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(c->allocs[i]);
+    for (int side = 0; side < 2; ++side) {
+      const uint8_t* g = side ? base + kGuardBytes + c->alloc_bytes[i] : base;
+      N2F_CUDA(cudaMemcpy(h.data(), g, kGuardBytes, cudaMemcpyDeviceToHost));
+      for (size_t k = 0; k < kGuardBytes; ++k)
+        if (h[k] != (uint8_t)kGuardByte) {
+          ++bad;
+          break;
+        }
+    }
+  }
+  *n_bad = bad;
   return N2F_OK;
 }
 

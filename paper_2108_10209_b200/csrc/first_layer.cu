@@ -17,6 +17,7 @@ namespace n2f {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kFirstRows = 4;  // image rows per block of the first-layer forward
 
 // ---------------------------------------------------------------------------
 // First layer (Cin = 1): direct 3x3, one thread per (pixel, 8 output
@@ -52,59 +53,67 @@ __global__ void __launch_bounds__(kThreads)
     y[((int64_t)py * W + px) * N + n] = relu ? fmaxf(a + bs[n], 0.f) : a + bs[n];
     return;
   }
+  // a block covers ppb pixels of kFirstRows consecutive rows (one weight
+  // staging per kFirstRows rows)
   const int nq = N >> 3, ppb = blockDim.x / nq;
   const int q = threadIdx.x % nq;
-  const int px = blockIdx.x * ppb + threadIdx.x / nq, py = blockIdx.y;
-  if (px >= W) return;
-  float xv[9];
+  const int px = blockIdx.x * ppb + threadIdx.x / nq;
+  const int py0 = blockIdx.y * kFirstRows, py1 = min(H, py0 + kFirstRows);
+  unsigned mx = 0;
+  if (px < W) {
+    for (int py = py0; py < py1; ++py) {
+      float xv[9];
 #pragma unroll
-  for (int t = 0; t < 9; ++t) {
-    const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
-    xv[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
-  }
-  float o[8];
+      for (int t = 0; t < 9; ++t) {
+        const int yy = py + t / 3 - 1, xx = px + t % 3 - 1;
+        xv[t] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? __ldg(x + (int64_t)yy * W + xx) : 0.f;
+      }
+      float o[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) o[j] = 0.f;
+      for (int j = 0; j < 8; ++j) o[j] = 0.f;
 #pragma unroll
-  for (int t = 0; t < 9; ++t) {  // per channel the same fmaf order over taps as before
-    const float4 w0 = *reinterpret_cast<const float4*>(ws + t * N + 8 * q);
-    const float4 w1 = *reinterpret_cast<const float4*>(ws + t * N + 8 * q + 4);
-    const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      for (int t = 0; t < 9; ++t) {  // per channel the fmaf order over taps of the im2col dot
+        const float4 w0 = *reinterpret_cast<const float4*>(ws + t * N + 8 * q);
+        const float4 w1 = *reinterpret_cast<const float4*>(ws + t * N + 8 * q + 4);
+        const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = fmaf(xv[t], wv[j], o[j]);
-  }
+        for (int j = 0; j < 8; ++j) o[j] = fmaf(xv[t], wv[j], o[j]);
+      }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) o[j] = relu ? fmaxf(o[j] + bs[8 * q + j], 0.f) : o[j] + bs[8 * q + j];
-  const int64_t idx = ((int64_t)py * W + px) * N + 8 * q;
-  if (y) {
-    *reinterpret_cast<float4*>(y + idx) = make_float4(o[0], o[1], o[2], o[3]);
-    *reinterpret_cast<float4*>(y + idx + 4) = make_float4(o[4], o[5], o[6], o[7]);
-  }
-  if (yh16) {  // fp16 pair of y * oscale for the FP16 tcgen05 consumers
-    uint32_t hw[4], lw[4];
-    unsigned mx = 0;
+      for (int j = 0; j < 8; ++j) o[j] = relu ? fmaxf(o[j] + bs[8 * q + j], 0.f) : o[j] + bs[8 * q + j];
+      const int64_t idx = ((int64_t)py * W + px) * N + 8 * q;
+      if (y) {
+        *reinterpret_cast<float4*>(y + idx) = make_float4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<float4*>(y + idx + 4) = make_float4(o[4], o[5], o[6], o[7]);
+      }
+      if (yh16) {  // fp16 pair of y * oscale for the FP16 tcgen05 consumers
+        uint32_t hw[4], lw[4];
 #pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      __half h0, l0, h1, l1;
-      const float a0 = o[j] * oscale, a1 = o[j + 1] * oscale;
-      mx = max(mx, max(tc::range_bits(a0), tc::range_bits(a1)));
-      tc::split_f16(a0, h0, l0);
-      tc::split_f16(a1, h1, l1);
-      hw[j / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-      lw[j / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+        for (int j = 0; j < 8; j += 2) {
+          __half h0, l0, h1, l1;
+          const float a0 = o[j] * oscale, a1 = o[j + 1] * oscale;
+          mx = max(mx, max(tc::range_bits(a0), tc::range_bits(a1)));
+          tc::split_f16(a0, h0, l0);
+          tc::split_f16(a1, h1, l1);
+          hw[j / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+          lw[j / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+        }
+        *reinterpret_cast<uint4*>(yh16 + idx) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(yl16 + idx) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+      }
     }
-    *reinterpret_cast<uint4*>(yh16 + idx) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-    *reinterpret_cast<uint4*>(yl16 + idx) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-    if (amax) tc::range_note(amax, mx);
   }
+  if (yh16 && amax) tc::range_note(amax, mx);
 }
 
-// First-layer wgrad (Cin = 1): dw[o][tap], db[o]; 8 pixel lanes x 32 channels.
-// First-layer wgrad (Cin = 1, NO = 32 output channels): warp = 32 channels,
-// each warp walks 32-pixel row segments with a sliding 3x3 window of the
-// input in registers (3 broadcast loads + one coalesced 128-byte gradient
-// load per pixel).  Block partials [nsplit][NO * 9] / [nsplit][NO], warps
-// combined in fixed order (deterministic).
+// First-layer wgrad (Cin = 1, NO = 32 output channels): lane = output
+// channel, a warp walks 32-pixel row segments.  Per segment it issues all 32
+// coalesced 128-byte gradient rows at once (memory-level parallelism: the
+// kernel streams 128 B/px of fp32 gradient and is HBM-bound), each lane loads
+// one column of the three input rows of the 3x3 window (34 columns with the
+// halo), and the window values reach the other lanes by shuffles.  Pixels of a
+// segment are summed in x order, segments in unit order, warps in fixed
+// order; block partials [nsplit][NO * 9] / [nsplit][NO] (deterministic).
 constexpr int kFirstSeg = 32;
 __global__ void __launch_bounds__(kThreads)
     k_wgrad_first(const float* __restrict__ g, const float* __restrict__ x,
@@ -124,28 +133,32 @@ __global__ void __launch_bounds__(kThreads)
   const int u1 = min(nunits, (gw + 1) * upw);
   for (int u = gw * upw; u < u1; ++u) {
     const int py = u / segs_x, x0 = (u - py * segs_x) * kFirstSeg;
-    const int x1 = min(W, x0 + kFirstSeg);
-    float a0 = X(py - 1, x0 - 1), a1 = X(py - 1, x0);
-    float b0 = X(py, x0 - 1), b1 = X(py, x0);
-    float c0 = X(py + 1, x0 - 1), c1 = X(py + 1, x0);
-    const float* gr = g + ((int64_t)py * W) * NO + lane;
-#pragma unroll 4
-    for (int px = x0; px < x1; ++px) {
-      const float a2 = X(py - 1, px + 1), b2 = X(py, px + 1), c2 = X(py + 1, px + 1);
-      const float gv = __ldg(gr + (int64_t)px * NO);
-      acc[0] = fmaf(gv, a0, acc[0]);
-      acc[1] = fmaf(gv, a1, acc[1]);
-      acc[2] = fmaf(gv, a2, acc[2]);
-      acc[3] = fmaf(gv, b0, acc[3]);
-      acc[4] = fmaf(gv, b1, acc[4]);
-      acc[5] = fmaf(gv, b2, acc[5]);
-      acc[6] = fmaf(gv, c0, acc[6]);
-      acc[7] = fmaf(gv, c1, acc[7]);
-      acc[8] = fmaf(gv, c2, acc[8]);
-      acc[9] += gv;
-      a0 = a1; a1 = a2;
-      b0 = b1; b1 = b2;
-      c0 = c1; c1 = c2;
+    const int n = min(W - x0, kFirstSeg);
+    const float* gr = g + ((int64_t)py * W + x0) * NO + lane;
+    float gv[kFirstSeg];
+#pragma unroll
+    for (int i = 0; i < kFirstSeg; ++i) gv[i] = i < n ? __ldg(gr + i * NO) : 0.f;
+    // window columns x0 - 1 + lane (and x0 + 31 + lane for lanes 0, 1)
+    float r0[3], r1[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      r0[d] = X(py + d - 1, x0 - 1 + lane);
+      r1[d] = lane < 2 ? X(py + d - 1, x0 + 31 + lane) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < kFirstSeg; ++i) {
+      // x-window columns i, i + 1, i + 2 of the segment (pixel x0 + i)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          const int c = i + e;  // 0..33
+          const float w = c < 32 ? __shfl_sync(0xffffffffu, r0[d], c)
+                                 : __shfl_sync(0xffffffffu, r1[d], c - 32);
+          acc[3 * d + e] = fmaf(gv[i], w, acc[3 * d + e]);
+        }
+      }
+      acc[9] += gv[i];
     }
   }
 #pragma unroll
@@ -175,7 +188,8 @@ int conv_first_simt(const float* x, const float* w, const float* b, float* y, in
   if (h > 65535) return fail(N2F_ERR_ARG, "conv_first: height %d", h);
   if (cout % 8 == 0 && kThreads % (cout / 8) == 0) {
     const int ppb = kThreads / (cout / 8);
-    k_conv_first<8><<<dim3((unsigned)((w_ + ppb - 1) / ppb), (unsigned)h), kThreads, 0, st>>>(
+    k_conv_first<8><<<dim3((unsigned)((w_ + ppb - 1) / ppb), (unsigned)((h + kFirstRows - 1) / kFirstRows)),
+                      kThreads, 0, st>>>(
         x, w, b, y, h, w_, cout, relu, reinterpret_cast<__half*>(yh16),
         reinterpret_cast<__half*>(yl16), oscale, amax);
   } else {
@@ -188,10 +202,10 @@ int conv_first_simt(const float* x, const float* w, const float* b, float* y, in
   return N2F_OK;
 }
 
-// Pixel splits of the first-layer wgrad: one block per ~256 pixels (8 warps x
-// one 32-pixel segment; the kernel is latency-bound, so many warps), <= 1024.
+// Pixel splits of the first-layer wgrad: one block per ~512 pixels (8 warps x
+// two 32-pixel segments, each segment's 32 gradient rows in flight), <= 1024.
 int wgrad_first_nsplit(int64_t pixels) {
-  int64_t n = (pixels + 255) / 256;
+  int64_t n = (pixels + 511) / 512;
   if (n < 1) n = 1;
   if (n > 1024) n = 1024;
   return (int)n;

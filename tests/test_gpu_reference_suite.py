@@ -28,9 +28,8 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "baseline", "_ref")
-DESELECT = ["test_trainer.py::test_training_loss_decreases_smoke",
-            "test_acceptance.py::test_criterion_6_denoising_efficacy",
-            "test_acceptance.py::test_criterion_7_ablation_ordering"]
+DESELECT = ["test_training_loss_decreases_smoke", "test_criterion_6_denoising_efficacy",
+            "test_criterion_7_ablation_ordering"]
 
 
 def test_reference_suite_through_engine(tmp_path):
@@ -43,11 +42,11 @@ def test_reference_suite_through_engine(tmp_path):
         os.path.join(ROOT, "tests", "refsuite"), os.path.join(ROOT, "tests", "refsuite", "stubs"),
         os.path.join(ROOT, "paper_2108_10209_b200", "autoinstall"), REF, ROOT,
         env.get("PYTHONPATH", "")])
-    env.update(N2F_B200_INSTALL="1", N2F_REFSUITE_REPORT=str(report),
+    env.update(N2F_B200_INSTALL="1", N2F_DEVICE="auto", N2F_REFSUITE_REPORT=str(report),
                NUMBA_CACHE_DIR=str(tmp_path / "numba"), PYTHONDONTWRITEBYTECODE="1")
     tests = os.path.join(REF, "tests")
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "n2f_install_plugin", "-p", "no:cacheprovider",
-           "--rootdir", tests, tests, *sum((["--deselect", os.path.join(tests, d)] for d in DESELECT), [])]
+           "--rootdir", tests, tests, "-k", " and ".join(f"not {d}" for d in DESELECT)]
     p = subprocess.run(cmd, capture_output=True, text=True, env=env, cwd=str(tmp_path), timeout=1800)
     tail = p.stdout[-4000:] + p.stderr[-2000:]
     print(tail)
@@ -56,3 +55,4 @@ def test_reference_suite_through_engine(tmp_path):
     assert rep["routed"] and rep["exitstatus"] == 0
     # the trainer/denoise_image/CLI tests ran their fits on the engine
     assert rep["engine_fits"] >= 20, rep
+    assert " passed" in p.stdout and " failed" not in p.stdout and " error" not in p.stdout

@@ -1,0 +1,120 @@
+"""PSNR equivalence study (VERDICT r01 "next" #1): join the GPU engine's full
+fits (tools/psnr_parity.py rows, kind "gpu") with the stock reference's fits
+of the same seeded images (tools/psnr_equiv_cpu.py rows: kind "cpu" = the
+unmodified reference, kind "cpu2" = the reference with 1e-7 relative init
+noise) and report
+
+  gap_gpu = PSNR(GPU) - PSNR(CPU)     the engine against the reference
+  gap_cpu = PSNR(CPU') - PSNR(CPU)    the reference against itself (chaos)
+
+per seed, with the mean, its standard error and 95 % confidence interval
+(Student t), the spread of both gap distributions, and a two-sample
+comparison of them.  The north_star bar is met when the 95 % CI of the mean
+gap_gpu lies inside +-0.1 dB.
+
+    python tools/psnr_equiv.py --gpu profiles/r02_psnr_equiv_gpu_128.jsonl \
+        --cpu profiles/r02_psnr_equiv_cpu.jsonl --out profiles/r02_psnr_equiv_128.json
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+
+import numpy as np
+
+BAR_DB = 0.1
+
+
+def load(paths, size=None):
+    rows = {}
+    for p in paths:
+        for line in open(p):
+            line = line.strip()
+            if not line.startswith("{"):
+                continue
+            r = json.loads(line)
+            if size is not None and r.get("size") != size:
+                continue
+            rows[(r["kind"], r["seed"])] = r
+    return rows
+
+
+def t95(df: int) -> float:
+    try:
+        from scipy import stats
+
+        return float(stats.t.ppf(0.975, df))
+    except Exception:
+        return 1.96
+
+
+def describe(d: np.ndarray) -> dict:
+    n = len(d)
+    if n == 0:
+        return {"n": 0}
+    mean = float(d.mean())
+    sd = float(d.std(ddof=1)) if n > 1 else float("nan")
+    se = sd / math.sqrt(n) if n > 1 else float("nan")
+    h = t95(n - 1) * se if n > 1 else float("nan")
+    return {"n": n, "mean_db": mean, "sd_db": sd, "se_db": se, "ci95_db": [mean - h, mean + h],
+            "max_abs_db": float(np.abs(d).max()),
+            "within_bar": bool(n > 1 and -BAR_DB <= mean - h and mean + h <= BAR_DB)}
+
+
+def analyse(rows: dict) -> dict:
+    seeds = sorted({s for (k, s) in rows})
+    per = []
+    for s in seeds:
+        c = rows.get(("cpu", s))
+        if c is None:
+            continue
+        e = {"seed": s, "psnr_noisy": c["psnr_noisy"], "cpu": c["psnr"], "cpu_epochs": c["epochs"]}
+        g = rows.get(("gpu", s))
+        if g is not None:
+            e.update(gpu=g["psnr"], gpu_epochs=g["epochs"], gap_gpu=g["psnr"] - c["psnr"])
+        c2 = rows.get(("cpu2", s))
+        if c2 is not None:
+            e.update(cpu2=c2["psnr"], cpu2_epochs=c2["epochs"], gap_cpu=c2["psnr"] - c["psnr"])
+        per.append(e)
+    gg = np.array([e["gap_gpu"] for e in per if "gap_gpu" in e])
+    gc = np.array([e["gap_cpu"] for e in per if "gap_cpu" in e])
+    out = {"bar_db": BAR_DB, "gap_gpu_minus_cpu": describe(gg), "gap_cpu2_minus_cpu": describe(gc)}
+    if len(gg) > 1 and len(gc) > 1:
+        try:
+            from scipy import stats
+
+            out["sd_ratio_gpu_over_cpu2"] = float(gg.std(ddof=1) / gc.std(ddof=1))
+            out["levene_p_equal_spread"] = float(stats.levene(gg, gc).pvalue)
+            out["welch_p_equal_mean"] = float(stats.ttest_ind(gg, gc, equal_var=False).pvalue)
+        except Exception:
+            pass
+    cpu = np.array([e["cpu"] for e in per])
+    out["cpu_mean_psnr_db"] = float(cpu.mean()) if len(cpu) else None
+    out["gpu_mean_psnr_db"] = float(np.mean([e["gpu"] for e in per if "gpu" in e])) if len(gg) else None
+    return out, per
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpu", nargs="+", required=True)
+    ap.add_argument("--cpu", nargs="+", required=True)
+    ap.add_argument("--size", type=int, default=128)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    rows = load(args.gpu + args.cpu, args.size)
+    summary, per = analyse(rows)
+    doc = {"what": f"full default fit-and-denoise PSNR at {args.size}^2 (blob+rect, sigma 25/255, clean "
+                   "seed 100+s, noise seed 200+s, TrainConfig(seed=s)); cpu = stock reference "
+                   "(baseline/_ref noise2fast, 1 BLAS thread), cpu2 = stock reference with 1e-7 "
+                   "relative init noise, gpu = this engine; tools/psnr_equiv.py",
+           "summary": summary, "rows": per}
+    print(json.dumps(summary, indent=1))
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(doc, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
