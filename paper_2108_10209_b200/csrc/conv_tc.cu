@@ -26,8 +26,21 @@
 #include "train.cuh"
 
 // Build with -DN2F_TC_TRACE=1 for per-warp cycle accounting (profiling builds only).
+// Tuning constants (A/B builds override them with -D via N2F_EXTRA_FLAGS;
+// the product build uses these defaults).
 // dy kernels with N <= kDy2SmMaxN run two CTAs per SM
-constexpr int kDy2SmMaxN = 32;
+#ifndef N2F_DY_2SM_MAXN
+#define N2F_DY_2SM_MAXN 32
+#endif
+constexpr int kDy2SmMaxN = N2F_DY_2SM_MAXN;
+// accumulation groups per tile of the dy kernels with N < 256
+#ifndef N2F_DY_GROUPS_NARROW
+#define N2F_DY_GROUPS_NARROW 4
+#endif
+// wgrad CTAs per SM for N <= 64 (split-K factor)
+#ifndef N2F_WG_PER_SM_NARROW
+#define N2F_WG_PER_SM_NARROW 2
+#endif
 // stages (32 pixels each) per accumulation group of the wgrad CTA pairs
 constexpr int kWgGroupPair = 4;
 #ifndef N2F_TC_TRACE
@@ -228,7 +241,7 @@ struct DyCfg {
   // K / kGroupsPerTile.  The MMAs run kBufs groups ahead of the accumulate
   // warps, so (kBufs / kGroupsPerTile) of a tile's MMA time hides that tile's
   // predecessor's epilogue: 2/3 of a tile for N = 256, a whole tile below.
-  static constexpr int kGroupsPerTile = BN >= 256 ? 3 : 4;
+  static constexpr int kGroupsPerTile = BN >= 256 ? 3 : N2F_DY_GROUPS_NARROW;
   static constexpr int kTmemCols = kBufs * kCols <= 32 ? 32 : kBufs * kCols <= 64 ? 64
                                    : kBufs * kCols <= 128 ? 128 : kBufs * kCols <= 256 ? 256 : 512;
   static constexpr int kHalf = BN / 2;
@@ -407,6 +420,14 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
     }
+    // fused training head: the L8 gradient pair this thread writes is
+    // w9[n] * dz * 2^e (ReLU-masked), so max |w9| of its column half bounds the
+    // range-guard value per pixel (one product per pixel instead of per element)
+    float w9max = 0.f;
+    if constexpr (HEAD == 1) {
+      const int nh = ((warp - 2) >> 2) * HALF;
+      for (int j = 0; j < HALF; ++j) w9max = fmaxf(w9max, fabsf(sw9[nh + j]));
+    }
     // this lane's pixel: GEMM row m = 32 q + lane = 8 * xl + yl
     const int xl = 4 * q + (lane >> 3), yl = lane & 7;
     constexpr int EC = Cfg::kEpiCols, CH = EC / 4;
@@ -497,6 +518,7 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
         } else {
           float elem = 0.f, dz = 0.f;
           if (valid) dz = loss_grad(z, __ldg(ht.tgt + pix), ht.loss, ht.nf, ht.two_over_n, &elem);
+          if (valid) rmax = max(rmax, range_bits(fabsf(dz) * w9max * oscale));
           if (half == 0 && valid) ht.zout[pix] = z;
 #pragma unroll
           for (int c0 = 0; c0 < HALF; c0 += EC) {
@@ -541,10 +563,8 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
 #pragma unroll
             for (int i = 0; i < EC; i += 2) {
               __half h0, l0, h1, l1;
-              const float a0 = __fmul_rn(gk[i], oscale), a1 = __fmul_rn(gk[i + 1], oscale);
-              if (valid) rmax = max(rmax, max(range_bits(a0), range_bits(a1)));
-              split_f16(a0, h0, l0);
-              split_f16(a1, h1, l1);
+              split_f16(__fmul_rn(gk[i], oscale), h0, l0);
+              split_f16(__fmul_rn(gk[i + 1], oscale), h1, l1);
               hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
               lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
             }
@@ -1333,7 +1353,7 @@ int wgrad_tc_nsplit(int cin, int cout, int H, int W) {
   const int nseg = ((W + kSegW - 1) / kSegW) * H;
   // narrow layers (N <= 64) fit two CTAs per SM: twice the splits keeps two
   // TMA pipelines in flight per SM (their short MMA stages are latency-bound)
-  const int per_sm = cout <= 64 ? 2 : 1;
+  const int per_sm = cout <= 64 ? N2F_WG_PER_SM_NARROW : 1;
   int n = per_sm * sm_count() / gridx;
   if (n < 1) n = 1;
   if (n > nseg) n = nseg;

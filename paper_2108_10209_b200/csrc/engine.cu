@@ -98,6 +98,7 @@ struct n2f_ctx {
   ConvTcPlan val_plan[kLayers]{};
   WgradTcPlan wgrad_plan[2][kLayers]{};
   AdamArgs adam_sc[2]{};  // per training-plane shape class
+  TransposePairs tpose{};  // Adam's forward weight pairs -> dgrad-transposed pairs
   // profiling
   struct Mark {
     int cls, li;
@@ -211,6 +212,7 @@ int enqueue_step(n2f_ctx* c, int k) {
   PROF(kPWgradFirst, 0, conv_flop(P, 0),
        wgrad_first_simt(c->gB, x0, c->part_w[0], c->part_b[0], h, w, kCout[0], c->nsplit0, st));
   PROF(kPAdam, 0, 0.0, launch_adam(c->adam_sc[sc], c->step_counter, 0, st));
+  PROF(kPAdam, 1, 0.0, launch_transpose_pairs(c->tpose, st));
   return N2F_OK;
 }
 
@@ -489,14 +491,31 @@ int setup(n2f_ctx* c) {
       T.cout = kCout[li];
     }
   }
-  // tcgen05 weights (layers 1..7): Adam also writes their fp16 pairs (the
-  // forward operand and the dgrad-transposed one) from the same registers
+  // tcgen05 weights (layers 1..7): Adam also writes their forward fp16 pairs
+  // from the same registers; the dgrad-transposed pairs follow in one tiled
+  // transpose launch (coalesced, instead of 2-byte scattered stores)
   for (int li = 1; li < 8; ++li) {
     AdamTensor& T = a.t[2 * li];
     T.want16 = 1;
     T.amax = RS_(c, kRangeWeight, li);
-    T.wth16 = c->wt16[0][li];
-    T.wtl16 = c->wt16[1][li];
+    T.wth16 = nullptr;
+    T.wtl16 = nullptr;
+  }
+  {
+    TransposePairs& tp = c->tpose;
+    tp.whi = c->w16[0];
+    tp.wlo = c->w16[1];
+    int tiles = 0;
+    for (int li = 1; li < 8; ++li) {
+      tp.thi[li] = c->wt16[0][li];
+      tp.tlo[li] = c->wt16[1][li];
+      tp.off[li] = c->poff[2 * li];
+      tp.cin[li] = kCin[li];
+      tp.cout[li] = kCout[li];
+      tp.tile0[li] = tiles;
+      tiles += 9 * ((kCin[li] + 31) / 32) * ((kCout[li] + 31) / 32);
+    }
+    tp.tile0[8] = tiles;
   }
   // split counts per shape class: bias gradients of layers 1..7 are per-tile
   // column sums (dgrad epilogue of the layer above; L8's from the head), the

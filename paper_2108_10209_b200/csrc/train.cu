@@ -205,6 +205,49 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
+// Dgrad-transposed weight pairs: one block per (layer, tap, 32 output x 32
+// input channels) tile; reads rows of 32 consecutive input channels and
+// writes rows of 32 consecutive output channels (64-byte segments both ways)
+// through a shared-memory tile, for the hi and lo parts.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_transpose_pairs(TransposePairs t) {
+  __shared__ unsigned short sh[2][32][33];
+  const int b = blockIdx.x;
+  int li = 1;
+  while (li < 7 && b >= t.tile0[li + 1]) ++li;
+  const int cin = t.cin[li], cout = t.cout[li];
+  const int ctiles = (cin + 31) / 32, otiles = (cout + 31) / 32;
+  int r = b - t.tile0[li];
+  const int tap = r / (ctiles * otiles);
+  r -= tap * ctiles * otiles;
+  const int ob = r / ctiles, cb = r - ob * ctiles;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const unsigned short* whi = reinterpret_cast<const unsigned short*>(t.whi + t.off[li]);
+  const unsigned short* wlo = reinterpret_cast<const unsigned short*>(t.wlo + t.off[li]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int o = ob * 32 + ty + 8 * k, c = cb * 32 + tx;
+    if (o < cout && c < cin) {
+      const int64_t i = ((int64_t)o * 9 + tap) * cin + c;
+      sh[0][ty + 8 * k][tx] = __ldg(whi + i);
+      sh[1][ty + 8 * k][tx] = __ldg(wlo + i);
+    }
+  }
+  __syncthreads();
+  unsigned short* thi = reinterpret_cast<unsigned short*>(t.thi[li]);
+  unsigned short* tlo = reinterpret_cast<unsigned short*>(t.tlo[li]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = cb * 32 + ty + 8 * k, o = ob * 32 + tx;
+    if (o < cout && c < cin) {
+      const int64_t q = ((int64_t)c * 9 + (8 - tap)) * cout + o;
+      thi[q] = sh[0][tx][ty + 8 * k];
+      tlo[q] = sh[1][tx][ty + 8 * k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // End-of-epoch bookkeeping (trainer.py:78-94): reduce the validation and loss
 // partials in fixed order, record history, strict-improvement patience rule,
 // and drive the graph's while-condition.  Range guard: the epoch's
@@ -430,6 +473,12 @@ int launch_adam(const AdamArgs& args, const int* step_counter, int fixed_t, cuda
   if (args.cnt_total && (!args.scratch || !args.counters))
     return fail(N2F_ERR_ARG, "launch_adam: plan needs scratch and counters");
   k_adam<<<(unsigned)args.nblocks, kThreads, 0, st>>>(args, step_counter, fixed_t);
+  N2F_LAUNCH_CHECK();
+  return N2F_OK;
+}
+
+int launch_transpose_pairs(const TransposePairs& t, cudaStream_t st) {
+  k_transpose_pairs<<<(unsigned)t.tile0[8], 256, 0, st>>>(t);
   N2F_LAUNCH_CHECK();
   return N2F_OK;
 }

@@ -101,6 +101,20 @@ struct AdamArgs {
   int* counters;
 };
 
+// The dgrad-transposed fp16 weight pairs wt[c][8-tap][o] = w[o][tap][c] of
+// the tcgen05 layers, rebuilt from the forward pairs after every Adam step
+// by one tiled (coalesced) launch over all layers.
+struct TransposePairs {
+  const __half* whi;  // forward pair arenas (AdamArgs::phi16 / plo16 layout)
+  const __half* wlo;
+  __half* thi[kLayers];
+  __half* tlo[kLayers];
+  int64_t off[kLayers];  // weight offset of layer li in the arena
+  int cin[kLayers], cout[kLayers];
+  int tile0[kLayers + 1];  // first 32 x 32 tile of layer li (layers 1..7), tile0[8] = total
+};
+int launch_transpose_pairs(const TransposePairs& t, cudaStream_t st);
+
 // Fill the reduction plan of every tensor (needs t[].n / nsplit) and the
 // scratch / counter sizes; the caller allocates scratch and zeroed counters.
 void adam_plan(AdamArgs& a);
