@@ -5,6 +5,7 @@ The compute runs in hand-written sm_100a CUDA kernels behind the C ABI in
 reference's trainer interface.
 """
 
+from .imageio import ImageFormatError, from_plane, load_image, save_image  # noqa: F401
 from .trainer import (  # noqa: F401
     DenoiseResult,
     Engine,
@@ -21,10 +22,14 @@ __all__ = [
     "DenoiseResult",
     "Engine",
     "ImageData",
+    "ImageFormatError",
     "TrainConfig",
     "denoise_image",
     "derive_seed",
+    "from_plane",
     "install",
+    "load_image",
     "release_engines",
+    "save_image",
     "train_single_channel",
 ]

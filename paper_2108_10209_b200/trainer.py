@@ -28,6 +28,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .imageio import ImageData  # noqa: F401  (re-exported; imaging.py:26)
 from . import _lib
 from ._lib import N2FConfig, N2FResult, STOP_REASONS, call, load
 
@@ -366,26 +367,6 @@ def train_single_channel(noisy, config, clean=None, telemetry=None, telemetry_ta
         wall_time=time.perf_counter() - t0,
         stop_reason=reason,
     )
-
-
-@dataclass
-class ImageData:
-    """Minimal stand-in for the reference ImageData (imaging.py): samples are
-    (n_slices, height, width, channels)."""
-
-    samples: np.ndarray
-    bit_depth: str = "float32"
-    data_range: float | None = 1.0
-
-    @property
-    def n_slices(self) -> int:
-        return self.samples.shape[0]
-
-    @property
-    def channels(self) -> int:
-        return self.samples.shape[3]
-
-
 def denoise_image(image, config, clean=None, telemetry=None):
     """Denoise every channel of every slice with independent runs (trainer.py:216-250)."""
     if not 1 <= image.channels <= 4:

@@ -164,27 +164,3 @@ def test_dead_relu_path_has_zero_weight_gradient(oracle):
     assert not gw0[dead].any() and gb0[dead] == 0.0
     assert gw0[0].any()
     eng.close()
-
-
-@pytest.mark.parametrize("cin,cout", [(32, 32), (32, 64), (64, 64)])
-def test_dx_stacked_experiment_still_exact(lib, monkeypatch, cin, cout):
-    """The dx-stacked narrow conv (N2F_DY_DX3=1, an experiment kept off by
-    default) on the box-sum known answer and a random conv vs the oracle."""
-    monkeypatch.setenv("N2F_DY_DX3", "1")
-    hw = (17, 70)
-    out = _fwd(lib, np.ones((cin, *hw), np.float32), np.ones((cout, cin, 3, 3), np.float32),
-               np.zeros(cout, np.float32))
-    ny = np.full(hw[0], 3.0)
-    ny[[0, -1]] -= 1
-    nx = np.full(hw[1], 3.0)
-    nx[[0, -1]] -= 1
-    assert np.array_equal(out, np.broadcast_to((np.outer(ny, nx) * cin).astype(np.float32), out.shape))
-    from oracle import n2f_oracle as o
-
-    rng = np.random.default_rng(cin + cout)
-    x = rng.standard_normal((cin, *hw)).astype(np.float32)
-    w = (rng.standard_normal((cout, cin, 3, 3)) / np.sqrt(9 * cin)).astype(np.float32)
-    b = rng.standard_normal(cout).astype(np.float32)
-    ref = o.conv_forward(x, w, b)
-    got = _fwd(lib, x, w, b)
-    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-5 * np.abs(ref).max())
