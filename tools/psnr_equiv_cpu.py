@@ -35,14 +35,18 @@ def _worker_init():
     sys.path.insert(0, REPO)
 
 
-def _fit(kind: str, seed: int, size: int, sigma: float):
+def _fit(kind: str, seed: int, size: int, sigma: float, image: str = "study"):
     import numpy as np
     from noise2fast import model, trainer
 
     from paper_2108_10209_b200 import synthetic
 
-    clean = synthetic.blob_rect_image(size, size, 100 + seed)
-    noisy = synthetic.gaussian_noisy(clean, sigma / 255, 200 + seed).astype(np.float64)
+    if image == "config1":  # BASELINE.json config 1 (256^2, sigma 25/255), image seed = fit seed
+        noisy, clean = synthetic.config_image(1, seed)
+        noisy, size = noisy.astype(np.float64), 256
+    else:
+        clean = synthetic.blob_rect_image(size, size, 100 + seed)
+        noisy = synthetic.gaussian_noisy(clean, sigma / 255, 200 + seed).astype(np.float64)
     orig = model.build_network
     if kind == "cpu2":
         rng = np.random.default_rng(10_000 + seed)
@@ -62,7 +66,7 @@ def _fit(kind: str, seed: int, size: int, sigma: float):
     finally:
         model.build_network = orig
     p = 10 * np.log10(1.0 / np.mean((res.denoised - clean) ** 2))
-    return {"kind": kind, "seed": seed, "size": size, "psnr": float(p),
+    return {"kind": kind, "seed": seed, "size": size, "image": image, "psnr": float(p),
             "psnr_noisy": float(10 * np.log10(1.0 / np.mean((noisy - clean) ** 2))),
             "epochs": res.epochs_run, "stop": res.stop_reason, "s": dt}
 
@@ -83,22 +87,26 @@ def main():
     ap.add_argument("--size", type=int, default=128)
     ap.add_argument("--sigma", type=float, default=25.0)
     ap.add_argument("--workers", type=int, default=6)
+    ap.add_argument("--image", default="study", choices=["study", "config1"])
+    ap.add_argument("--blas-threads", type=int, default=1)
     args = ap.parse_args()
+    if args.image == "config1":
+        args.size = 256
     done = set()
     if os.path.exists(args.out):
         for line in open(args.out):
             if line.startswith("{"):
                 r = json.loads(line)
-                done.add((r["kind"], r["seed"], r["size"]))
+                if r.get("image", "study") == args.image:
+                    done.add((r["kind"], r["seed"], r["size"]))
     kinds = args.kinds.split(",")
     jobs = [(k, s) for s in _parse_seeds(args.seeds) for k in kinds
             if (k, s, args.size) not in done]
     print(f"{len(jobs)} fits to run", flush=True)
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
-    os.environ["OMP_NUM_THREADS"] = "1"
-    os.environ["MKL_NUM_THREADS"] = "1"
+    for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = str(args.blas_threads)
     with ProcessPoolExecutor(args.workers, initializer=_worker_init) as ex:
-        futs = [ex.submit(_fit, k, s, args.size, args.sigma) for k, s in jobs]
+        futs = [ex.submit(_fit, k, s, args.size, args.sigma, args.image) for k, s in jobs]
         with open(args.out, "a") as f:
             for fu in as_completed(futs):
                 row = fu.result()

@@ -37,14 +37,19 @@ def main():
     ap.add_argument("--seeds", default="0-149")
     ap.add_argument("--sigma", type=float, default=25.0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--image", default="study", choices=["study", "config1"])
     args = ap.parse_args()
     sink = open(args.out, "a") if args.out else None
     for s in parse_seeds(args.seeds):
-        clean = synthetic.blob_rect_image(args.size, args.size, 100 + s)
-        noisy = synthetic.gaussian_noisy(clean, args.sigma / 255, 200 + s).astype(np.float64)
+        if args.image == "config1":  # BASELINE.json config 1 (256^2, sigma 25/255)
+            noisy, clean = synthetic.config_image(1, s)
+            noisy, args.size = noisy.astype(np.float64), 256
+        else:
+            clean = synthetic.blob_rect_image(args.size, args.size, 100 + s)
+            noisy = synthetic.gaussian_noisy(clean, args.sigma / 255, 200 + s).astype(np.float64)
         t = time.time()
         r = train_single_channel(noisy, TrainConfig(seed=s))
-        row = {"kind": "gpu", "seed": s, "size": args.size, "psnr": float(psnr(r.denoised, clean)),
+        row = {"kind": "gpu", "seed": s, "size": args.size, "image": args.image, "psnr": float(psnr(r.denoised, clean)),
                "psnr_noisy": float(psnr(noisy, clean)), "epochs": r.epochs_run,
                "stop": r.stop_reason, "s": time.time() - t}
         print(json.dumps(row), flush=True)
