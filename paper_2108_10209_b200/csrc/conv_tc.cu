@@ -439,6 +439,19 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
     for (int ut = cid; ut < nunits; ut += ncl) {
       const int x0 = (ut % tiles_x) * 2 * Cfg::kTileW + Cfg::kTileW * (int)rank, y0 = (ut / tiles_x) * 8;
       const int tile = ut * 2 + (int)rank;  // colsum row
+      // this tile's pixel and (dgrad) its bit-packed ReLU mask words, requested
+      // before the accumulation wait so the load latency hides behind the MMAs
+      const int px = x0 + xl, py = y0 + yl;
+      const bool valid = py < H && px < W;
+      const int n0 = half * HALF;
+      constexpr int WPP = BN / 32, MW = HALF / 32 > 0 ? HALF / 32 : 1;
+      const int64_t pix = (int64_t)py * W + px;
+      uint32_t mw[MW];
+      if (epi == kEpiMask && mask_bits) {
+#pragma unroll
+        for (int k = 0; k < MW; ++k)
+          mw[k] = valid ? __ldg(reinterpret_cast<const uint32_t*>(mask) + pix * WPP + n0 / 32 + k) : 0u;
+      }
       float acc[ACOLS];
 #pragma unroll
       for (int j = 0; j < ACOLS; ++j) acc[j] = 0.f;
@@ -472,17 +485,6 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
       // ---- epilogue (see k_conv3x3_tc): scale removal, bias+ReLU or the ReLU
       // mask, column sums, bit masks, staging in the TMA swizzle layout and
       // TMA tensor stores of {EC channels, 4 x, 8 y} boxes
-      const int px = x0 + xl, py = y0 + yl;
-      const bool valid = py < H && px < W;
-      const int n0 = half * HALF;
-      constexpr int WPP = BN / 32, MW = HALF / 32 > 0 ? HALF / 32 : 1;
-      const int64_t pix = (int64_t)py * W + px;
-      uint32_t mw[MW];
-      if (epi == kEpiMask && mask_bits) {
-#pragma unroll
-        for (int k = 0; k < MW; ++k)
-          mw[k] = valid ? __ldg(reinterpret_cast<const uint32_t*>(mask) + pix * WPP + n0 / 32 + k) : 0u;
-      }
       uint32_t ob = 0;
       if constexpr (HEAD != 0) {
         // ---- fused L9 head.  The L8 activation (fp32, the regular epilogue's
@@ -562,11 +564,7 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
             uint32_t hw[EC / 2], lw[EC / 2];
 #pragma unroll
             for (int i = 0; i < EC; i += 2) {
-              __half h0, l0, h1, l1;
-              split_f16(__fmul_rn(gk[i], oscale), h0, l0);
-              split_f16(__fmul_rn(gk[i + 1], oscale), h1, l1);
-              hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-              lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+              split_f16x2(__fmul_rn(gk[i], oscale), __fmul_rn(gk[i + 1], oscale), hw[i / 2], lw[i / 2]);
             }
             uint8_t* stg = stg0;
             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -648,10 +646,14 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
           uint32_t sbits = 0;
 #pragma unroll
           for (int i = 0; i < EC; ++i) sbits |= (v[i] > 0.f ? 1u : 0u) << i;
-          ob |= sbits << (n % 32);
-          if ((n + EC) % 32 == 0) {
-            if (valid) mbits_out[pix * WPP + n / 32] = ob;
-            ob = 0;
+          if constexpr (HALF < 32) {  // N = 32: each column half owns a 16-bit half word
+            if (valid) reinterpret_cast<uint16_t*>(mbits_out)[pix * (BN / 16) + n / 16] = (uint16_t)sbits;
+          } else {
+            ob |= sbits << (n % 32);
+            if ((n + EC) % 32 == 0) {
+              if (valid) mbits_out[pix * WPP + n / 32] = ob;
+              ob = 0;
+            }
           }
         }
         if (colsum) {  // transpose-reduce column sums over the warp's 32 pixels
@@ -701,13 +703,9 @@ __global__ void __launch_bounds__(kThreadsTc, DyCfg<BN>::kPerSm)  // 168 registe
           uint32_t hw[EC / 2], lw[EC / 2];
 #pragma unroll
           for (int i = 0; i < EC; i += 2) {
-            __half h0, l0, h1, l1;
             const float a0 = v[i] * oscale, a1 = v[i + 1] * oscale;
             if (valid) rmax = max(rmax, max(range_bits(a0), range_bits(a1)));
-            split_f16(a0, h0, l0);
-            split_f16(a1, h1, l1);
-            hw[i / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-            lw[i / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+            split_f16x2(a0, a1, hw[i / 2], lw[i / 2]);
           }
 #pragma unroll
           for (int k = 0; k < EC / 8; ++k) {
@@ -1308,8 +1306,8 @@ int conv_tc_plan_out(ConvTcPlan* pl, float* y, void* yhi, void* ylo, float oscal
 }
 
 int conv_tc_plan_maskbits(ConvTcPlan* pl, uint32_t* mbits_out, int mask_bits_in) {
-  if ((mbits_out || mask_bits_in) && pl->N < 64)
-    return fail(N2F_ERR_ARG, "bit-packed ReLU masks need N >= 64, N=%d", pl->N);
+  if ((mbits_out || mask_bits_in) && pl->N < 32)
+    return fail(N2F_ERR_ARG, "bit-packed ReLU masks need N >= 32, N=%d", pl->N);
   pl->mbits_out = mbits_out;
   pl->mask_bits = mask_bits_in;
   return N2F_OK;

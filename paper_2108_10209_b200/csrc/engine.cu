@@ -92,7 +92,7 @@ struct n2f_ctx {
   __half* act16[2][kLayers] = {}; // layer outputs 0..6
   __half* g16[2][2] = {};         // [A/B][hi/lo] gradient ping-pong
   __half* v16[2][2] = {};         // [A/B][hi/lo] validation ping-pong
-  uint32_t* mbits[kLayers] = {};  // bit-packed ReLU masks of the wide forward outputs (L5..L7)
+  uint32_t* mbits[kLayers] = {};  // bit-packed ReLU masks of the tcgen05 forward outputs (L2..L7)
   ConvTcPlan fwd_plan[2][kLayers]{};
   ConvTcPlan dgrad_plan[2][kLayers]{};
   ConvTcPlan val_plan[kLayers]{};
@@ -386,9 +386,12 @@ int setup(n2f_ctx* c) {
   auto g_op = [&](int ab) { return TcOperand{c->g16[ab][0], c->g16[ab][1], c->exp_g}; };
   auto v_op = [&](int ab) { return TcOperand{c->v16[ab][0], c->v16[ab][1], kExpAct}; };
   const float sa = ldexpf(1.f, kExpAct), sg = ldexpf(1.f, c->exp_g);
-  // wide forward outputs feeding a wide dgrad also emit bit-packed ReLU masks
-  for (int li = 1; li < 7; ++li)
-    if (kCout[li] >= 128) N2F_TRY(dalloc(c, &c->mbits[li], c->Pt * (kCout[li] / 32)));
+  // the tcgen05 forward outputs (L2..L7) also emit their ReLU mask bit-packed
+  // for the dgrad above them: one word per 32 channels and pixel instead of
+  // re-reading the fp16 activation as the mask (dgrad L4 -17 %; the L2 dgrad
+  // reads the L1 activation: emitting bits from the first-layer kernel cost
+  // more there than the dgrad gained)
+  for (int li = 1; li < 7; ++li) N2F_TRY(dalloc(c, &c->mbits[li], c->Pt * (kCout[li] / 32)));
   for (int sc = 0; sc < 2; ++sc) {
     const int h = c->ph[2 * sc], w = c->pw[2 * sc];
     for (int li = 1; li < 8; ++li) {

@@ -90,13 +90,9 @@ __global__ void __launch_bounds__(kThreads)
         uint32_t hw[4], lw[4];
 #pragma unroll
         for (int j = 0; j < 8; j += 2) {
-          __half h0, l0, h1, l1;
           const float a0 = o[j] * oscale, a1 = o[j + 1] * oscale;
           mx = max(mx, max(tc::range_bits(a0), tc::range_bits(a1)));
-          tc::split_f16(a0, h0, l0);
-          tc::split_f16(a1, h1, l1);
-          hw[j / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-          lw[j / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+          tc::split_f16x2(a0, a1, hw[j / 2], lw[j / 2]);
         }
         *reinterpret_cast<uint4*>(yh16 + idx) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         *reinterpret_cast<uint4*>(yl16 + idx) = make_uint4(lw[0], lw[1], lw[2], lw[3]);

@@ -315,6 +315,19 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
   lo = __float2half_rn(__fsub_rn(x, __half2float(hi)));
 }
 
+// Two values at once, packed (hw = hi(a0) | hi(a1) << 16, lw likewise): the
+// packed conversion (F2FP.F16.F32.PACK_AB, an ALU-rate instruction) replaces
+// four scalar F2F.F16.F32 (conversion-unit rate, 16 lanes/clk/SM), which bound
+// the epilogues of the mid-width layers.  Bit-identical to split_f16 per value
+// (both round to nearest even).
+__device__ __forceinline__ void split_f16x2(float a0, float a1, uint32_t& hw, uint32_t& lw) {
+  const __half2 h = __floats2half2_rn(a0, a1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(__fsub_rn(a0, hf.x), __fsub_rn(a1, hf.y));
+  hw = *reinterpret_cast<const uint32_t*>(&h);
+  lw = *reinterpret_cast<const uint32_t*>(&l);
+}
+
 // ---- FP16x3 range guard -------------------------------------------------------
 // Magnitude of a scaled operand value as ordered bits: for non-negative floats
 // the IEEE bit pattern orders like the value, and NaN (0x7FC00000+) sorts

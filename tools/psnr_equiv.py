@@ -27,7 +27,7 @@ import numpy as np
 BAR_DB = 0.1
 
 
-def load(paths, size=None):
+def load(paths, size=None, image="study"):
     rows = {}
     for p in paths:
         for line in open(p):
@@ -37,8 +37,24 @@ def load(paths, size=None):
             r = json.loads(line)
             if size is not None and r.get("size") != size:
                 continue
+            if r.get("image", "study") != image:
+                continue
             rows[(r["kind"], r["seed"])] = r
     return rows
+
+
+def load_r01_cpu(path, rows, size):
+    """CPU rows of a round-1 profile (tools/psnr_merge.py format): full fits of
+    the oracle port, which is bitwise the stock reference on one epoch with the
+    same BLAS (tests/golden).  Only seeds without a stock-reference row."""
+    n = 0
+    for r in json.load(open(path))["rows"]:
+        if "cpu_oracle" in r and ("cpu", r["seed"]) not in rows:
+            rows[("cpu", r["seed"])] = {"kind": "cpu", "seed": r["seed"], "size": size,
+                                        "psnr": r["cpu_oracle"], "psnr_noisy": r["psnr_noisy"],
+                                        "epochs": r["cpu_epochs"], "port": True}
+            n += 1
+    return n
 
 
 def t95(df: int) -> float:
@@ -71,6 +87,8 @@ def analyse(rows: dict) -> dict:
         if c is None:
             continue
         e = {"seed": s, "psnr_noisy": c["psnr_noisy"], "cpu": c["psnr"], "cpu_epochs": c["epochs"]}
+        if c.get("port"):
+            e["port"] = True
         g = rows.get(("gpu", s))
         if g is not None:
             e.update(gpu=g["psnr"], gpu_epochs=g["epochs"], gap_gpu=g["psnr"] - c["psnr"])
@@ -101,13 +119,23 @@ def main():
     ap.add_argument("--gpu", nargs="+", required=True)
     ap.add_argument("--cpu", nargs="+", required=True)
     ap.add_argument("--size", type=int, default=128)
+    ap.add_argument("--image", default="study", choices=["study", "config1"])
+    ap.add_argument("--r01-cpu", default=None,
+                    help="round-1 profile whose oracle-port CPU fits fill seeds without a stock-reference row")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
-    rows = load(args.gpu + args.cpu, args.size)
+    if args.image == "config1":
+        args.size = 256
+    rows = load(args.gpu + args.cpu, args.size, args.image)
+    n_port = load_r01_cpu(args.r01_cpu, rows, args.size) if args.r01_cpu else 0
     summary, per = analyse(rows)
-    doc = {"what": f"full default fit-and-denoise PSNR at {args.size}^2 (blob+rect, sigma 25/255, clean "
-                   "seed 100+s, noise seed 200+s, TrainConfig(seed=s)); cpu = stock reference "
-                   "(baseline/_ref noise2fast, 1 BLAS thread), cpu2 = stock reference with 1e-7 "
+    summary["cpu_rows_from_oracle_port"] = n_port
+    images = ("BASELINE config-1 images (256^2, sigma 25/255, image seed = fit seed s)"
+              if args.image == "config1" else
+              f"{args.size}^2 blob+rect, sigma 25/255, clean seed 100+s, noise seed 200+s")
+    doc = {"what": f"full default fit-and-denoise PSNR, {images}, TrainConfig(seed=s); cpu = stock reference "
+                   "(noise2fast from /root/reference, 1-2 BLAS threads; rows marked port = the "
+                   "oracle port's round-1 fits), cpu2 = stock reference with 1e-7 "
                    "relative init noise, gpu = this engine; tools/psnr_equiv.py",
            "summary": summary, "rows": per}
     print(json.dumps(summary, indent=1))
