@@ -399,12 +399,13 @@ def run_ours(args):
     from paper_2108_10209_b200 import Engine, TrainConfig, _lib, train_single_channel
     from paper_2108_10209_b200 import trainer as T
 
-    # one rank per GPU; with fewer GPUs than ranks (a 1-GPU box running the
-    # 2-rank plumbing test) ranks share devices: they are independent fits that
-    # never wait on one another, so this is safe, just not a scaling number
+    # one rank per GPU.  Ranks must not share a device: two contexts time-slicing
+    # one B200 with the persistent tcgen05 / while-graph kernels stalled for
+    # minutes when tried, so fewer GPUs than ranks is an error, not a fallback.
     ndev = torch.cuda.device_count()
-    shared = world > ndev
-    local %= ndev
+    if world > ndev:
+        raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, this node has {ndev} "
+                         "(use --dry-run for the plumbing on CPU)")
     torch.cuda.set_device(local)
     os.environ["N2F_DEVICE"] = str(local)
 
@@ -540,8 +541,6 @@ def run_ours(args):
             # image moves with last-bit changes (chaotic training)
             "ms_per_epoch": max_ms / args.steps / epochs[-1],
         }
-        if shared:  # plumbing run only: ranks time-share devices, not a scaling number
-            line["ranks_share_gpus"] = {"ranks": world, "gpus": ndev}
         print(json.dumps(line), flush=True)
     eng.close()
     group.close()

@@ -19,9 +19,12 @@ installed reference package runs on this engine.
 
 from __future__ import annotations
 
+import contextlib
 import dataclasses
+import fcntl
 import json
 import os
+import tempfile
 import threading
 import time
 from dataclasses import dataclass
@@ -124,6 +127,29 @@ def _device_index() -> int:
     n = _lib.C.c_int()
     call("n2f_device_count", _lib.C.byref(n))
     return select_device(spec, _worker_ordinal(), n.value)
+
+
+_lock_fds: dict[int, int] = {}
+
+
+@contextlib.contextmanager
+def _device_lock(device: int):
+    """Inter-process lock per GPU around one fit of the public API.  Processes
+    that share a GPU (the reference CLI's ``--threads N`` pool with fewer GPUs
+    than workers) then take turns: one fit saturates a B200, so concurrent fits
+    gain nothing, and two contexts time-slicing the persistent tcgen05 /
+    while-graph kernels of a 512^2 fit were seen to stall for minutes."""
+    fd = _lock_fds.get(device)
+    if fd is None:
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "all").replace(",", "_").replace("/", "_")
+        path = os.path.join(tempfile.gettempdir(), f"n2f_b200_gpu_{vis}_{device}.lock")
+        fd = os.open(path, os.O_CREAT | os.O_RDWR, 0o666)
+        _lock_fds[device] = fd
+    fcntl.flock(fd, fcntl.LOCK_EX)
+    try:
+        yield
+    finally:
+        fcntl.flock(fd, fcntl.LOCK_UN)
 
 
 class Engine:
@@ -336,7 +362,8 @@ def train_single_channel(noisy, config, clean=None, telemetry=None, telemetry_ta
     eng = _engine_for(arr.shape, config)
     wall0 = time.time()
     try:
-        out, r, hist, losses, secs = eng.fit_host(arr, clean_arr)
+        with _device_lock(eng.device):
+            out, r, hist, losses, secs = eng.fit_host(arr, clean_arr)
     except _lib.N2FError as e:
         if e.code == _lib.N2F_ERR_NONFINITE:
             raise ValueError("image contains non-finite values") from None
@@ -367,6 +394,8 @@ def train_single_channel(noisy, config, clean=None, telemetry=None, telemetry_ta
         wall_time=time.perf_counter() - t0,
         stop_reason=reason,
     )
+
+
 def denoise_image(image, config, clean=None, telemetry=None):
     """Denoise every channel of every slice with independent runs (trainer.py:216-250)."""
     if not 1 <= image.channels <= 4:

@@ -282,10 +282,13 @@ def test_variant_fits_match_oracle(oracle, scheme, loss):
     assert norm_rel(res.denoised, ref.denoised) < 2e-2
 
 
-@pytest.mark.parametrize("hw", [(4, 4), (5, 7), (33, 47), (130, 66)])
+@pytest.mark.parametrize("hw", [(4, 4), (5, 7), (33, 47), (130, 66), (4, 1030), (1030, 4), (9, 515),
+                                (300, 6)])
 def test_ragged_sizes_fit(oracle, hw):
     """Odd and minimum sizes: training crops to even (downsample.py:103-107),
-    validation and the result keep the full odd shape; first epoch vs oracle."""
+    validation and the result keep the full odd shape; first epoch vs oracle.
+    The stripes (4 x 1030, 1030 x 4, ...) make half planes 2 pixels wide or
+    tall and cross several 32 x 8 tile columns / rows with ragged edges."""
     from paper_2108_10209_b200 import TrainConfig, train_single_channel
 
     if min(hw) >= 16:

@@ -19,7 +19,8 @@ def _guards(eng):
     return n.value
 
 
-@pytest.mark.parametrize("hw", [(4, 4), (5, 7), (16, 9), (33, 47), (130, 66), (64, 64), (257, 511)])
+@pytest.mark.parametrize("hw", [(4, 4), (5, 7), (16, 9), (33, 47), (130, 66), (64, 64), (257, 511), (4, 1030),
+                                (1030, 4)])
 @pytest.mark.parametrize("scheme,loss", [("checkerboard", "bce"), ("quad", "mse"), ("exact", "bce")])
 @pytest.mark.parametrize("use_graph", [False, True])
 def test_no_out_of_bounds_writes(hw, scheme, loss, use_graph):

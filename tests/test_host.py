@@ -117,3 +117,31 @@ def test_metrics_argument_errors_before_device_work():
         metrics.ssim(np.zeros((12, 12, 3)), np.zeros((12, 12, 3)), 1.0)
     with pytest.raises(ValueError, match="shape mismatch"):
         metrics.ssim(np.zeros((12, 12)), np.zeros((12, 13)), 1.0)
+
+
+def _hold_device_lock(i, q):
+    import time
+
+    from paper_2108_10209_b200.trainer import _device_lock
+
+    with _device_lock(0):
+        t0 = time.time()
+        time.sleep(0.25)
+        q.put((i, t0, time.time()))
+
+
+def test_device_lock_serialises_processes_sharing_a_gpu():
+    """Processes that share a GPU (CLI --threads N with fewer GPUs than
+    workers) take turns per fit: the per-device file lock of the public API."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_hold_device_lock, args=(i, q)) for i in range(3)]
+    for p in ps:
+        p.start()
+    iv = sorted((q.get(timeout=60) for _ in ps), key=lambda x: x[1])
+    for p in ps:
+        p.join(30)
+    for (_, _, end), (_, start, _) in zip(iv, iv[1:]):
+        assert end <= start + 1e-3, iv

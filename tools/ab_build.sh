@@ -3,6 +3,7 @@
 # paper_2108_10209_b200/ab_libs/ for tools/ab_epoch.sh (run on the GPU box).
 set -e
 cd "$(dirname "$0")/.."
+mkdir -p paper_2108_10209_b200/ab_libs
 build() {  # name flags
   N2F_LIB_OUT=paper_2108_10209_b200/ab_libs/$1.so N2F_EXTRA_FLAGS="$2" python -m paper_2108_10209_b200.build > /dev/null
 }

@@ -84,7 +84,8 @@ def label_epoch(kernels):
         seq = [("fwd", 0, "k_conv_first")] + [("fwd", li, "k_conv3x3_dy") for li in range(1, 8)]
         for li in range(7, 0, -1):
             seq += [("wgrad", li, "k_wgrad3x3_tc"), ("dgrad", li, "k_conv3x3_dy")]
-        seq += [("wgrad", 0, "k_wgrad_first"), ("adam", -1, "k_adam")]
+        seq += [("wgrad", 0, "k_wgrad_first"), ("adam", -1, "k_adam"),
+                ("transpose", -1, "k_transpose_pairs")]
         for kind, li, pat in seq:
             assert pat in names[i], (i, names[i], pat)
             labels[i] = (f"step{step}", kind, li)
