@@ -10,7 +10,8 @@ tools/psnr_equiv_cpu.py and is committed as tests/golden/psnr_reference_fits.jso
 with the same TrainConfig and the paired gaps are tested:
 
   * the images are the same (noisy-image PSNR equal to 1e-9 dB);
-  * every fit denoises (> +3 dB) and stops by patience;
+  * every fit denoises (> +1 dB; the reference itself gains only +2.9 dB on
+    the hardest 64^2 image) and stops by patience;
   * no single gap beyond 3.5 dB (the reference's own chaos partner stays
     within ~1.3 dB; the largest GPU gap measured is 2.1 dB);
   * per image size the mean gap is inside +-0.1 dB;
@@ -56,7 +57,7 @@ def _fit_gaps(key, fits):
         assert abs(p_in - ref["psnr_noisy"]) < 1e-9, (key, seed, p_in, ref["psnr_noisy"])
         r = train_single_channel(noisy, TrainConfig(seed=seed))
         p = _psnr(r.denoised, clean)
-        assert r.stop_reason == "patience" and p > p_in + 3.0, (key, seed, p, r.stop_reason)
+        assert r.stop_reason == "patience" and p > p_in + 1.0, (key, seed, p, r.stop_reason)
         assert abs(p - ref["psnr"]) <= 3.5, (key, seed, p, ref["psnr"], r.epochs_run, ref["epochs"])
         gaps.append(p - ref["psnr"])
     return np.asarray(gaps)
