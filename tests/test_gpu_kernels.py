@@ -136,6 +136,55 @@ def test_conv_backward(lib, oracle, cin, cout, k, hw):
         np.testing.assert_allclose(dx, dx_ref, rtol=0, atol=1e-5 * np.abs(dx_ref).max())
 
 
+def _random_conv_cases(n, seed):
+    """Seeded random (layer shape, image size) cases in the spirit of the
+    reference's 200-shape acceptance sweep (test_acceptance.py:183-229): every
+    layer shape of the network over ragged sizes from 1 pixel to a few tile
+    rows / columns, including 1 x W and H x 1 planes."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        cin, cout, k = CONV_SHAPES[i % len(CONV_SHAPES)]
+        h, w = int(rng.integers(1, 41)), int(rng.integers(1, 71))
+        if i % 7 == 0:
+            h = 1
+        if i % 11 == 0:
+            w = 1
+        cases.append((cin, cout, k, h, w))
+    return cases
+
+
+@pytest.mark.parametrize("cin,cout,k,h,w", _random_conv_cases(45, 2108))
+def test_conv_forward_backward_random_shapes(lib, oracle, cin, cout, k, h, w):
+    rng = np.random.default_rng(cin * 31 + cout * 7 + h * 131 + w)
+    x = np.maximum(rng.standard_normal((cin, h, w)), 0).astype(np.float32)
+    wt = (rng.standard_normal((cout, cin, k, k)) / np.sqrt(cin * k * k)).astype(np.float32)
+    b = rng.standard_normal(cout).astype(np.float32)
+    g = rng.standard_normal((cout, h, w)).astype(np.float32)
+    P = h * w
+    d_x, d_w, d_b, d_g = dev(chw_to_hwc(x)), dev(oihw_to_engine(wt)), dev(b), dev(chw_to_hwc(g))
+    y = empty(P * cout)
+    _call(lib, "n2f_conv_fwd", d_x.data_ptr(), d_w.data_ptr(), d_b.data_ptr(), y.data_ptr(),
+          h, w, cin, cout, k, 1, IMPL, None)
+    ref = np.maximum(oracle.conv_forward(x, wt, b), 0)
+    got = hwc_to_chw(host(y).reshape(h, w, cout))
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-5 * max(np.abs(ref).max(), 1e-3))
+    dx_ref, dw_ref, db_ref = oracle.conv_backward(g, x, wt, need_dx=True)
+    dx_ref = dx_ref * (x > 0)
+    need_dx = cin > 1
+    d_dw, d_db = empty(wt.size), empty(cout)
+    d_dx = empty(P * cin) if need_dx else None
+    _call(lib, "n2f_conv_bwd", d_g.data_ptr(), d_x.data_ptr(), d_w.data_ptr(),
+          d_x.data_ptr() if need_dx else None, d_dx.data_ptr() if need_dx else None,
+          d_dw.data_ptr(), d_db.data_ptr(), h, w, cin, cout, k, IMPL, None)
+    dw = engine_to_oihw(host(d_dw), cout, cin, k)
+    np.testing.assert_allclose(dw, dw_ref, rtol=0, atol=1e-5 * max(np.abs(dw_ref).max(), 1e-3))
+    np.testing.assert_allclose(host(d_db), db_ref, rtol=0, atol=1e-5 * max(np.abs(db_ref).max(), 1e-3))
+    if need_dx:
+        dx = hwc_to_chw(host(d_dx).reshape(h, w, cin))
+        np.testing.assert_allclose(dx, dx_ref, rtol=0, atol=1e-5 * max(np.abs(dx_ref).max(), 1e-3))
+
+
 @pytest.mark.parametrize("loss", [0, 1])
 def test_loss(lib, oracle, loss):
     rng = np.random.default_rng(5 + loss)
