@@ -95,10 +95,18 @@ def analyse(rows: dict) -> dict:
         c2 = rows.get(("cpu2", s))
         if c2 is not None:
             e.update(cpu2=c2["psnr"], cpu2_epochs=c2["epochs"], gap_cpu=c2["psnr"] - c["psnr"])
+        g2 = rows.get(("gpu2", s))
+        if g is not None and g2 is not None:
+            e.update(gpu2=g2["psnr"], gpu2_epochs=g2["epochs"], gap_gpu2=g2["psnr"] - g["psnr"])
         per.append(e)
     gg = np.array([e["gap_gpu"] for e in per if "gap_gpu" in e])
     gc = np.array([e["gap_cpu"] for e in per if "gap_cpu" in e])
-    out = {"bar_db": BAR_DB, "gap_gpu_minus_cpu": describe(gg), "gap_cpu2_minus_cpu": describe(gc)}
+    # the engine against itself (kind gpu2: last-bit perturbed input), over every seed that has both
+    # GPU fits, with or without a CPU row
+    g2all = np.array([rows[("gpu2", s)]["psnr"] - rows[("gpu", s)]["psnr"]
+                      for (k, s) in rows if k == "gpu2" and ("gpu", s) in rows])
+    out = {"bar_db": BAR_DB, "gap_gpu_minus_cpu": describe(gg), "gap_cpu2_minus_cpu": describe(gc),
+           "gap_gpu2_minus_gpu": describe(g2all)}
     if len(gg) > 1 and len(gc) > 1:
         try:
             from scipy import stats
@@ -136,7 +144,8 @@ def main():
     doc = {"what": f"full default fit-and-denoise PSNR, {images}, TrainConfig(seed=s); cpu = stock reference "
                    "(noise2fast from /root/reference, 1-2 BLAS threads; rows marked port = the "
                    "oracle port's round-1 fits), cpu2 = stock reference with 1e-7 "
-                   "relative init noise, gpu = this engine; tools/psnr_equiv.py",
+                   "relative init noise, gpu = this engine, gpu2 = this engine on the image times "
+                   "(1 + N(0, 1e-7)) per pixel; tools/psnr_equiv.py",
            "summary": summary, "rows": per}
     print(json.dumps(summary, indent=1))
     if args.out:

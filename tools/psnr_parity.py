@@ -38,6 +38,10 @@ def main():
     ap.add_argument("--sigma", type=float, default=25.0)
     ap.add_argument("--out", default=None)
     ap.add_argument("--image", default="study", choices=["study", "config1"])
+    ap.add_argument("--perturb", type=float, default=0.0,
+                    help="kind gpu2: the engine's own chaos partner, the same fit of the image "
+                         "multiplied by (1 + N(0, perturb)) per pixel (1e-7: last-bit changes of the "
+                         "normalised float32 image); PSNR is still taken against the clean image")
     args = ap.parse_args()
     sink = open(args.out, "a") if args.out else None
     for s in parse_seeds(args.seeds):
@@ -47,9 +51,11 @@ def main():
         else:
             clean = synthetic.blob_rect_image(args.size, args.size, 100 + s)
             noisy = synthetic.gaussian_noisy(clean, args.sigma / 255, 200 + s).astype(np.float64)
+        if args.perturb > 0:
+            noisy = noisy * (1 + np.random.default_rng(10_000 + s).normal(0, args.perturb, noisy.shape))
         t = time.time()
         r = train_single_channel(noisy, TrainConfig(seed=s))
-        row = {"kind": "gpu", "seed": s, "size": args.size, "image": args.image, "psnr": float(psnr(r.denoised, clean)),
+        row = {"kind": "gpu2" if args.perturb > 0 else "gpu", "seed": s, "size": args.size, "image": args.image, "psnr": float(psnr(r.denoised, clean)),
                "psnr_noisy": float(psnr(noisy, clean)), "epochs": r.epochs_run,
                "stop": r.stop_reason, "s": time.time() - t}
         print(json.dumps(row), flush=True)

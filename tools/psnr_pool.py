@@ -35,7 +35,8 @@ def main():
                        "max_abs_db": float(np.abs(g).max()),
                        "chaos_n": int(len(c)), "chaos_sd_db": float(c.std(ddof=1)) if len(c) > 1 else None,
                        "chaos_mean_db": float(c.mean()) if len(c) else None,
-                       "chaos_max_abs_db": float(np.abs(c).max()) if len(c) else None})
+                       "chaos_max_abs_db": float(np.abs(c).max()) if len(c) else None,
+                       "gpu_self_chaos": d["summary"].get("gap_gpu2_minus_gpu")})
         all_gaps.append(g)
         all_chaos.append(c)
     w = np.array([1.0 / s["se_db"] ** 2 for s in strata])
